@@ -1,0 +1,388 @@
+#!/usr/bin/env python
+"""Benchmark of the student-group hot path (BASELINE.json metric and configs).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl engine|reference] [--config base]
+
+A step is ONE batch-1 request of the BERT-base-sized 8-student group (BASELINE.json configs[1]:
+K=8, H=768, 12 heads, 2 layers, ragged L ~ U{16..512}): token ids -> all students -> boosting sum
+-> logits. With N GPUs (torchrun) the same group is sharded K/N students per GPU (round-robin,
+servesim.py:231) with one NCCL all-reduce of the fp32 logits per request ("strong" scaling: the
+total work per request is fixed). L2 is flushed (256 MiB write) before every timed request, so the
+weights stream from HBM even when a shard fits in the 126 MB L2.
+
+value = requests/s over the K timed requests (device time, CUDA events, max over ranks);
+p50_ms/p99_ms = nearest-rank percentiles (servesim.py:370-376) of the per-request latency.
+e2e = the same metric through the public API with host buffers (pinned ids in, logits out).
+--impl reference times the float64 CPU port of the path (oracle/, the reference is pure Python and
+has no BERT student) on the host cores, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "p50/p99 request latency (ms) at batch-1 and req/s for K-student group"
+UNIT = "req/s"
+L2_FLUSH_BYTES = 256 << 20
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1000)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", choices=["engine", "reference"], default="engine")
+    ap.add_argument("--config", default="base", choices=["tiny", "base", "large", "k32"])
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--len-min", type=int, default=16)
+    ap.add_argument("--len-max", type=int, default=512)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0, help="bounded CPU-baseline sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-steps", type=int, default=200)
+    return ap.parse_args()
+
+
+def nearest_rank(values, pct):
+    """servesim.nearest_rank_percentile (servesim.py:370-376)."""
+    ordered = sorted(values)
+    rank = max(1, math.ceil(pct / 100.0 * len(ordered)))
+    return ordered[rank - 1]
+
+
+def make_requests(n, seed, lo, hi, vocab):
+    from paper_2408_12526_b200.seeding import rng_for
+
+    rng = rng_for(seed, "bench-requests")
+    lens = rng.integers(lo, hi + 1, size=n)
+    reqs = []
+    for L in lens:
+        ids = rng.integers(1000, vocab, size=int(L)).astype(np.int32)
+        ids[0] = 101  # [CLS]
+        reqs.append(ids)
+    return reqs
+
+
+def workload_config(args, cfg, K, world):
+    return {
+        "workload": f"{args.config}: K={K} BERT-style 2-layer students, H={cfg.hidden}, {cfg.n_heads} heads, "
+                    f"F={cfg.ffn}, batch-1 ragged L~U{{{args.len_min}..{args.len_max}}}, random-init",
+        "model": "student group (boosting sum of K flat BERT-style students)",
+        "K": K, "hidden": cfg.hidden, "heads": cfg.n_heads, "layers": cfg.n_layers, "ffn": cfg.ffn,
+        "global_batch": 1, "seq_len": [args.len_min, args.len_max], "k_active": K,
+        "students_per_gpu": [len(s) for s in __import__("paper_2408_12526_b200.parallel", fromlist=["x"]).placement(K, world)],
+        "parallelism": f"student-parallel x{world}" if world > 1 else "single GPU",
+        "l2": "flushed: 256 MiB write before every timed request",
+    }
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- CPU port
+def cpu_port_sample(weights, reqs, seconds, max_samples=None):
+    """Time the float64 oracle port (oracle/bert.py) one (request, student) pair at a time.
+
+    Students are independent and identical in cost, so K x (mean per-student time) + the head is
+    the per-request cost; returns (req/s, samples, seconds)."""
+    from oracle.bert import OracleBertGroup  # the CPU baseline is the checker, timed, never shipped
+
+    orc = OracleBertGroup(weights)
+    K = orc.n_students
+    for m in range(K):  # f64 weight copies are resident before timing (like the reference's arrays)
+        orc.student(m)
+    times = []
+    t_start = time.perf_counter()
+    i = 0
+    while True:
+        ids = reqs[i % len(reqs)]
+        m = i % K
+        t0 = time.perf_counter()
+        orc.pooled(m, [ids])
+        times.append(time.perf_counter() - t0)
+        i += 1
+        if max_samples is not None and i >= max_samples:
+            break
+        if max_samples is None and time.perf_counter() - t_start >= seconds:
+            break
+    per_req = K * float(np.mean(times))
+    return 1.0 / per_req, len(times), float(np.sum(times))
+
+
+def host_cores():
+    return len(os.sched_getaffinity(0))
+
+
+# ----------------------------------------------------------------------------- reference arm
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from paper_2408_12526_b200 import PRESETS, random_bert_group
+
+    cfg, K = PRESETS[args.config]
+    weights = random_bert_group(cfg, K, seed=args.seed)
+    reqs = make_requests(max(64, args.steps + args.warmup), args.seed, args.len_min, args.len_max, cfg.vocab)
+    cpu_port_sample(weights, reqs, 0.0, max_samples=max(1, args.warmup))
+    t0 = time.perf_counter()
+    value, n, busy = cpu_port_sample(weights, reqs[args.warmup:] + reqs[: args.warmup], 0.0, max_samples=args.steps)
+    wall = time.perf_counter() - t0
+    cores = host_cores()
+    sample = (f"{n} (request, student) forwards of the {args.config} group (L~U{{{args.len_min}..{args.len_max}}}), "
+              f"float64 numpy/OpenBLAS port (oracle/bert.py); req/s = 1 / (K x mean student time)")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * busy / max(n, 1),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(args, cfg, K, 1),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "wall_s": wall,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- engine arm
+def run_engine(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    from paper_2408_12526_b200 import PRESETS
+    from paper_2408_12526_b200._lib import GEMM_KINDS, LAUNCH_KINDS  # noqa: F401
+    from paper_2408_12526_b200.parallel import ShardedStudentGroup
+
+    cfg, K = PRESETS[args.config]
+    dev = torch.device("cuda", local_rank)
+    grp = ShardedStudentGroup(cfg, K, seed=args.seed, rank=rank, world=world, device=local_rank,
+                              max_tokens=args.len_max, max_seqs=1)
+    n_req = args.steps + args.warmup
+    reqs = make_requests(n_req, args.seed, args.len_min, args.len_max, cfg.vocab)
+    # inputs resident in HBM before the timed region
+    lens = np.array([len(r) for r in reqs], np.int64)
+    offs = np.concatenate([[0], np.cumsum(lens)])
+    ids_all = torch.from_numpy(np.concatenate(reqs).astype(np.int32)).to(dev)
+    cu_all = torch.from_numpy(np.stack([np.zeros(n_req, np.int32), lens.astype(np.int32)], 1).copy()).to(dev)
+    logits = torch.empty((1, cfg.n_classes), dtype=torch.float32, device=dev)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+
+    def step(i):
+        L = int(lens[i])
+        grp.forward_packed_device(ids_all[offs[i]: offs[i] + L], cu_all[i], 1, L, L, K, logits)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for i in range(args.warmup):
+        flush.zero_()
+        step(i)
+    barrier()
+    launches_per_step = grp.local.last_launches
+
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    clocks = ClockSampler(torch.cuda.current_device()) if rank == 0 else None
+    if clocks:
+        clocks.start()
+    barrier()
+    for j in range(args.steps):
+        i = args.warmup + j
+        flush.fill_(float(j & 1))
+        starts[j].record()
+        step(i)
+        ends[j].record()
+    barrier()
+    clock_info = clocks.stop() if clocks else None
+    step_ms = torch.tensor([s.elapsed_time(e) for s, e in zip(starts, ends)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(step_ms, op=dist.ReduceOp.MAX)
+    step_ms = step_ms.cpu().numpy()
+    total_s = float(step_ms.sum()) / 1e3
+    value = args.steps / total_s
+
+    # ---- roofline: per-launch CUDA events on an instrumented replay of the timed requests
+    grp.local.set_profiling(True)
+    agg: dict[str, list[float]] = {}
+    n_prof = min(args.profile_steps, args.steps)
+    step_total_ms = 0.0
+    for j in range(n_prof):
+        i = args.warmup + j
+        flush.zero_()
+        step(i)
+        recs = grp.local.profile_records()
+        for r in recs:
+            a = agg.setdefault(r["kind"], [0.0, 0.0, 0.0, 0])
+            a[0] += r["ms"]
+            a[1] += r["bytes"]
+            a[2] += r["flops"]
+            a[3] += 1
+        step_total_ms += sum(r["ms"] for r in recs)
+    grp.local.set_profiling(False)
+    peaks = {}
+    try:
+        peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+        hbm_peak, peak_src = float(peaks["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (measured)"
+        tc_peak = float(peaks["bf16_tflops"])
+    except Exception:
+        hbm_peak, peak_src, tc_peak = 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)", 1590.0
+    gemm_names = [LAUNCH_KINDS[k] for k in sorted(GEMM_KINDS)]
+    g_ms = sum(agg[k][0] for k in gemm_names if k in agg)
+    g_bytes = sum(agg[k][1] for k in gemm_names if k in agg)
+    g_flops = sum(agg[k][2] for k in gemm_names if k in agg)
+    g_launches = sum(agg[k][3] for k in gemm_names if k in agg)
+    achieved = g_bytes / (g_ms / 1e3) / 1e9 if g_ms > 0 else 0.0
+    traffic = None
+    tfile = ROOT / "profiles" / "gemm_dram_traffic.json"
+    if tfile.exists():
+        try:
+            traffic = json.loads(tfile.read_text()).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    roofline = {
+        "bound": "hbm", "kernel": "gemm_kernel (tcgen05 grouped projection: QKV/O/FFN1/FFN2/pooler)",
+        "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
+        "traffic": traffic, "peak_source": peak_src,
+        "algorithmic_bytes_per_launch": g_bytes / max(g_launches, 1),
+        "avg_launch_us": 1e3 * g_ms / max(g_launches, 1),
+        "tensor_tflops": g_flops / (g_ms / 1e3) / 1e12 if g_ms > 0 else 0.0, "tensor_peak_tflops": tc_peak,
+        "gemm_share_of_step": g_ms / step_total_ms if step_total_ms else None,
+        "method": f"CUDA events around every launch on the launching stream, instrumented replay of {n_prof} timed requests",
+        "per_kind_ms_per_request": {k: v[0] / n_prof for k, v in sorted(agg.items())},
+    }
+    # request-level roofline: all weight bytes of a request vs its latency
+    w_bytes = grp.local.weights  # local weights (host copy)
+    req_bytes_local = sum(getattr(w_bytes, n).nbytes for n in
+                          ["w_qkv", "w_o", "w_ffn1", "w_ffn2", "w_pool", "b_qkv", "b_o", "b_ffn1", "b_ffn2", "b_pool"])
+    roofline["request_weight_bytes_per_gpu"] = req_bytes_local
+    roofline["request_hbm_frac_p50"] = (req_bytes_local / (nearest_rank(step_ms, 50) / 1e3) / 1e9) / hbm_peak
+
+    # ---- e2e through the public API with host buffers
+    pinned_ids = [torch.from_numpy(r).pin_memory() for r in reqs]
+    pinned_cu = [torch.tensor([0, len(r)], dtype=torch.int32).pin_memory() for r in reqs]
+    e2e_s = []
+    barrier()
+    for j in range(args.steps):
+        i = args.warmup + j
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        if world == 1:
+            grp.local.forward_host(pinned_ids[i].numpy(), pinned_cu[i].numpy(), K)
+        else:
+            grp.forward_host(pinned_ids[i].numpy(), pinned_cu[i].numpy(), K)
+        e2e_s.append(time.perf_counter() - t0)
+    e2e_t = torch.tensor(e2e_s, dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+    e2e_s = e2e_t.cpu().numpy()
+    e2e = {"value": args.steps / float(e2e_s.sum()), "unit": UNIT,
+           "h2d_bytes_per_step": float(np.mean([4 * (len(r) + 2) for r in reqs[args.warmup:]])),
+           "d2h_bytes_per_step": 4 * cfg.n_classes,
+           "p50_ms": 1e3 * nearest_rank(e2e_s, 50), "p99_ms": 1e3 * nearest_rank(e2e_s, 99),
+           "api": "StudentGroup.forward_host (C ABI sp_group_forward_host)" if world == 1 else
+                  "ShardedStudentGroup.forward_host (pinned H2D, engine, NCCL all-reduce, D2H)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, n, busy = cpu_port_sample(grp.local.weights, reqs, args.cpu_seconds)
+        cpu = {"value": v, "unit": UNIT, "cores": host_cores(), "kind": "port",
+               "sample": f"{n} (request, student) float64 forwards of this workload in {busy:.1f} s "
+                         f"(oracle/bert.py, numpy/OpenBLAS, all {host_cores()} host threads); "
+                         f"req/s = 1/(K x mean student time)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * total_s / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "fp16", "data": "synthetic",
+            "config": workload_config(args, cfg, K, world),
+            "p50_ms": nearest_rank(step_ms, 50), "p99_ms": nearest_rank(step_ms, 99),
+            "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clock_info,
+            "gpu_launches": launches_per_step * args.steps,
+            "launches_per_request": launches_per_step,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_engine(args)
+
+
+if __name__ == "__main__":
+    main()

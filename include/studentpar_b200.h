@@ -1,0 +1,169 @@
+/* studentpar_b200.h — C ABI of the B200 student-group inference engine.
+ *
+ * The reference (arXiv 2408.12526 artifact, /root/reference/pkg/src/studentpar) is pure Python; its
+ * hot path sits behind a Python object API, not an FFI. Each entry point below replaces one piece of
+ * that API; the Python host (paper_2408_12526_b200/group.py) binds them with ctypes exactly as a
+ * reference maintainer would (INTEGRATION.md shows the binding).
+ *
+ *   sp_group_create        <- EnsembleState(students, multipliers, classifier)   distill.py:147-154
+ *                             (students from StudentModel.build nnkernel.py:270-274 or
+ *                              load_ensemble distill.py:610-612); weights are packed ONCE (snapshot)
+ *   sp_group_forward       <- EnsembleState.rep(x, k) + classifier.forward(rep)  distill.py:169-178, :512
+ *                             (BERT-kind students: token ids + cu_seqlens, device buffers)
+ *   sp_group_forward_dense <- the same for the reference's dense StudentModel      nnkernel.py:289-301
+ *   sp_group_forward_host  <- the same call with HOST buffers (ids in, logits out), the serving seam
+ *                             Simulation._dispatch -> service_time                 servesim.py:486, :287-307
+ *   sp_last_error          <- the ValueError / RuntimeError message the reference would raise
+ *
+ * Conventions: plain pointers and sizes only. "device" pointers are CUDA device addresses on the
+ * group's device; `stream` is a cudaStream_t (NULL = legacy default stream). Every call is
+ * re-entrant per stream for distinct groups (the reference forward is not: nnkernel.py:74).
+ * Return value: SP_OK or an SP_E* code; sp_last_error() then describes the failure.
+ */
+#ifndef STUDENTPAR_B200_H
+#define STUDENTPAR_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SP_ABI_VERSION 1
+
+enum sp_status {
+  SP_OK = 0,
+  SP_EINVAL = 1, /* argument error: the reference raises ValueError (distill.py:172-173, nnkernel.py:71-72) */
+  SP_ECUDA = 2,  /* CUDA launch/runtime failure: RuntimeError */
+  SP_ENOMEM = 3  /* device allocation failed */
+};
+
+enum sp_kind {
+  SP_KIND_DENSE = 0, /* reference StudentModel: tanh(input_proj) -> n_layers x tanh(H x H) (nnkernel.py:256-301) */
+  SP_KIND_BERT = 1   /* paper's BERT-style student: embeddings+LN -> n_layers post-LN encoder -> tanh pooler */
+};
+
+typedef struct sp_config {
+  int32_t kind;         /* enum sp_kind */
+  int32_t n_students;   /* students resident on this device (the local shard of the group) */
+  int32_t hidden;       /* H, multiple of 128 (dense kind: rep_dim zero-padded to 128) */
+  int32_t n_layers;     /* BERT: encoder layers; dense: H x H tanh layers after input_proj (>= 2) */
+  int32_t n_heads;      /* BERT: attention heads, head_dim = hidden / n_heads in {32, 64} */
+  int32_t ffn;          /* BERT: intermediate width F, multiple of 128 */
+  int32_t d_in;         /* dense: input width, multiple of 64 (zero-padded) */
+  int32_t vocab;        /* BERT: word-embedding rows */
+  int32_t max_pos;      /* BERT: position-embedding rows = longest sequence */
+  int32_t n_classes;    /* classifier outputs C */
+  int32_t max_tokens;   /* capacity: packed tokens (BERT) or rows (dense) per call */
+  int32_t max_seqs;     /* capacity: sequences per call (BERT) */
+  float ln_eps;         /* LayerNorm epsilon (BERT) */
+} sp_config;
+
+/* Device pointers. Every per-student tensor is stacked over the local students on its leading
+ * axis (S = n_students); per-layer tensors are additionally stacked over layers: [n_layers][S]...
+ * Matrices are row-major (out, in) — the reference's DenseLayer.weight layout (nnkernel.py:73).
+ * fp16 = IEEE half, f32 = float. */
+typedef struct sp_weights {
+  /* BERT kind */
+  const void* word_emb;       /* fp16 [S][vocab][H] */
+  const void* pos_emb;        /* fp16 [S][max_pos][H] */
+  const void* type_emb;       /* fp16 [S][H]   (token type 0) */
+  const float* emb_ln_gamma;  /* f32 [S][H] */
+  const float* emb_ln_beta;   /* f32 [S][H] */
+  const void* w_qkv;          /* fp16 [n_layers][S][3H][H]  rows: Q | K | V */
+  const float* b_qkv;         /* f32  [n_layers][S][3H] */
+  const void* w_o;            /* fp16 [n_layers][S][H][H] */
+  const float* b_o;           /* f32  [n_layers][S][H] */
+  const float* ln1_gamma;     /* f32  [n_layers][S][H] */
+  const float* ln1_beta;
+  const void* w_ffn1;         /* fp16 [n_layers][S][F][H] */
+  const float* b_ffn1;        /* f32  [n_layers][S][F] */
+  const void* w_ffn2;         /* fp16 [n_layers][S][H][F] */
+  const float* b_ffn2;        /* f32  [n_layers][S][H] */
+  const float* ln2_gamma;     /* f32  [n_layers][S][H] */
+  const float* ln2_beta;
+  const void* w_pool;         /* fp16 [S][H][H]  pooler: tanh(W h_CLS + b) */
+  const float* b_pool;        /* f32  [S][H] */
+  /* dense kind */
+  const void* w_in;           /* fp16 [S][H][d_in]   input_proj (tanh) */
+  const float* b_in;          /* f32  [S][H] */
+  const void* w_layers;       /* fp16 [n_layers][S][H][H] (tanh) */
+  const float* b_layers;      /* f32  [n_layers][S][H] */
+  /* group head (both kinds) */
+  const float* alpha;         /* f32 [S]     boosting multipliers of the local students */
+  const float* w_cls;         /* f32 [C][H]  shared classifier (identity activation, distill.py:535) */
+  const float* b_cls;         /* f32 [C] */
+} sp_weights;
+
+typedef struct sp_group sp_group;
+
+int sp_abi_version(void);
+const char* sp_last_error(void);
+
+/* Allocate workspace on `device`, build TMA descriptors over the packed weights. The weight
+ * buffers are borrowed (not copied) and must outlive the group. */
+int sp_group_create(const sp_config* cfg, const sp_weights* weights, int device, sp_group** out);
+int sp_group_destroy(sp_group* group);
+
+/* BERT kind. ids: int32 [n_tokens] device; cu_seqlens: int32 [n_seqs + 1] device (cu[0] = 0,
+ * strictly increasing, cu[n_seqs] = n_tokens); max_seq_len = max_b (cu[b+1] - cu[b]).
+ * k_active: number of leading local students that take part (0 .. n_students; the host maps the
+ * reference's global prefix k, distill.py:171-173, to the local count).
+ * rep_out: f32 [n_seqs][H] or NULL — sum_{m<k} alpha_m * pooled_m (EnsembleState.rep).
+ * logits_out: f32 [n_seqs][C] — W_c rep (+ b_c iff add_bias; a multi-GPU shard passes 0 and the
+ * root adds the bias once after the reduce). */
+int sp_group_forward(sp_group* group, const int32_t* ids, const int32_t* cu_seqlens, int32_t n_seqs,
+                     int32_t n_tokens, int32_t max_seq_len, int32_t k_active, float* rep_out, float* logits_out,
+                     int32_t add_bias, void* stream);
+
+/* Dense kind: x fp16 [n_rows][d_in] device (one row per sample, shared by every student). */
+int sp_group_forward_dense(sp_group* group, const void* x, int32_t n_rows, int32_t k_active, float* rep_out,
+                           float* logits_out, int32_t add_bias, void* stream);
+
+/* BERT kind end to end with HOST buffers: validates ids/cu_seqlens like the reference validates its
+ * inputs, copies them to the device, runs the group, copies logits back and synchronizes `stream`. */
+int sp_group_forward_host(sp_group* group, const int32_t* ids, const int32_t* cu_seqlens, int32_t n_seqs,
+                          int32_t n_tokens, int32_t k_active, float* logits_out, int32_t add_bias, void* stream);
+
+/* Number of kernels the last forward call on this group launched. */
+int sp_group_last_launches(const sp_group* group);
+
+/* Per-launch profiling: when enabled, every kernel of a forward is bracketed by CUDA events on
+ * the call's stream (adds a few microseconds of host work per launch; off by default). */
+enum sp_launch_kind {
+  SP_LAUNCH_EMBED_LN = 1,
+  SP_LAUNCH_GEMM_QKV = 2,
+  SP_LAUNCH_ATTENTION = 3,
+  SP_LAUNCH_GEMM_O = 4,
+  SP_LAUNCH_REDUCE_LN = 5,
+  SP_LAUNCH_GEMM_FFN1 = 6,
+  SP_LAUNCH_GEMM_FFN2 = 7,
+  SP_LAUNCH_GEMM_POOL = 8,
+  SP_LAUNCH_HEAD = 9,
+  SP_LAUNCH_GEMM_DENSE = 10
+};
+
+typedef struct sp_launch_record {
+  int32_t kind;   /* enum sp_launch_kind */
+  float ms;       /* device duration (CUDA events) */
+  double bytes;   /* algorithmic HBM bytes: compulsory reads + writes of the launch */
+  double flops;   /* algorithmic flops */
+} sp_launch_record;
+
+int sp_group_set_profiling(sp_group* group, int enable);
+/* Waits for the last forward's events; fills up to max_records entries; returns the number of
+ * launches recorded (or a negative sp_status). */
+int sp_group_profile_read(sp_group* group, sp_launch_record* out, int max_records);
+
+/* Op-level entry points (single kernels, used by the per-kernel parity tests). */
+int sp_op_gemm(const void* w, const void* x, int32_t groups, int32_t n_out, int32_t k_dim, int32_t t_rows,
+               int32_t x_group_rows, int32_t x_rows_total, const float* bias, int32_t act, void* out,
+               int32_t out_f32, int32_t splits, void* stream);
+int sp_op_attention(const void* qkv, void* ctx, const int32_t* cu_seqlens, int32_t n_seqs, int32_t max_seq_len,
+                    int32_t groups, int32_t n_heads, int32_t head_dim, int32_t group_rows, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* STUDENTPAR_B200_H */

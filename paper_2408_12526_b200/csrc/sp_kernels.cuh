@@ -1,0 +1,74 @@
+// sp_kernels.cuh — launch wrappers for the student-group kernels (internal to the .so).
+#pragma once
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+namespace sp {
+
+enum Act : int { ACT_NONE = 0, ACT_TANH = 1, ACT_GELU = 2 };
+
+// One student-batched ("grouped") projection, swap-AB form:
+//   Y[g][t][n] = act( sum_k W[g][n][k] * X[g][t][k] + b[g][n] )     g < groups, t < t_rows, n < n_out
+// W: fp16 [groups * n_out, k_dim] (row = output feature, K-major — the reference's (out,in) layout,
+//    nnkernel.py:73). X: fp16 rows g * x_group_rows + t of a [rows, k_dim] tensor (x_group_rows = 0:
+//    every student reads the same input). With splits > 1, raw fp32 partial sums are written to
+//    out[split][g][t][n] and bias/act are applied by the consumer (split-K reduce kernel).
+struct GemmParams {
+  int n_out;        // multiple of 128
+  int k_dim;        // multiple of 64
+  int t_rows;       // valid rows per student
+  int x_group_rows; // X row stride between students
+  int bn;           // token tile, multiple of 16, <= 256
+  int n_tiles;
+  int m_tiles;
+  int splits;
+  int kb_per_split;
+  int stages;
+  void* out;
+  long long out_group_stride;  // elements
+  long long out_split_stride;  // elements
+  int out_ld;                  // elements between rows
+  const float* bias;           // [groups][n_out] or null
+  int bias_group_stride;
+  int act;
+  int out_f32;
+};
+
+struct GemmMaps {
+  CUtensorMap w;    // box {64, 128}
+  CUtensorMap x64;  // box {64, 64}
+  CUtensorMap x16;  // box {64, 16}
+};
+
+void launch_gemm(const GemmMaps& maps, const GemmParams& p, int groups, cudaStream_t stream);
+size_t gemm_smem_bytes(int bn, int stages);
+void gemm_configure_tiles(int t_rows, int* bn, int* n_tiles, int* stages);
+
+// Unpadded multi-head attention over cu_seqlens-packed sequences.
+//   qkv: fp16 [groups][x_group_rows][3H] (Q | K | V, head h at columns h*D within each third)
+//   ctx: fp16 [groups][x_group_rows][H]
+void launch_attention(const half* qkv, half* ctx, const int* cu_seqlens, int n_seqs, int max_len, int groups,
+                      int n_heads, int head_dim, int hidden, long long group_rows, cudaStream_t stream);
+
+// Embedding gather + LayerNorm: x = LN(E_word[g][id_t] + E_pos[g][pos_t] + E_type[g][0]).
+void launch_embed_ln(const int* ids, const int* cu_seqlens, int n_seqs, int n_tokens, int groups,
+                     const half* word, const half* pos, const half* type, long long word_gs, long long pos_gs,
+                     const float* gamma, const float* beta, int hidden, float eps, float* x32, half* x16,
+                     long long x_gs, cudaStream_t stream);
+
+// Split-K reduce + bias + residual + LayerNorm:
+//   x = LN(x + b + sum_s part[s]); optional CLS rows copied to cls16[g][seq].
+void launch_reduce_ln(const float* part, int splits, long long part_split_stride, const float* bias,
+                      const float* gamma, const float* beta, int hidden, float eps, float* x32, half* x16,
+                      long long x_gs, int n_tokens, int groups, const int* cu_seqlens, int n_seqs, half* cls16,
+                      long long cls_gs, cudaStream_t stream);
+
+// Boosting sum + shared classifier (distill.py:169-178, :512):
+//   rep[b] = sum_{m < groups} alpha[m] * final[m][b];  logits[b] = W_c rep[b] (+ b_c)
+void launch_head(const float* final_rep, long long final_gs, int groups, const float* alpha, const float* w_cls,
+                 const float* b_cls, int n_classes, int hidden, int n_rows, int add_bias, float* rep,
+                 float* logits, cudaStream_t stream);
+
+}  // namespace sp

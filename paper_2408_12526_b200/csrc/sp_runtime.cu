@@ -1,0 +1,568 @@
+// sp_runtime.cu — C-ABI runtime: group construction (weight snapshot + TMA descriptors + HBM
+// workspace) and the per-request launch sequence of the student-group forward.
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/studentpar_b200.h"
+#include "sp_kernels.cuh"
+
+namespace sp {
+bool rowops_supported_hidden(int hidden);
+}
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define SP_CUDA(expr)                                                                         \
+  do {                                                                                        \
+    cudaError_t _e = (expr);                                                                  \
+    if (_e != cudaSuccess) return fail(SP_ECUDA, "%s: %s", #expr, cudaGetErrorString(_e));   \
+  } while (0)
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (fn == nullptr) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// fp16 row-major [rows, cols] viewed as a 2-D tensor map with a {64, box_rows} box, 128-B swizzle.
+bool make_map(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+  auto fn = encode_fn();
+  if (fn == nullptr || ptr == nullptr || rows == 0) return false;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 2};
+  cuuint32_t box[2] = {64, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+struct XMaps {
+  CUtensorMap x64, x16;
+};
+
+bool make_xmaps(XMaps* m, const void* ptr, uint64_t rows, uint64_t cols) {
+  return make_map(&m->x64, ptr, rows, cols, 64) && make_map(&m->x16, ptr, rows, cols, 16);
+}
+
+int choose_splits(int units, int nkb, int smax) {
+  int best = 1;
+  for (int s = 1; s <= smax; ++s) {
+    if (nkb % s) continue;
+    if (s > 1 && nkb / s < 2) continue;
+    best = s;
+    if (units * s >= 128) break;
+  }
+  return best;
+}
+
+constexpr int kMaxSplits = 4;
+
+}  // namespace
+
+struct sp_group {
+  sp_config cfg;
+  sp_weights w;
+  int device = 0;
+  int rows_cap = 0;  // max(max_tokens, max_seqs)
+  // workspace
+  float* x32 = nullptr;    // [S][max_tokens][H] residual stream (fp32)
+  half* x16 = nullptr;     // [S][max_tokens][H] GEMM operand copy of x32
+  half* qkv = nullptr;     // [S][max_tokens][3H]
+  half* ctx = nullptr;     // [S][max_tokens][H]
+  half* ffn = nullptr;     // [S][max_tokens][F]
+  float* part = nullptr;   // [kMaxSplits][S][max_tokens][H] split-K partials
+  half* cls16 = nullptr;   // [S][max_seqs][H] CLS rows
+  float* final32 = nullptr;  // [S][rows_cap][H] per-student final representation
+  half* xin = nullptr;     // dense: [max_tokens][d_in] staged input (host API)
+  int32_t* d_ids = nullptr;
+  int32_t* d_cu = nullptr;
+  float* d_logits = nullptr;
+  std::vector<void*> allocs;
+  // tensor maps
+  std::vector<CUtensorMap> m_qkv, m_o, m_f1, m_f2, m_layers;
+  CUtensorMap m_pool, m_in;
+  XMaps xm_x16, xm_ctx, xm_ffn, xm_cls, xm_ha, xm_hb;
+  int last_launches = 0;
+  double sum_len_sq = 0.0;  // sum_b L_b^2 of the current request (attention flops)
+  // per-launch profiling (CUDA events around every kernel of the last forward)
+  bool profiling = false;
+  struct Rec {
+    int kind;
+    double bytes, flops;
+    cudaEvent_t e0, e1;
+  };
+  std::vector<Rec> recs;
+  size_t n_recs = 0;
+  cudaStream_t rec_stream = nullptr;
+  void rec_reset(cudaStream_t st) {
+    n_recs = 0;
+    rec_stream = st;
+  }
+  void rec_begin(int kind, double bytes, double flops) {
+    if (!profiling) return;
+    if (n_recs == recs.size()) {
+      Rec r{};
+      cudaEventCreate(&r.e0);
+      cudaEventCreate(&r.e1);
+      recs.push_back(r);
+    }
+    Rec& r = recs[n_recs];
+    r.kind = kind;
+    r.bytes = bytes;
+    r.flops = flops;
+    cudaEventRecord(r.e0, rec_stream);
+  }
+  void rec_end() {
+    if (!profiling) return;
+    cudaEventRecord(recs[n_recs].e1, rec_stream);
+    ++n_recs;
+  }
+};
+
+namespace {
+
+template <typename T>
+int dev_alloc(sp_group* g, T** p, size_t count) {
+  if (count == 0) count = 1;
+  void* q = nullptr;
+  cudaError_t e = cudaMalloc(&q, count * sizeof(T));
+  if (e != cudaSuccess) return fail(SP_ENOMEM, "cudaMalloc(%zu bytes): %s", count * sizeof(T), cudaGetErrorString(e));
+  g->allocs.push_back(q);
+  *p = static_cast<T*>(q);
+  return SP_OK;
+}
+
+void free_all(sp_group* g) {
+  for (void* p : g->allocs) cudaFree(p);
+  g->allocs.clear();
+  for (auto& r : g->recs) {
+    cudaEventDestroy(r.e0);
+    cudaEventDestroy(r.e1);
+  }
+  g->recs.clear();
+}
+
+int validate_config(const sp_config& c) {
+  if (c.kind != SP_KIND_DENSE && c.kind != SP_KIND_BERT) return fail(SP_EINVAL, "unknown student kind %d", c.kind);
+  if (c.n_students < 1) return fail(SP_EINVAL, "n_students must be >= 1");
+  if (c.hidden < 128 || c.hidden % 128) return fail(SP_EINVAL, "hidden=%d must be a multiple of 128", c.hidden);
+  if (c.kind == SP_KIND_BERT && !sp::rowops_supported_hidden(c.hidden))
+    return fail(SP_EINVAL, "BERT hidden=%d must be one of 128, 256, 512, 768, 1024", c.hidden);
+  if (c.n_classes < 1) return fail(SP_EINVAL, "n_classes must be >= 1");
+  if (c.max_tokens < 1 || c.max_seqs < 1) return fail(SP_EINVAL, "capacities must be >= 1");
+  if (c.kind == SP_KIND_BERT) {
+    if (c.n_layers < 1) return fail(SP_EINVAL, "BERT student needs n_layers >= 1");
+    if (c.n_heads < 1 || c.hidden % c.n_heads) return fail(SP_EINVAL, "hidden must be divisible by n_heads");
+    const int hd = c.hidden / c.n_heads;
+    if (hd != 32 && hd != 64) return fail(SP_EINVAL, "head_dim=%d unsupported (32 or 64)", hd);
+    if (c.ffn < 128 || c.ffn % 128) return fail(SP_EINVAL, "ffn must be a positive multiple of 128");
+    if (c.vocab < 1 || c.max_pos < 1) return fail(SP_EINVAL, "vocab and max_pos must be >= 1");
+  } else {
+    if (c.n_layers < 2) return fail(SP_EINVAL, "student needs at least 2 layers");  // nnkernel.py:265-266
+    if (c.d_in < 64 || c.d_in % 64) return fail(SP_EINVAL, "d_in must be a positive multiple of 64");
+  }
+  return SP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int sp_abi_version(void) { return SP_ABI_VERSION; }
+
+const char* sp_last_error(void) { return g_err.c_str(); }
+
+int sp_group_create(const sp_config* cfg, const sp_weights* weights, int device, sp_group** out) {
+  if (cfg == nullptr || weights == nullptr || out == nullptr) return fail(SP_EINVAL, "null argument");
+  *out = nullptr;
+  int rc = validate_config(*cfg);
+  if (rc) return rc;
+  if (encode_fn() == nullptr) return fail(SP_ECUDA, "cuTensorMapEncodeTiled unavailable (driver too old?)");
+  SP_CUDA(cudaSetDevice(device));
+  sp_group* g = new sp_group();
+  g->cfg = *cfg;
+  g->w = *weights;
+  g->device = device;
+  const sp_config& c = g->cfg;
+  const sp_weights& w = g->w;
+  const size_t S = c.n_students, H = c.hidden, T = c.max_tokens, B = c.max_seqs, F = c.ffn;
+  g->rows_cap = std::max(c.max_tokens, c.max_seqs);
+  const size_t R = g->rows_cap;
+  auto bail = [&](int code) {
+    free_all(g);
+    delete g;
+    return code;
+  };
+  if ((rc = dev_alloc(g, &g->final32, S * R * H))) return bail(rc);
+  if ((rc = dev_alloc(g, &g->d_ids, T))) return bail(rc);
+  if ((rc = dev_alloc(g, &g->d_cu, B + 1))) return bail(rc);
+  if ((rc = dev_alloc(g, &g->d_logits, R * c.n_classes))) return bail(rc);
+
+  if (c.kind == SP_KIND_BERT) {
+    if (!w.word_emb || !w.pos_emb || !w.type_emb || !w.emb_ln_gamma || !w.emb_ln_beta || !w.w_qkv || !w.b_qkv ||
+        !w.w_o || !w.b_o || !w.ln1_gamma || !w.ln1_beta || !w.w_ffn1 || !w.b_ffn1 || !w.w_ffn2 || !w.b_ffn2 ||
+        !w.ln2_gamma || !w.ln2_beta || !w.w_pool || !w.b_pool || !w.alpha || !w.w_cls || !w.b_cls)
+      return bail(fail(SP_EINVAL, "missing BERT weight pointer"));
+    if ((rc = dev_alloc(g, &g->x32, S * T * H))) return bail(rc);
+    if ((rc = dev_alloc(g, &g->x16, S * T * H))) return bail(rc);
+    if ((rc = dev_alloc(g, &g->qkv, S * T * 3 * H))) return bail(rc);
+    if ((rc = dev_alloc(g, &g->ctx, S * T * H))) return bail(rc);
+    if ((rc = dev_alloc(g, &g->ffn, S * T * F))) return bail(rc);
+    if ((rc = dev_alloc(g, &g->part, (size_t)kMaxSplits * S * T * H))) return bail(rc);
+    if ((rc = dev_alloc(g, &g->cls16, S * B * H))) return bail(rc);
+    const auto* wq = static_cast<const half*>(w.w_qkv);
+    const auto* wo = static_cast<const half*>(w.w_o);
+    const auto* w1 = static_cast<const half*>(w.w_ffn1);
+    const auto* w2 = static_cast<const half*>(w.w_ffn2);
+    g->m_qkv.resize(c.n_layers);
+    g->m_o.resize(c.n_layers);
+    g->m_f1.resize(c.n_layers);
+    g->m_f2.resize(c.n_layers);
+    bool ok = true;
+    for (int l = 0; l < c.n_layers; ++l) {
+      ok &= make_map(&g->m_qkv[l], wq + (size_t)l * S * 3 * H * H, S * 3 * H, H, 128);
+      ok &= make_map(&g->m_o[l], wo + (size_t)l * S * H * H, S * H, H, 128);
+      ok &= make_map(&g->m_f1[l], w1 + (size_t)l * S * F * H, S * F, H, 128);
+      ok &= make_map(&g->m_f2[l], w2 + (size_t)l * S * H * F, S * H, F, 128);
+    }
+    ok &= make_map(&g->m_pool, w.w_pool, S * H, H, 128);
+    ok &= make_xmaps(&g->xm_x16, g->x16, S * T, H);
+    ok &= make_xmaps(&g->xm_ctx, g->ctx, S * T, H);
+    ok &= make_xmaps(&g->xm_ffn, g->ffn, S * T, F);
+    ok &= make_xmaps(&g->xm_cls, g->cls16, S * B, H);
+    if (!ok) return bail(fail(SP_EINVAL, "tensor-map creation failed (pointer alignment / shape)"));
+  } else {
+    if (!w.w_in || !w.b_in || !w.w_layers || !w.b_layers || !w.alpha || !w.w_cls || !w.b_cls)
+      return bail(fail(SP_EINVAL, "missing dense weight pointer"));
+    half *ha = nullptr, *hb = nullptr;
+    if ((rc = dev_alloc(g, &ha, S * T * H))) return bail(rc);
+    if ((rc = dev_alloc(g, &hb, S * T * H))) return bail(rc);
+    if ((rc = dev_alloc(g, &g->xin, T * (size_t)c.d_in))) return bail(rc);
+    g->x16 = ha;
+    g->ctx = hb;
+    const auto* wl = static_cast<const half*>(w.w_layers);
+    g->m_layers.resize(c.n_layers);
+    bool ok = make_map(&g->m_in, w.w_in, S * H, c.d_in, 128);
+    for (int l = 0; l < c.n_layers; ++l) ok &= make_map(&g->m_layers[l], wl + (size_t)l * S * H * H, S * H, H, 128);
+    ok &= make_xmaps(&g->xm_ha, ha, S * T, H);
+    ok &= make_xmaps(&g->xm_hb, hb, S * T, H);
+    if (!ok) return bail(fail(SP_EINVAL, "tensor-map creation failed (pointer alignment / shape)"));
+  }
+  *out = g;
+  return SP_OK;
+}
+
+int sp_group_destroy(sp_group* g) {
+  if (g == nullptr) return SP_OK;
+  cudaSetDevice(g->device);
+  free_all(g);
+  delete g;
+  return SP_OK;
+}
+
+int sp_group_last_launches(const sp_group* g) { return g ? g->last_launches : 0; }
+
+int sp_group_set_profiling(sp_group* g, int enable) {
+  if (g == nullptr) return fail(SP_EINVAL, "null group");
+  cudaSetDevice(g->device);
+  g->profiling = enable != 0;
+  g->n_recs = 0;
+  return SP_OK;
+}
+
+int sp_group_profile_read(sp_group* g, sp_launch_record* out, int max_records) {
+  if (g == nullptr || (out == nullptr && max_records > 0)) return -fail(SP_EINVAL, "null argument");
+  cudaSetDevice(g->device);
+  const int n = static_cast<int>(std::min<size_t>(g->n_recs, max_records > 0 ? (size_t)max_records : 0));
+  for (int i = 0; i < n; ++i) {
+    const auto& r = g->recs[i];
+    if (cudaEventSynchronize(r.e1) != cudaSuccess) return -fail(SP_ECUDA, "event sync failed");
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, r.e0, r.e1);
+    out[i].kind = r.kind;
+    out[i].ms = ms;
+    out[i].bytes = r.bytes;
+    out[i].flops = r.flops;
+  }
+  return static_cast<int>(g->n_recs);
+}
+
+}  // extern "C"
+
+namespace {
+
+// Launch one grouped projection. Returns the number of kernels launched (1).
+int run_gemm(sp_group* grp, int kind, const CUtensorMap& wmap, const XMaps& xm, int groups, int n_out, int k_dim,
+             int t_rows, int x_group_rows, const float* bias, int bias_gs, int act, void* out, long long out_gs,
+             int out_f32, int splits, long long split_stride, cudaStream_t st) {
+  sp::GemmParams p{};
+  p.n_out = n_out;
+  p.k_dim = k_dim;
+  p.t_rows = t_rows;
+  p.x_group_rows = x_group_rows;
+  sp::gemm_configure_tiles(t_rows, &p.bn, &p.n_tiles, &p.stages);
+  p.m_tiles = n_out / 128;
+  p.splits = splits;
+  p.kb_per_split = (k_dim / 64) / splits;
+  p.out = out;
+  p.out_group_stride = out_gs;
+  p.out_split_stride = split_stride;
+  p.out_ld = n_out;
+  p.bias = bias;
+  p.bias_group_stride = bias_gs;
+  p.act = act;
+  p.out_f32 = out_f32;
+  sp::GemmMaps maps;
+  maps.w = wmap;
+  maps.x64 = xm.x64;
+  maps.x16 = xm.x16;
+  if (grp) {
+    const double G = groups, N = n_out, K = k_dim, T = t_rows;
+    const double xin = (x_group_rows == 0 ? 1.0 : G) * T * K * 2.0;
+    const double outb = G * T * N * (splits > 1 ? 4.0 * splits : (out_f32 ? 4.0 : 2.0));
+    grp->rec_begin(kind, G * N * K * 2.0 + xin + outb + (bias ? G * N * 4.0 : 0.0), 2.0 * G * N * K * T);
+  }
+  sp::launch_gemm(maps, p, groups, st);
+  if (grp) grp->rec_end();
+  return 1;
+}
+
+int bert_forward(sp_group* g, const int32_t* ids, const int32_t* cu, int n_seqs, int n_tokens, int max_len, int k,
+                 float* rep, float* logits, int add_bias, cudaStream_t st) {
+  const sp_config& c = g->cfg;
+  const sp_weights& w = g->w;
+  const int S = c.n_students, H = c.hidden, F = c.ffn, T = c.max_tokens, B = c.max_seqs;
+  const long long xgs = (long long)T * H;
+  int launches = 0;
+  g->rec_reset(st);
+  const double GTH = (double)k * n_tokens * H;
+  if (k > 0) {
+    g->rec_begin(SP_LAUNCH_EMBED_LN, GTH * 10.0, 0.0);
+    sp::launch_embed_ln(ids, cu, n_seqs, n_tokens, k, static_cast<const half*>(w.word_emb),
+                        static_cast<const half*>(w.pos_emb), static_cast<const half*>(w.type_emb),
+                        (long long)c.vocab * H, (long long)c.max_pos * H, w.emb_ln_gamma, w.emb_ln_beta, H, c.ln_eps,
+                        g->x32, g->x16, xgs, st);
+    g->rec_end();
+    ++launches;
+    int bn, n_tiles, stages;
+    sp::gemm_configure_tiles(n_tokens, &bn, &n_tiles, &stages);
+    const int s_o = choose_splits(k * (H / 128) * n_tiles, H / 64, kMaxSplits);
+    const int s_f = choose_splits(k * (H / 128) * n_tiles, F / 64, kMaxSplits);
+    const long long part_ss = (long long)S * xgs;
+    for (int l = 0; l < c.n_layers; ++l) {
+      const size_t lS = (size_t)l * S;
+      launches += run_gemm(g, SP_LAUNCH_GEMM_QKV, g->m_qkv[l], g->xm_x16, k, 3 * H, H, n_tokens, T, w.b_qkv + lS * 3 * H, 3 * H,
+                           sp::ACT_NONE, g->qkv, (long long)T * 3 * H, 0, 1, 0, st);
+      g->rec_begin(SP_LAUNCH_ATTENTION, GTH * 8.0, 4.0 * k * H * g->sum_len_sq);
+      sp::launch_attention(g->qkv, g->ctx, cu, n_seqs, max_len, k, c.n_heads, H / c.n_heads, H, T, st);
+      g->rec_end();
+      ++launches;
+      // O and FFN2 write raw partial sums; the reduce+LN kernel owns bias, residual and LayerNorm
+      launches += run_gemm(g, SP_LAUNCH_GEMM_O, g->m_o[l], g->xm_ctx, k, H, H, n_tokens, T, nullptr, H, sp::ACT_NONE, g->part, xgs, 1,
+                           s_o, part_ss, st);
+      g->rec_begin(SP_LAUNCH_REDUCE_LN, GTH * (4.0 * s_o + 10.0), 0.0);
+      sp::launch_reduce_ln(g->part, s_o, part_ss, w.b_o + lS * H, w.ln1_gamma + lS * H, w.ln1_beta + lS * H, H,
+                           c.ln_eps, g->x32, g->x16, xgs, n_tokens, k, cu, n_seqs, nullptr, 0, st);
+      g->rec_end();
+      ++launches;
+      launches += run_gemm(g, SP_LAUNCH_GEMM_FFN1, g->m_f1[l], g->xm_x16, k, F, H, n_tokens, T, w.b_ffn1 + lS * F, F, sp::ACT_GELU, g->ffn,
+                           (long long)T * F, 0, 1, 0, st);
+      launches += run_gemm(g, SP_LAUNCH_GEMM_FFN2, g->m_f2[l], g->xm_ffn, k, H, F, n_tokens, T, nullptr, H, sp::ACT_NONE, g->part, xgs, 1,
+                           s_f, part_ss, st);
+      const bool last = (l == c.n_layers - 1);
+      g->rec_begin(SP_LAUNCH_REDUCE_LN, GTH * (4.0 * s_f + 10.0), 0.0);
+      sp::launch_reduce_ln(g->part, s_f, part_ss, w.b_ffn2 + lS * H, w.ln2_gamma + lS * H, w.ln2_beta + lS * H, H,
+                           c.ln_eps, g->x32, g->x16, xgs, n_tokens, k, cu, n_seqs, last ? g->cls16 : nullptr,
+                           (long long)B * H, st);
+      g->rec_end();
+      ++launches;
+    }
+    // pooler on the CLS rows: tanh(W_p h_CLS + b_p), fp32 out
+    launches += run_gemm(g, SP_LAUNCH_GEMM_POOL, g->m_pool, g->xm_cls, k, H, H, n_seqs, B, w.b_pool, H, sp::ACT_TANH, g->final32,
+                         (long long)g->rows_cap * H, 1, 1, 0, st);
+  }
+  g->rec_begin(SP_LAUNCH_HEAD, (double)k * n_seqs * H * 4.0 + (double)c.n_classes * H * 4.0 + n_seqs * H * 4.0, 0.0);
+  sp::launch_head(g->final32, (long long)g->rows_cap * H, k, w.alpha, w.w_cls, w.b_cls, c.n_classes, H, n_seqs,
+                  add_bias, rep, logits, st);
+  g->rec_end();
+  ++launches;
+  g->last_launches = launches;
+  return SP_OK;
+}
+
+int dense_forward(sp_group* g, const half* x, int n_rows, int k, float* rep, float* logits, int add_bias,
+                  cudaStream_t st, const XMaps& xin_maps) {
+  const sp_config& c = g->cfg;
+  const sp_weights& w = g->w;
+  const int S = c.n_students, H = c.hidden, T = c.max_tokens;
+  const long long hgs = (long long)T * H;
+  const long long fgs = (long long)g->rows_cap * H;
+  int launches = 0;
+  g->rec_reset(st);
+  if (k > 0) {
+    // input_proj: every student reads the same rows (x_group_rows = 0)
+    half* bufs[2] = {g->x16, g->ctx};
+    const XMaps* maps[2] = {&g->xm_ha, &g->xm_hb};
+    launches += run_gemm(g, SP_LAUNCH_GEMM_DENSE, g->m_in, xin_maps, k, H, c.d_in, n_rows, 0, w.b_in, H, sp::ACT_TANH, bufs[0], hgs, 0, 1, 0, st);
+    int cur = 0;
+    for (int l = 0; l < c.n_layers; ++l) {
+      const bool last = (l == c.n_layers - 1);
+      const size_t lS = (size_t)l * S;
+      void* out = last ? static_cast<void*>(g->final32) : static_cast<void*>(bufs[cur ^ 1]);
+      launches += run_gemm(g, SP_LAUNCH_GEMM_DENSE, g->m_layers[l], *maps[cur], k, H, H, n_rows, T, w.b_layers + lS * H, H, sp::ACT_TANH, out,
+                           last ? fgs : hgs, last ? 1 : 0, 1, 0, st);
+      cur ^= 1;
+    }
+  }
+  g->rec_begin(SP_LAUNCH_HEAD, (double)k * n_rows * H * 4.0 + (double)c.n_classes * H * 4.0, 0.0);
+  sp::launch_head(g->final32, fgs, k, w.alpha, w.w_cls, w.b_cls, c.n_classes, H, n_rows, add_bias, rep, logits, st);
+  g->rec_end();
+  ++launches;
+  g->last_launches = launches;
+  (void)x;
+  return SP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int sp_group_forward(sp_group* g, const int32_t* ids, const int32_t* cu_seqlens, int32_t n_seqs, int32_t n_tokens,
+                     int32_t max_seq_len, int32_t k_active, float* rep_out, float* logits_out, int32_t add_bias,
+                     void* stream) {
+  if (g == nullptr) return fail(SP_EINVAL, "null group");
+  const sp_config& c = g->cfg;
+  if (c.kind != SP_KIND_BERT) return fail(SP_EINVAL, "sp_group_forward needs a BERT-kind group");
+  if (k_active < 0 || k_active > c.n_students)
+    return fail(SP_EINVAL, "k=%d out of range 0..%d", k_active, c.n_students);
+  if (n_seqs < 1 || n_seqs > c.max_seqs) return fail(SP_EINVAL, "n_seqs=%d outside 1..%d", n_seqs, c.max_seqs);
+  if (n_tokens < n_seqs || n_tokens > c.max_tokens)
+    return fail(SP_EINVAL, "n_tokens=%d outside %d..%d", n_tokens, n_seqs, c.max_tokens);
+  if (max_seq_len < 1 || max_seq_len > c.max_pos || max_seq_len > n_tokens)
+    return fail(SP_EINVAL, "max_seq_len=%d outside 1..%d", max_seq_len, c.max_pos);
+  if (!ids || !cu_seqlens || !logits_out) return fail(SP_EINVAL, "null buffer");
+  cudaSetDevice(g->device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (g->profiling) {  // exact attention flops need the lengths (profiling already perturbs timing)
+    std::vector<int32_t> h(n_seqs + 1);
+    SP_CUDA(cudaMemcpyAsync(h.data(), cu_seqlens, sizeof(int32_t) * (n_seqs + 1), cudaMemcpyDeviceToHost, st));
+    SP_CUDA(cudaStreamSynchronize(st));
+    g->sum_len_sq = 0.0;
+    for (int b = 0; b < n_seqs; ++b) g->sum_len_sq += double(h[b + 1] - h[b]) * double(h[b + 1] - h[b]);
+  }
+  int rc = bert_forward(g, ids, cu_seqlens, n_seqs, n_tokens, max_seq_len, k_active, rep_out, logits_out, add_bias, st);
+  if (rc) return rc;
+  SP_CUDA(cudaGetLastError());
+  return SP_OK;
+}
+
+int sp_group_forward_dense(sp_group* g, const void* x, int32_t n_rows, int32_t k_active, float* rep_out,
+                           float* logits_out, int32_t add_bias, void* stream) {
+  if (g == nullptr) return fail(SP_EINVAL, "null group");
+  const sp_config& c = g->cfg;
+  if (c.kind != SP_KIND_DENSE) return fail(SP_EINVAL, "sp_group_forward_dense needs a dense-kind group");
+  if (k_active < 0 || k_active > c.n_students)
+    return fail(SP_EINVAL, "k=%d out of range 0..%d", k_active, c.n_students);
+  if (n_rows < 1 || n_rows > c.max_tokens) return fail(SP_EINVAL, "n_rows=%d outside 1..%d", n_rows, c.max_tokens);
+  if (!x || !logits_out) return fail(SP_EINVAL, "null buffer");
+  cudaSetDevice(g->device);
+  XMaps xm;
+  if (!make_xmaps(&xm, x, (uint64_t)n_rows, (uint64_t)c.d_in))
+    return fail(SP_EINVAL, "input tensor map failed (x must be 16-byte aligned fp16 [n_rows][d_in])");
+  int rc = dense_forward(g, static_cast<const half*>(x), n_rows, k_active, rep_out, logits_out, add_bias,
+                         static_cast<cudaStream_t>(stream), xm);
+  if (rc) return rc;
+  SP_CUDA(cudaGetLastError());
+  return SP_OK;
+}
+
+int sp_group_forward_host(sp_group* g, const int32_t* ids, const int32_t* cu, int32_t n_seqs, int32_t n_tokens,
+                          int32_t k_active, float* logits_out, int32_t add_bias, void* stream) {
+  if (g == nullptr) return fail(SP_EINVAL, "null group");
+  const sp_config& c = g->cfg;
+  if (c.kind != SP_KIND_BERT) return fail(SP_EINVAL, "sp_group_forward_host needs a BERT-kind group");
+  if (!ids || !cu || !logits_out) return fail(SP_EINVAL, "null buffer");
+  if (n_seqs < 1 || n_seqs > c.max_seqs) return fail(SP_EINVAL, "n_seqs=%d outside 1..%d", n_seqs, c.max_seqs);
+  if (cu[0] != 0) return fail(SP_EINVAL, "cu_seqlens[0] must be 0");
+  int max_len = 0;
+  g->sum_len_sq = 0.0;
+  for (int b = 0; b < n_seqs; ++b) {
+    const int len = cu[b + 1] - cu[b];
+    g->sum_len_sq += double(len) * double(len);
+    if (len < 1) return fail(SP_EINVAL, "sequence %d is empty or cu_seqlens decreases", b);
+    if (len > c.max_pos) return fail(SP_EINVAL, "sequence %d has %d tokens > max_pos %d", b, len, c.max_pos);
+    max_len = std::max(max_len, len);
+  }
+  if (cu[n_seqs] != n_tokens) return fail(SP_EINVAL, "cu_seqlens[-1]=%d != n_tokens=%d", cu[n_seqs], n_tokens);
+  if (n_tokens > c.max_tokens) return fail(SP_EINVAL, "n_tokens=%d > capacity %d", n_tokens, c.max_tokens);
+  for (int t = 0; t < n_tokens; ++t)
+    if (ids[t] < 0 || ids[t] >= c.vocab) return fail(SP_EINVAL, "token id %d at %d outside vocab", ids[t], t);
+  cudaSetDevice(g->device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  SP_CUDA(cudaMemcpyAsync(g->d_ids, ids, sizeof(int32_t) * n_tokens, cudaMemcpyHostToDevice, st));
+  SP_CUDA(cudaMemcpyAsync(g->d_cu, cu, sizeof(int32_t) * (n_seqs + 1), cudaMemcpyHostToDevice, st));
+  int rc = bert_forward(g, g->d_ids, g->d_cu, n_seqs, n_tokens, max_len, k_active, nullptr, g->d_logits, add_bias, st);
+  if (rc) return rc;
+  SP_CUDA(cudaGetLastError());
+  SP_CUDA(cudaMemcpyAsync(logits_out, g->d_logits, sizeof(float) * n_seqs * c.n_classes, cudaMemcpyDeviceToHost, st));
+  SP_CUDA(cudaStreamSynchronize(st));
+  return SP_OK;
+}
+
+int sp_op_gemm(const void* w, const void* x, int32_t groups, int32_t n_out, int32_t k_dim, int32_t t_rows,
+               int32_t x_group_rows, int32_t x_rows_total, const float* bias, int32_t act, void* out, int32_t out_f32,
+               int32_t splits, void* stream) {
+  if (!w || !x || !out) return fail(SP_EINVAL, "null buffer");
+  if (groups < 1 || n_out < 128 || n_out % 128 || k_dim < 64 || k_dim % 64 || t_rows < 1)
+    return fail(SP_EINVAL, "bad gemm shape groups=%d n_out=%d k=%d t=%d", groups, n_out, k_dim, t_rows);
+  if (splits < 1 || (k_dim / 64) % splits) return fail(SP_EINVAL, "splits=%d must divide k/64", splits);
+  if (act < 0 || act > 2) return fail(SP_EINVAL, "unknown activation %d", act);
+  CUtensorMap wm;
+  XMaps xm;
+  if (!make_map(&wm, w, (uint64_t)groups * n_out, k_dim, 128) || !make_xmaps(&xm, x, x_rows_total, k_dim))
+    return fail(SP_EINVAL, "tensor-map creation failed");
+  const long long ogs = (long long)t_rows * n_out;
+  run_gemm(nullptr, 0, wm, xm, groups, n_out, k_dim, t_rows, x_group_rows, bias, n_out, act, out, ogs, splits > 1 ? 1 : out_f32,
+           splits, ogs * groups, static_cast<cudaStream_t>(stream));
+  SP_CUDA(cudaGetLastError());
+  return SP_OK;
+}
+
+int sp_op_attention(const void* qkv, void* ctx, const int32_t* cu_seqlens, int32_t n_seqs, int32_t max_seq_len,
+                    int32_t groups, int32_t n_heads, int32_t head_dim, int32_t group_rows, void* stream) {
+  if (!qkv || !ctx || !cu_seqlens) return fail(SP_EINVAL, "null buffer");
+  if (head_dim != 32 && head_dim != 64) return fail(SP_EINVAL, "head_dim must be 32 or 64");
+  if (n_seqs < 1 || groups < 1 || n_heads < 1 || max_seq_len < 1) return fail(SP_EINVAL, "bad attention shape");
+  sp::launch_attention(static_cast<const half*>(qkv), static_cast<half*>(ctx), cu_seqlens, n_seqs, max_seq_len,
+                       groups, n_heads, head_dim, n_heads * head_dim, group_rows, static_cast<cudaStream_t>(stream));
+  SP_CUDA(cudaGetLastError());
+  return SP_OK;
+}
+
+}  // extern "C"

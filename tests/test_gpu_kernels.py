@@ -1,0 +1,114 @@
+"""Per-kernel numerics on the B200: each sm_100a kernel against a plain PyTorch fp32 reference of
+the same op (the kernels compute in fp16 operands with fp32 accumulation)."""
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+
+def _gemm_ref(w, x, bias, act, x_group_rows):
+    G, N, K = w.shape
+    T = x.shape[0] if x_group_rows == 0 else x_group_rows
+    outs = []
+    for g in range(G):
+        xg = x if x_group_rows == 0 else x[g * x_group_rows:(g + 1) * x_group_rows]
+        y = xg.float() @ w[g].float().T
+        if bias is not None:
+            y = y + bias[g]
+        if act == 1:
+            y = torch.tanh(y)
+        elif act == 2:
+            y = torch.nn.functional.gelu(y)
+        outs.append(y)
+    return torch.stack(outs)
+
+
+@pytest.mark.parametrize("T", [1, 16, 20, 64, 100, 256, 300, 520])
+@pytest.mark.parametrize("act", [0, 1, 2])
+def test_gemm_matches_torch(cuda_lib, T, act):
+    from paper_2408_12526_b200 import _lib
+
+    torch.manual_seed(T * 3 + act)
+    G, N, K = 3, 256, 192
+    dev = "cuda"
+    w = (torch.randn(G, N, K, device=dev) * 0.05).half()
+    x = torch.randn(G * T, K, device=dev).half()
+    bias = torch.randn(G, N, device=dev) * 0.1
+    out = torch.empty(G, T, N, device=dev, dtype=torch.float32)
+    _lib.check(cuda_lib.sp_op_gemm(w.data_ptr(), x.data_ptr(), G, N, K, T, T, G * T, bias.data_ptr(), act,
+                                   out.data_ptr(), 1, 1, None))
+    torch.cuda.synchronize()
+    ref = _gemm_ref(w, x, bias, act, T)
+    torch.testing.assert_close(out, ref, rtol=1e-3, atol=1e-3)
+
+
+@pytest.mark.parametrize("T", [5, 48, 130])
+def test_gemm_fp16_out_shared_input(cuda_lib, T):
+    """x_group_rows = 0: every student reads the same rows (dense kind input_proj)."""
+    from paper_2408_12526_b200 import _lib
+
+    torch.manual_seed(7)
+    G, N, K = 4, 128, 64
+    w = (torch.randn(G, N, K, device="cuda") * 0.1).half()
+    x = torch.randn(T, K, device="cuda").half()
+    out = torch.empty(G, T, N, device="cuda", dtype=torch.float16)
+    _lib.check(cuda_lib.sp_op_gemm(w.data_ptr(), x.data_ptr(), G, N, K, T, 0, T, None, 1, out.data_ptr(), 0, 1,
+                                   None))
+    torch.cuda.synchronize()
+    ref = _gemm_ref(w, x, None, 1, 0)
+    torch.testing.assert_close(out.float(), ref, rtol=2e-3, atol=2e-3)
+
+
+@pytest.mark.parametrize("splits", [2, 3, 6])
+def test_gemm_split_k_partials(cuda_lib, splits):
+    from paper_2408_12526_b200 import _lib
+
+    torch.manual_seed(splits)
+    G, N, K, T = 2, 384, 768, 37
+    w = (torch.randn(G, N, K, device="cuda") * 0.03).half()
+    x = torch.randn(G * T, K, device="cuda").half()
+    part = torch.empty(splits, G, T, N, device="cuda", dtype=torch.float32)
+    _lib.check(cuda_lib.sp_op_gemm(w.data_ptr(), x.data_ptr(), G, N, K, T, T, G * T, None, 0, part.data_ptr(), 1,
+                                   splits, None))
+    torch.cuda.synchronize()
+    ref = _gemm_ref(w, x, None, 0, T)
+    torch.testing.assert_close(part.sum(0), ref, rtol=1e-3, atol=1e-3)
+
+
+def _attn_ref(qkv, cu, G, nh, hd):
+    H = nh * hd
+    out = torch.zeros(qkv.shape[0], qkv.shape[1], H, device=qkv.device)
+    for g in range(G):
+        for b in range(len(cu) - 1):
+            s, e = int(cu[b]), int(cu[b + 1])
+            q = qkv[g, s:e, :H].float().view(e - s, nh, hd).transpose(0, 1)
+            k = qkv[g, s:e, H:2 * H].float().view(e - s, nh, hd).transpose(0, 1)
+            v = qkv[g, s:e, 2 * H:].float().view(e - s, nh, hd).transpose(0, 1)
+            p = torch.softmax(q @ k.transpose(1, 2) / math.sqrt(hd), dim=-1)
+            out[g, s:e] = (p @ v).transpose(0, 1).reshape(e - s, H)
+    return out
+
+
+@pytest.mark.parametrize("hd,nh,lens", [(64, 12, [1, 17, 64, 65, 200]), (32, 4, [8, 33, 64, 3]),
+                                         (64, 16, [512, 1, 130])])
+def test_attention_varlen_matches_torch(cuda_lib, hd, nh, lens):
+    from paper_2408_12526_b200 import _lib
+
+    torch.manual_seed(sum(lens))
+    G, H = 2, nh * hd
+    cu = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    T = int(cu[-1])
+    cap = T + 5
+    qkv = torch.randn(G, cap, 3 * H, device="cuda").half()
+    ctx = torch.zeros(G, cap, H, device="cuda", dtype=torch.float16)
+    cu_d = torch.from_numpy(cu).cuda()
+    _lib.check(cuda_lib.sp_op_attention(qkv.data_ptr(), ctx.data_ptr(), cu_d.data_ptr(), len(lens), max(lens), G,
+                                        nh, hd, cap, None))
+    torch.cuda.synchronize()
+    ref = _attn_ref(qkv, cu, G, nh, hd)
+    torch.testing.assert_close(ctx[:, :T].float(), ref[:, :T], rtol=5e-3, atol=5e-3)
+    assert torch.all(ctx[:, T:] == 0), "attention wrote past the packed tokens"

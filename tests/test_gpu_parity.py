@@ -1,0 +1,154 @@
+"""Group-level parity on the B200: the CUDA engine (through the C ABI) vs the float64 oracle on
+identical (fp16/fp32-rounded) weights and identical inputs.
+
+Bar (BASELINE.json north star): fp32 logits within 1e-3 relative — |dz| <= 1e-3 * max|z_ref| over
+the batch (conftest.rel_err_rows; per row at batch-1) — and identical argmax wherever the
+reference's top-2 margin exceeds twice that tolerance (rows inside the band must be rare).
+"""
+import numpy as np
+import pytest
+
+from conftest import rel_err_rows
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-3
+
+
+def _check_logits(got, ref, tol=TOL):
+    err = rel_err_rows(got, ref)
+    assert err <= tol, f"max row-relative logit error {err:.3e} > {tol}"
+    ref2 = np.atleast_2d(ref)
+    got2 = np.atleast_2d(got)
+    srt = np.sort(ref2, axis=1)
+    margin = (srt[:, -1] - srt[:, -2]) / max(float(np.abs(ref2).max()), 1e-30)
+    decided = margin > 2 * tol
+    assert np.array_equal(np.argmax(got2, 1)[decided], np.argmax(ref2, 1)[decided])
+    assert decided.mean() >= 0.9, "too many near-tie rows to judge argmax parity"
+    return err
+
+
+def _seqs(rng, n, lo, hi, vocab=30522):
+    out = []
+    for _ in range(n):
+        L = int(rng.integers(lo, hi + 1))
+        ids = rng.integers(1000, vocab, size=L)
+        ids[0] = 101  # [CLS]
+        out.append(ids.astype(np.int32))
+    return out
+
+
+@pytest.fixture(scope="module")
+def tiny():
+    from oracle.bert import OracleBertGroup
+    from paper_2408_12526_b200 import PRESETS, StudentGroup, random_bert_group
+
+    cfg, K = PRESETS["tiny"]
+    w = random_bert_group(cfg, K, seed=11)
+    return StudentGroup(w, max_tokens=2048, max_seqs=64), OracleBertGroup(w)
+
+
+@pytest.mark.parametrize("k", [1, 2, 3, 4])
+def test_tiny_bert_group_all_prefixes(tiny, k):
+    grp, orc = tiny
+    rng = np.random.default_rng(100 + k)
+    seqs = _seqs(rng, 7, 8, 64)
+    rep_ref, z_ref = orc.forward(seqs, k)
+    z = grp.logits(seqs, k)
+    _check_logits(z, z_ref)
+    rep = grp.rep(seqs, k)
+    assert rel_err_rows(rep, rep_ref) <= TOL
+
+
+def test_tiny_bert_batch1_single_sequence_squeezes(tiny):
+    grp, orc = tiny
+    ids = _seqs(np.random.default_rng(5), 1, 8, 64)[0]
+    z = grp.logits(ids)
+    assert z.shape == (2,)
+    _, z_ref = orc.forward([ids])
+    _check_logits(z, z_ref[0])
+
+
+def test_tiny_bert_edge_lengths(tiny):
+    """Length-1 sequences (CLS only), exactly one and just over one 64-token attention block."""
+    grp, orc = tiny
+    rng = np.random.default_rng(9)
+    seqs = [s[:L] for s, L in zip(_seqs(rng, 5, 64, 64), [1, 2, 63, 64, 64])] + _seqs(rng, 2, 65, 130)
+    _, z_ref = orc.forward(seqs)
+    _check_logits(grp.logits(seqs), z_ref)
+
+
+def test_tiny_bert_k_out_of_range(tiny):
+    grp, _ = tiny
+    seqs = _seqs(np.random.default_rng(1), 2, 8, 16)
+    for bad in (0, 5, -1):
+        with pytest.raises(ValueError):
+            grp.logits(seqs, bad)
+
+
+def test_tiny_bert_rejects_bad_tokens(tiny):
+    grp, _ = tiny
+    with pytest.raises(ValueError):
+        grp.logits([np.array([101, 30522], np.int32)])
+    with pytest.raises(ValueError):
+        grp.logits([np.array([], np.int32)])
+    with pytest.raises(ValueError):
+        grp.logits([np.arange(513, dtype=np.int32) + 1000])
+
+
+def test_tiny_bert_host_api_matches_device_api(tiny):
+    from paper_2408_12526_b200.group import pack_sequences
+
+    grp, _ = tiny
+    seqs = _seqs(np.random.default_rng(3), 4, 8, 64)
+    ids, cu, _ = pack_sequences(seqs)
+    z_host = grp.forward_host(ids, cu, 3)
+    z_dev = grp.logits(seqs, 3)
+    np.testing.assert_array_equal(z_host, z_dev.astype(np.float32))  # same kernels, same order: bit-identical
+
+
+def test_dense_group_matches_oracle():
+    from oracle.dense import group_forward_weights
+    from paper_2408_12526_b200 import StudentGroup, random_dense_group
+
+    w = random_dense_group(d_in=8, rep_dim=16, depth=2, n_students=3, n_classes=2, seed=4)
+    grp = StudentGroup(w, max_tokens=512)
+    x = np.random.default_rng(2).normal(size=(300, 8))
+    for k in (1, 2, 3):
+        rep_ref, z_ref = group_forward_weights(w, np.float16(x).astype(np.float64), k)
+        _check_logits(grp.logits(x, k), z_ref)
+        assert rel_err_rows(grp.rep(x, k), rep_ref) <= TOL
+
+
+def test_dense_group_wide_matches_oracle():
+    """Reference-architecture students at the BERT-base width (H=768, K=8)."""
+    from oracle.dense import group_forward_weights
+    from paper_2408_12526_b200 import StudentGroup, random_dense_group
+
+    w = random_dense_group(d_in=768, rep_dim=768, depth=2, n_students=8, n_classes=2, seed=8)
+    grp = StudentGroup(w, max_tokens=256)
+    x = np.random.default_rng(3).normal(size=(256, 768))
+    rep_ref, z_ref = group_forward_weights(w, np.float16(x).astype(np.float64))
+    _check_logits(grp.logits(x), z_ref)
+    x1 = x[0]
+    z1 = grp.logits(x1)
+    assert z1.shape == (2,)
+
+
+def test_base_bert_group_batch1_parity():
+    """BERT-base-sized group (K=8, H=768, 12 heads) at batch-1 on ragged lengths incl. L=512."""
+    from oracle.bert import OracleBertGroup
+    from paper_2408_12526_b200 import PRESETS, StudentGroup, random_bert_group
+
+    cfg, K = PRESETS["base"]
+    w = random_bert_group(cfg, K, seed=1)
+    grp = StudentGroup(w, max_tokens=1024, max_seqs=8)
+    orc = OracleBertGroup(w)
+    rng = np.random.default_rng(0)
+    for L in (16, 100, 512):
+        ids = _seqs(rng, 1, L, L)
+        _, z_ref = orc.forward(ids)
+        _check_logits(grp.logits(ids), z_ref)
+        _, z_ref4 = orc.forward(ids, 4)
+        _check_logits(grp.logits(ids, 4), z_ref4)
