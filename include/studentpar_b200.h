@@ -162,6 +162,11 @@ int sp_op_gemm(const void* w, const void* x, int32_t groups, int32_t n_out, int3
 int sp_op_attention(const void* qkv, void* ctx, const int32_t* cu_seqlens, int32_t n_seqs, int32_t max_seq_len,
                     int32_t groups, int32_t n_heads, int32_t head_dim, int32_t group_rows, void* stream);
 
+/* Debug: when non-NULL, every subsequent GEMM launch writes 8 %globaltimer stamps per CTA
+ * (entry, prologue done, first TMA, last TMA, first MMA, last commit, epilogue start, exit) into
+ * this device buffer, indexed by CTA. */
+int sp_debug_set_gemm_trace(void* device_buf);
+
 #ifdef __cplusplus
 }
 #endif

@@ -41,6 +41,8 @@ __global__ void __launch_bounds__(128)
   __shared__ __align__(16) half sK[BK * LD];
   __shared__ __align__(16) half sV[BK * LD];
 
+  pdl_wait();
+  pdl_launch_dependents();
   const int b = blockIdx.y;
   const int s0 = cu[b];
   const int L = cu[b + 1] - s0;
@@ -191,9 +193,11 @@ void launch_attention(const half* qkv, half* ctx, const int* cu_seqlens, int n_s
   dim3 grid((max_len + 63) / 64, n_seqs, groups * n_heads);
   const float scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(head_dim));
   if (head_dim == 64)
-    attn_kernel<64><<<grid, 128, 0, stream>>>(qkv, ctx, cu_seqlens, n_heads, hidden, group_rows, scale_log2);
+    launch_pdl(attn_kernel<64>, grid, dim3(128), 0, stream, qkv, ctx, cu_seqlens, n_heads, hidden, group_rows,
+               scale_log2);
   else
-    attn_kernel<32><<<grid, 128, 0, stream>>>(qkv, ctx, cu_seqlens, n_heads, hidden, group_rows, scale_log2);
+    launch_pdl(attn_kernel<32>, grid, dim3(128), 0, stream, qkv, ctx, cu_seqlens, n_heads, hidden, group_rows,
+               scale_log2);
 }
 
 }  // namespace sp

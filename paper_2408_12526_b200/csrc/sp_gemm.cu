@@ -1,28 +1,47 @@
 // sp_gemm.cu — student-batched projection GEMM on 5th-gen tensor cores (tcgen05 + TMEM + TMA).
 //
 // Swap-AB: the weight slab is the UMMA "A" operand (M = 128 output features per CTA) and the
-// request's tokens are the "B" operand (N = token tile, 16..256). At batch-1 the token count is
-// small, so this puts the large dimension (weights, streamed once from HBM) on M and keeps every
-// SM busy streaming a distinct weight slab; the student index is the grid's y axis (group axis).
+// request's tokens are the "B" operand (N = token tile, 16..128). At batch-1 the token count is
+// small, so the large dimension (weights, streamed once from HBM) sits on M and every SM streams
+// a distinct weight slab; the student index is the grid's y axis (the group axis).
 //
-// Warp roles (192 threads, one tile per CTA):
-//   warp 0      TMA producer (one elected lane): W tile {64 x 128} + X tile {64 x bn} per stage
-//   warp 1      TMEM allocator + MMA issuer (one elected lane): 4 x UMMA 128 x bn x 16 per stage
-//   warps 2..5  epilogue: tcgen05.ld TMEM -> registers, bias + activation, store (quadrant = warp % 4)
+// Warp roles (320 threads, one output tile per CTA, <= ~100 KiB smem so two CTAs share an SM):
+//   warp 0       TMA producer (one elected lane): W tile {64 x 128} + X tile {64 x bn} per stage
+//   warp 1       TMEM allocator + MMA issuer (one elected lane): 4 x UMMA 128 x bn x 16 per stage
+//   warps 2..9   epilogue: tcgen05.ld TMEM -> registers (x32), bias + activation, per-warp smem
+//                transpose, 16-byte coalesced stores. Warp w reads TMEM lane quadrant w % 4 and
+//                one half of the token columns.
+//
+// Programmatic dependent launch: weights never depend on the previous kernel, so the producer
+// issues the weight loads of the first pipeline stages BEFORE griddepcontrol.wait and only the
+// activation loads after it — the weight stream of this projection overlaps the tail of the
+// previous kernel (attention / LayerNorm / another projection).
 //
 // Reference op: DenseLayer.forward, z = x @ W.T + b then act (nnkernel.py:66-76).
+#include <type_traits>
+
 #include "sp_kernels.cuh"
 #include "sp_ptx.cuh"
 
 namespace sp {
 
 static constexpr int kBlockM = 128;
-static constexpr int kBlockK = 64;                      // one 128-byte swizzle row of fp16
+static constexpr int kBlockK = 64;                         // one 128-byte swizzle row of fp16
 static constexpr int kATileBytes = kBlockM * kBlockK * 2;  // 16 KiB
-static constexpr int kTmemCols = 256;
-static constexpr int kThreads = 192;
+static constexpr int kTmemCols = 128;                      // bn <= 128 fp32 columns
+static constexpr int kEpiWarps = 8;
+static constexpr int kThreads = 64 + 32 * kEpiWarps;
+static constexpr int kMaxBn = 128;
 
-__global__ void __launch_bounds__(kThreads, 1)
+template <int ACT>
+__device__ __forceinline__ float apply_act(float y) {
+  if constexpr (ACT == ACT_TANH) return tanhf(y);
+  else if constexpr (ACT == ACT_GELU) return gelu_erf(y);
+  else return y;
+}
+
+template <int ACT, bool OUT_F32>
+__global__ void __launch_bounds__(kThreads, 2)
     gemm_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_x64,
                 const __grid_constant__ CUtensorMap map_x16, const GemmParams p) {
   extern __shared__ uint8_t smem_raw[];
@@ -47,6 +66,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = warp_id();
   const int lane = lane_id();
+  unsigned long long* tr = p.trace ? p.trace + 8ull * (blockIdx.y * gridDim.x + blockIdx.x) : nullptr;
+  if (tr && threadIdx.x == 0) tr[0] = globaltimer();
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < p.stages; ++s) {
@@ -67,6 +88,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_launch_dependents();
+  if (tr && threadIdx.x == 0) tr[1] = globaltimer();
 
   if (warp == 0) {
     if (elect_one()) {
@@ -74,23 +97,36 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t pol_x = policy_evict_last();   // activations: re-read by every M tile
       const int wrow = g * p.n_out + m0;
       const int xrow = g * p.x_group_rows + n0;
-      int s = 0;
-      uint32_t ph = 0;
-      for (int kb = kb0; kb < kb1; ++kb) {
-        mbar_wait(&empty[s], ph ^ 1);
-        uint8_t* sa = smem + s * stage_bytes;
-        uint8_t* sb = sa + kATileBytes;
-        mbar_arrive_expect_tx(&full[s], stage_bytes);
+      auto load_x = [&](int s, int kb) {
+        uint8_t* sb = smem + s * stage_bytes + kATileBytes;
         const int kc = kb * kBlockK;
-        tma_load_2d(&map_w, &full[s], sa, kc, wrow, pol_w);
         int r = 0;
         for (; r + 64 <= p.bn; r += 64) tma_load_2d(&map_x64, &full[s], sb + r * 128, kc, xrow + r, pol_x);
         for (; r < p.bn; r += 16) tma_load_2d(&map_x16, &full[s], sb + r * 128, kc, xrow + r, pol_x);
+      };
+      // 1) weight prefetch of the first stages: independent of the previous kernel
+      const int n_pre = min(p.stages, kb1 - kb0);
+      for (int i = 0; i < n_pre; ++i) {
+        mbar_arrive_expect_tx(&full[i], stage_bytes);
+        tma_load_2d(&map_w, &full[i], smem + i * stage_bytes, (kb0 + i) * kBlockK, wrow, pol_w);
+      }
+      if (tr) tr[2] = globaltimer();
+      // 2) activations are produced by the previous kernel
+      pdl_wait();
+      for (int i = 0; i < n_pre; ++i) load_x(i, kb0 + i);
+      int s = n_pre % p.stages;
+      uint32_t ph = (n_pre == p.stages) ? 1u : 0u;
+      for (int kb = kb0 + n_pre; kb < kb1; ++kb) {
+        mbar_wait(&empty[s], ph ^ 1);
+        mbar_arrive_expect_tx(&full[s], stage_bytes);
+        tma_load_2d(&map_w, &full[s], smem + s * stage_bytes, kb * kBlockK, wrow, pol_w);
+        load_x(s, kb);
         if (++s == p.stages) {
           s = 0;
           ph ^= 1;
         }
       }
+      if (tr) tr[3] = globaltimer();
     }
   } else if (warp == 1) {
     if (elect_one()) {
@@ -100,12 +136,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int kb = kb0; kb < kb1; ++kb) {
         mbar_wait(&full[s], ph);
         tc_fence_after();
+        if (tr && kb == kb0) tr[4] = globaltimer();
         const uint32_t sa = smem_u32(smem + s * stage_bytes);
         const uint64_t adesc = umma_sdesc_sw128(sa);
         const uint64_t bdesc = umma_sdesc_sw128(sa + kATileBytes);
 #pragma unroll
         for (int k = 0; k < kBlockK / 16; ++k) {
-          // +32 bytes per K=16 slice inside the 128-byte swizzle row (address field is in 16-byte units)
+          // +32 bytes per K=16 slice inside the 128-byte swizzle row (address field in 16-byte units)
           umma_f16_ss(tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
         }
         umma_commit(&empty[s]);
@@ -115,38 +152,64 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       umma_commit(tmem_full);
+      if (tr) tr[5] = globaltimer();
     }
     __syncwarp();
   } else {
-    // Epilogue: warp w owns TMEM lanes 32*(w%4) .. +31, i.e. output features m0 + 32*(w%4) + lane.
-    const int q = warp & 3;
+    // ---------------------------------------------------------------- epilogue
+    const int e = warp - 2;  // 0..7
+    const int q = warp & 3;  // TMEM lane quadrant (hardware: warp w accesses lanes 32*(w%4)..)
+    const int half_cols = p.bn >> 1;
+    const int c_begin = (e >> 2) * half_cols;
     const int feat = m0 + q * 32 + lane;
     const bool partial = p.splits > 1;
     float bias = 0.f;
-    if (!partial && p.bias != nullptr) bias = p.bias[(long long)g * p.bias_group_stride + feat];
+    if (!partial && p.bias != nullptr) bias = __ldg(p.bias + (long long)g * p.bias_group_stride + feat);
     const bool has_k = kb1 > kb0;
+    using OutT = typename std::conditional<OUT_F32, float, half>::type;
+    constexpr int kRowBytes = 32 * static_cast<int>(sizeof(OutT));  // one warp's 32 features of a token
+    constexpr int kLanesPerRow = kRowBytes / 16;
+    constexpr int kRowsPerPass = 32 / kLanesPerRow;
+    OutT* stage = reinterpret_cast<OutT*>(smem + e * 32 * kRowBytes);  // warp-private, pipeline smem is free now
+    OutT* out = reinterpret_cast<OutT*>(p.out) + (long long)g * p.out_group_stride +
+                (long long)split * p.out_split_stride + m0 + q * 32;
+
     mbar_wait(tmem_full, 0);
     tc_fence_after();
-    const long long obase = (long long)g * p.out_group_stride + (long long)split * p.out_split_stride + feat;
-    for (int c = 0; c < p.bn; c += 16) {
-      float v[16];
-      tmem_ld16(tmem + (static_cast<uint32_t>(q * 32) << 16) + c, v);
+    if (tr && warp == 2 && lane == 0) tr[6] = globaltimer();
+    const uint32_t taddr = tmem + (static_cast<uint32_t>(q * 32) << 16);
+    for (int c = c_begin; c < c_begin + half_cols; c += 32) {
+      const int n = min(32, c_begin + half_cols - c);  // multiple of 8, warp-uniform
+      uint32_t r[32];
+      if (n == 32) {
+        tmem_ld32_nowait(taddr + c, r);
+      } else {
+        for (int i = 0; i < n; i += 8) tmem_ld8_nowait(taddr + c + i, r + i);
+      }
+      tmem_wait_ld();
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const int t = n0 + c + j;
-        if (t < p.t_rows) {
-          float y = has_k ? v[j] : 0.f;
-          if (!partial) {
-            y += bias;
-            if (p.act == ACT_TANH) y = tanhf(y);
-            else if (p.act == ACT_GELU) y = gelu_erf(y);
-          }
-          const long long o = obase + (long long)t * p.out_ld;
-          if (p.out_f32) reinterpret_cast<float*>(p.out)[o] = y;
-          else reinterpret_cast<half*>(p.out)[o] = __float2half_rn(y);
+      for (int j = 0; j < 32; ++j) {
+        if (j < n) {
+          float y = has_k ? __uint_as_float(r[j]) : 0.f;
+          if (!partial) y = apply_act<ACT>(y + bias);
+          if constexpr (OUT_F32) stage[j * 32 + lane] = y;
+          else stage[j * 32 + lane] = __float2half_rn(y);
         }
       }
+      __syncwarp();
+      const int sub = lane % kLanesPerRow;
+      for (int j0 = 0; j0 < n; j0 += kRowsPerPass) {
+        const int j = j0 + lane / kLanesPerRow;
+        const int t = n0 + c + j;
+        if (j < n && t < p.t_rows) {
+          const uint4 v = *reinterpret_cast<const uint4*>(reinterpret_cast<const uint8_t*>(stage) + j * kRowBytes +
+                                                          sub * 16);
+          *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(out + (long long)t * p.out_ld) + sub * 16) = v;
+        }
+      }
+      __syncwarp();
     }
+    if (tr && warp == 2 && lane == 0) tr[7] = globaltimer();
   }
 
   tc_fence_before();
@@ -157,34 +220,71 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// Debug trace: launches append their per-CTA stamps one after another (slot 0 of the buffer
+// holds the number of CTAs recorded so far, host-side mirror in g_trace_used).
+static unsigned long long* g_trace = nullptr;
+static size_t g_trace_used = 0;
+void set_gemm_trace(unsigned long long* buf) {
+  g_trace = buf;
+  g_trace_used = 0;
+}
+
 size_t gemm_smem_bytes(int bn, int stages) {
   return static_cast<size_t>(stages) * (kATileBytes + bn * 128) + 1024 /*align*/ + 256 /*barriers*/;
 }
 
 void gemm_configure_tiles(int t_rows, int* bn, int* n_tiles, int* stages) {
-  int tiles = (t_rows + 255) / 256;
+  int tiles = (t_rows + kMaxBn - 1) / kMaxBn;
   if (tiles < 1) tiles = 1;
-  int per = (t_rows + tiles - 1) / tiles;
+  const int per = (t_rows + tiles - 1) / tiles;
   int b = ((per + 15) / 16) * 16;
   if (b < 16) b = 16;
   *bn = b;
   *n_tiles = tiles;
-  // <= ~100 KiB for small token tiles (two CTAs per SM), ~200 KiB otherwise.
-  const int budget = (b <= 64) ? 100 * 1024 : 200 * 1024;
-  int st = budget / (kATileBytes + b * 128);
-  if (st > 8) st = 8;
+  // ~96 KiB per CTA so that two CTAs (e.g. the tail of one projection and the prefetching head
+  // of the next) share an SM: smem 2 x ~97 KiB, TMEM 2 x 128 columns.
+  int st = (96 * 1024) / (kATileBytes + b * 128);
+  if (st > 6) st = 6;
   if (st < 2) st = 2;
   *stages = st;
 }
 
-void launch_gemm(const GemmMaps& maps, const GemmParams& p, int groups, cudaStream_t stream) {
+template <int ACT, bool OUT_F32>
+static void launch_gemm_t(const GemmMaps& maps, const GemmParams& p, int groups, cudaStream_t stream) {
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(gemm_kernel<ACT, OUT_F32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr_set = true;
   }
-  dim3 grid(p.m_tiles * p.n_tiles * p.splits, groups);
-  gemm_kernel<<<grid, kThreads, gemm_smem_bytes(p.bn, p.stages), stream>>>(maps.w, maps.x64, maps.x16, p);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(p.m_tiles * p.n_tiles * p.splits, groups);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = gemm_smem_bytes(p.bn, p.stages);
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  GemmParams q = p;
+  q.trace = g_trace ? g_trace + 8 * g_trace_used : nullptr;
+  if (g_trace) g_trace_used += (size_t)cfg.gridDim.x * cfg.gridDim.y;
+  cudaLaunchKernelEx(&cfg, gemm_kernel<ACT, OUT_F32>, maps.w, maps.x64, maps.x16, q);
+}
+
+void launch_gemm(const GemmMaps& maps, const GemmParams& p, int groups, cudaStream_t stream) {
+  const bool f32 = p.out_f32 || p.splits > 1;
+  const int act = p.splits > 1 ? ACT_NONE : p.act;
+  if (act == ACT_GELU) {
+    if (f32) launch_gemm_t<ACT_GELU, true>(maps, p, groups, stream);
+    else launch_gemm_t<ACT_GELU, false>(maps, p, groups, stream);
+  } else if (act == ACT_TANH) {
+    if (f32) launch_gemm_t<ACT_TANH, true>(maps, p, groups, stream);
+    else launch_gemm_t<ACT_TANH, false>(maps, p, groups, stream);
+  } else {
+    if (f32) launch_gemm_t<ACT_NONE, true>(maps, p, groups, stream);
+    else launch_gemm_t<ACT_NONE, false>(maps, p, groups, stream);
+  }
 }
 
 }  // namespace sp

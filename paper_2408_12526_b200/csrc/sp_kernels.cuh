@@ -5,7 +5,28 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <utility>
+
 namespace sp {
+
+// Launch with programmatic stream serialization: the kernel may start while its predecessor in
+// the stream finishes; every kernel of this library calls griddepcontrol.wait before touching
+// data the predecessor produces (and only prefetches read-only weights before that).
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 enum Act : int { ACT_NONE = 0, ACT_TANH = 1, ACT_GELU = 2 };
 
@@ -34,7 +55,11 @@ struct GemmParams {
   int bias_group_stride;
   int act;
   int out_f32;
+  unsigned long long* trace;  // debug: 8 globaltimer stamps per CTA, or null
 };
+
+// Debug hook: when set, every GEMM launch records a per-CTA timeline into this device buffer.
+void set_gemm_trace(unsigned long long* buf);
 
 struct GemmMaps {
   CUtensorMap w;    // box {64, 128}

@@ -1,9 +1,13 @@
 // sp_rowops.cu — row-wise HBM-bound kernels: embedding gather + LN, split-K reduce + residual + LN,
 // and the boosting-sum + classifier head. One warp per row; statistics in fp32 via warp shuffles.
+// Every load of a row is issued before the first use (no dependent load chains), and every kernel
+// is PDL-launched: griddepcontrol.wait first, then it lets the next projection start prefetching.
 #include "sp_kernels.cuh"
 #include "sp_ptx.cuh"
 
 namespace sp {
+
+static constexpr int kMaxSplitsRow = 4;
 
 // Largest b with cu[b] <= t (cu is nondecreasing, cu[0] = 0).
 __device__ __forceinline__ int seq_of(const int* cu, int n_seqs, int t) {
@@ -21,9 +25,15 @@ template <int NC>
 __device__ __forceinline__ void layer_norm_store(float (&v)[NC][4], const float* gamma, const float* beta, float eps,
                                                  int hidden, float* x32, half* x16, half* cls16) {
   const int lane = lane_id();
+  float4 gm[NC], bt[NC];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    gm[c] = __ldg(reinterpret_cast<const float4*>(gamma + c * 128 + lane * 4));
+    bt[c] = __ldg(reinterpret_cast<const float4*>(beta + c * 128 + lane * 4));
+  }
   float s = 0.f;
 #pragma unroll
-  for (int c = 0; c < NC; ++c) s += v[c][0] + v[c][1] + v[c][2] + v[c][3];
+  for (int c = 0; c < NC; ++c) s += (v[c][0] + v[c][1]) + (v[c][2] + v[c][3]);
   const float mean = warp_sum(s) / hidden;
   float q = 0.f;
 #pragma unroll
@@ -37,13 +47,11 @@ __device__ __forceinline__ void layer_norm_store(float (&v)[NC][4], const float*
 #pragma unroll
   for (int c = 0; c < NC; ++c) {
     const int f = c * 128 + lane * 4;
-    const float4 gm = *reinterpret_cast<const float4*>(gamma + f);
-    const float4 bt = *reinterpret_cast<const float4*>(beta + f);
     float4 y;
-    y.x = (v[c][0] - mean) * rstd * gm.x + bt.x;
-    y.y = (v[c][1] - mean) * rstd * gm.y + bt.y;
-    y.z = (v[c][2] - mean) * rstd * gm.z + bt.z;
-    y.w = (v[c][3] - mean) * rstd * gm.w + bt.w;
+    y.x = (v[c][0] - mean) * rstd * gm[c].x + bt[c].x;
+    y.y = (v[c][1] - mean) * rstd * gm[c].y + bt[c].y;
+    y.z = (v[c][2] - mean) * rstd * gm[c].z + bt[c].z;
+    y.w = (v[c][3] - mean) * rstd * gm[c].w + bt[c].w;
     *reinterpret_cast<float4*>(x32 + f) = y;
     __half2 h01 = __floats2half2_rn(y.x, y.y), h23 = __floats2half2_rn(y.z, y.w);
     uint2 packed = make_uint2(*reinterpret_cast<uint32_t*>(&h01), *reinterpret_cast<uint32_t*>(&h23));
@@ -52,8 +60,7 @@ __device__ __forceinline__ void layer_norm_store(float (&v)[NC][4], const float*
   }
 }
 
-__device__ __forceinline__ void load_h4(const half* p, float (&o)[4]) {
-  const uint2 u = *reinterpret_cast<const uint2*>(p);
+__device__ __forceinline__ void h4_to_f4(const uint2 u, float (&o)[4]) {
   const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&u.x));
   const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&u.y));
   o[0] = a.x;
@@ -68,24 +75,33 @@ __global__ void __launch_bounds__(128)
                     const half* __restrict__ word, const half* __restrict__ pos, const half* __restrict__ type,
                     long long word_gs, long long pos_gs, const float* __restrict__ gamma,
                     const float* __restrict__ beta, int hidden, float eps, float* x32, half* x16, long long x_gs) {
+  pdl_wait();
+  pdl_launch_dependents();
   const int t = blockIdx.x * 4 + warp_id();
   if (t >= n_tokens) return;
   const int g = blockIdx.y;
   const int lane = lane_id();
+  const int id = __ldg(ids + t);
   const int b = seq_of(cu, n_seqs, t);
   const int p = t - __ldg(cu + b);
-  const int id = __ldg(ids + t);
   const half* wr = word + g * word_gs + (long long)id * hidden;
   const half* pr = pos + g * pos_gs + (long long)p * hidden;
   const half* tr = type + (long long)g * hidden;
-  float v[NC][4];
+  uint2 wa[NC], pa[NC], ta[NC];
 #pragma unroll
   for (int c = 0; c < NC; ++c) {
     const int f = c * 128 + lane * 4;
+    wa[c] = __ldg(reinterpret_cast<const uint2*>(wr + f));
+    pa[c] = __ldg(reinterpret_cast<const uint2*>(pr + f));
+    ta[c] = __ldg(reinterpret_cast<const uint2*>(tr + f));
+  }
+  float v[NC][4];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
     float a[4], bb[4], cc[4];
-    load_h4(wr + f, a);
-    load_h4(pr + f, bb);
-    load_h4(tr + f, cc);
+    h4_to_f4(wa[c], a);
+    h4_to_f4(pa[c], bb);
+    h4_to_f4(ta[c], cc);
 #pragma unroll
     for (int j = 0; j < 4; ++j) v[c][j] = a[j] + bb[j] + cc[j];
   }
@@ -100,27 +116,39 @@ __global__ void __launch_bounds__(128)
                      const float* __restrict__ bias, const float* __restrict__ gamma, const float* __restrict__ beta,
                      int hidden, float eps, float* x32, half* x16, long long x_gs, int n_tokens,
                      const int* __restrict__ cu, int n_seqs, half* cls16, long long cls_gs) {
+  pdl_wait();
+  pdl_launch_dependents();
   const int t = blockIdx.x * 4 + warp_id();
   if (t >= n_tokens) return;
   const int g = blockIdx.y;
   const int lane = lane_id();
   const long long row = (long long)g * x_gs + (long long)t * hidden;
-  float v[NC][4];
+  // issue every load of the row up front: residual, bias and up to kMaxSplitsRow partial sums
+  float4 r[NC], bs[NC], pv[kMaxSplitsRow][NC];
 #pragma unroll
   for (int c = 0; c < NC; ++c) {
     const int f = c * 128 + lane * 4;
-    const float4 r = *reinterpret_cast<const float4*>(x32 + row + f);
-    const float4 bs = *reinterpret_cast<const float4*>(bias + (long long)g * hidden + f);
-    v[c][0] = r.x + bs.x;
-    v[c][1] = r.y + bs.y;
-    v[c][2] = r.z + bs.z;
-    v[c][3] = r.w + bs.w;
-    for (int s = 0; s < splits; ++s) {  // fixed order: deterministic
-      const float4 pv = *reinterpret_cast<const float4*>(part + s * part_split_stride + row + f);
-      v[c][0] += pv.x;
-      v[c][1] += pv.y;
-      v[c][2] += pv.z;
-      v[c][3] += pv.w;
+    r[c] = *reinterpret_cast<const float4*>(x32 + row + f);
+    bs[c] = __ldg(reinterpret_cast<const float4*>(bias + (long long)g * hidden + f));
+#pragma unroll
+    for (int s = 0; s < kMaxSplitsRow; ++s)
+      if (s < splits) pv[s][c] = *reinterpret_cast<const float4*>(part + s * part_split_stride + row + f);
+  }
+  float v[NC][4];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    v[c][0] = r[c].x + bs[c].x;
+    v[c][1] = r[c].y + bs[c].y;
+    v[c][2] = r[c].z + bs[c].z;
+    v[c][3] = r[c].w + bs[c].w;
+#pragma unroll
+    for (int s = 0; s < kMaxSplitsRow; ++s) {  // fixed order: deterministic
+      if (s < splits) {
+        v[c][0] += pv[s][c].x;
+        v[c][1] += pv[s][c].y;
+        v[c][2] += pv[s][c].z;
+        v[c][3] += pv[s][c].w;
+      }
     }
   }
   half* cls_row = nullptr;
@@ -132,24 +160,38 @@ __global__ void __launch_bounds__(128)
                        x16 + row, cls_row);
 }
 
-// One CTA per output row b. rep is accumulated over students in index order (distill.py:174-177).
+// One CTA per output row b. rep is accumulated over students in index order (distill.py:174-177);
+// the student loads are batched 8 at a time so they are in flight together.
 __global__ void __launch_bounds__(256)
     head_kernel(const float* __restrict__ final_rep, long long final_gs, int groups, const float* __restrict__ alpha,
                 const float* __restrict__ w_cls, const float* __restrict__ b_cls, int n_classes, int hidden,
                 int add_bias, float* __restrict__ rep, float* __restrict__ logits) {
+  pdl_wait();
+  pdl_launch_dependents();
   extern __shared__ float srep[];
   __shared__ float red[8];
   const int b = blockIdx.x;
   for (int j = threadIdx.x; j < hidden; j += blockDim.x) {
     float r = 0.f;
-    for (int m = 0; m < groups; ++m) r += alpha[m] * final_rep[m * final_gs + (long long)b * hidden + j];
+    for (int m0 = 0; m0 < groups; m0 += 8) {
+      float vals[8], al[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const bool ok = m0 + i < groups;
+        vals[i] = ok ? final_rep[(m0 + i) * final_gs + (long long)b * hidden + j] : 0.f;
+        al[i] = ok ? __ldg(alpha + m0 + i) : 0.f;
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        if (m0 + i < groups) r += al[i] * vals[i];
+    }
     srep[j] = r;
     if (rep) rep[(long long)b * hidden + j] = r;
   }
   __syncthreads();
   for (int c = 0; c < n_classes; ++c) {
     float acc = 0.f;
-    for (int j = threadIdx.x; j < hidden; j += blockDim.x) acc += w_cls[(long long)c * hidden + j] * srep[j];
+    for (int j = threadIdx.x; j < hidden; j += blockDim.x) acc += __ldg(w_cls + (long long)c * hidden + j) * srep[j];
     acc = warp_sum(acc);
     if (lane_id() == 0) red[warp_id()] = acc;
     __syncthreads();
@@ -168,20 +210,33 @@ bool rowops_supported_hidden(int hidden) {
   return hidden % 128 == 0 && (nc == 1 || nc == 2 || nc == 4 || nc == 6 || nc == 8);
 }
 
+template <int NC>
+static void embed_ln_t(dim3 grid, cudaStream_t st, const int* ids, const int* cu, int n_seqs, int n_tokens,
+                       const half* word, const half* pos, const half* type, long long word_gs, long long pos_gs,
+                       const float* gamma, const float* beta, int hidden, float eps, float* x32, half* x16,
+                       long long x_gs) {
+  launch_pdl(embed_ln_kernel<NC>, grid, dim3(128), 0, st, ids, cu, n_seqs, n_tokens, word, pos, type, word_gs,
+             pos_gs, gamma, beta, hidden, eps, x32, x16, x_gs);
+}
+
 void launch_embed_ln(const int* ids, const int* cu_seqlens, int n_seqs, int n_tokens, int groups, const half* word,
                      const half* pos, const half* type, long long word_gs, long long pos_gs, const float* gamma,
                      const float* beta, int hidden, float eps, float* x32, half* x16, long long x_gs,
                      cudaStream_t stream) {
   if (n_tokens <= 0 || groups <= 0) return;
   dim3 grid((n_tokens + 3) / 4, groups);
+#define SP_EMBED(NC_)                                                                                      \
+  embed_ln_t<NC_>(grid, stream, ids, cu_seqlens, n_seqs, n_tokens, word, pos, type, word_gs, pos_gs, gamma, \
+                  beta, hidden, eps, x32, x16, x_gs)
   switch (hidden / 128) {
-    case 1: embed_ln_kernel<1><<<grid, 128, 0, stream>>>(ids, cu_seqlens, n_seqs, n_tokens, word, pos, type, word_gs, pos_gs, gamma, beta, hidden, eps, x32, x16, x_gs); break;
-    case 2: embed_ln_kernel<2><<<grid, 128, 0, stream>>>(ids, cu_seqlens, n_seqs, n_tokens, word, pos, type, word_gs, pos_gs, gamma, beta, hidden, eps, x32, x16, x_gs); break;
-    case 4: embed_ln_kernel<4><<<grid, 128, 0, stream>>>(ids, cu_seqlens, n_seqs, n_tokens, word, pos, type, word_gs, pos_gs, gamma, beta, hidden, eps, x32, x16, x_gs); break;
-    case 6: embed_ln_kernel<6><<<grid, 128, 0, stream>>>(ids, cu_seqlens, n_seqs, n_tokens, word, pos, type, word_gs, pos_gs, gamma, beta, hidden, eps, x32, x16, x_gs); break;
-    case 8: embed_ln_kernel<8><<<grid, 128, 0, stream>>>(ids, cu_seqlens, n_seqs, n_tokens, word, pos, type, word_gs, pos_gs, gamma, beta, hidden, eps, x32, x16, x_gs); break;
+    case 1: SP_EMBED(1); break;
+    case 2: SP_EMBED(2); break;
+    case 4: SP_EMBED(4); break;
+    case 6: SP_EMBED(6); break;
+    case 8: SP_EMBED(8); break;
     default: break;
   }
+#undef SP_EMBED
 }
 
 void launch_reduce_ln(const float* part, int splits, long long part_split_stride, const float* bias,
@@ -190,22 +245,26 @@ void launch_reduce_ln(const float* part, int splits, long long part_split_stride
                       long long cls_gs, cudaStream_t stream) {
   if (n_tokens <= 0 || groups <= 0) return;
   dim3 grid((n_tokens + 3) / 4, groups);
+#define SP_REDUCE(NC_)                                                                                          \
+  launch_pdl(reduce_ln_kernel<NC_>, grid, dim3(128), 0, stream, part, splits, part_split_stride, bias, gamma, \
+             beta, hidden, eps, x32, x16, x_gs, n_tokens, cu_seqlens, n_seqs, cls16, cls_gs)
   switch (hidden / 128) {
-    case 1: reduce_ln_kernel<1><<<grid, 128, 0, stream>>>(part, splits, part_split_stride, bias, gamma, beta, hidden, eps, x32, x16, x_gs, n_tokens, cu_seqlens, n_seqs, cls16, cls_gs); break;
-    case 2: reduce_ln_kernel<2><<<grid, 128, 0, stream>>>(part, splits, part_split_stride, bias, gamma, beta, hidden, eps, x32, x16, x_gs, n_tokens, cu_seqlens, n_seqs, cls16, cls_gs); break;
-    case 4: reduce_ln_kernel<4><<<grid, 128, 0, stream>>>(part, splits, part_split_stride, bias, gamma, beta, hidden, eps, x32, x16, x_gs, n_tokens, cu_seqlens, n_seqs, cls16, cls_gs); break;
-    case 6: reduce_ln_kernel<6><<<grid, 128, 0, stream>>>(part, splits, part_split_stride, bias, gamma, beta, hidden, eps, x32, x16, x_gs, n_tokens, cu_seqlens, n_seqs, cls16, cls_gs); break;
-    case 8: reduce_ln_kernel<8><<<grid, 128, 0, stream>>>(part, splits, part_split_stride, bias, gamma, beta, hidden, eps, x32, x16, x_gs, n_tokens, cu_seqlens, n_seqs, cls16, cls_gs); break;
+    case 1: SP_REDUCE(1); break;
+    case 2: SP_REDUCE(2); break;
+    case 4: SP_REDUCE(4); break;
+    case 6: SP_REDUCE(6); break;
+    case 8: SP_REDUCE(8); break;
     default: break;
   }
+#undef SP_REDUCE
 }
 
 void launch_head(const float* final_rep, long long final_gs, int groups, const float* alpha, const float* w_cls,
                  const float* b_cls, int n_classes, int hidden, int n_rows, int add_bias, float* rep, float* logits,
                  cudaStream_t stream) {
   if (n_rows <= 0) return;
-  head_kernel<<<n_rows, 256, hidden * sizeof(float), stream>>>(final_rep, final_gs, groups, alpha, w_cls, b_cls,
-                                                               n_classes, hidden, add_bias, rep, logits);
+  launch_pdl(head_kernel, dim3(n_rows), dim3(256), hidden * sizeof(float), stream, final_rep, final_gs, groups,
+             alpha, w_cls, b_cls, n_classes, hidden, add_bias, rep, logits);
 }
 
 }  // namespace sp

@@ -554,6 +554,11 @@ int sp_op_gemm(const void* w, const void* x, int32_t groups, int32_t n_out, int3
   return SP_OK;
 }
 
+int sp_debug_set_gemm_trace(void* device_buf) {
+  sp::set_gemm_trace(static_cast<unsigned long long*>(device_buf));
+  return SP_OK;
+}
+
 int sp_op_attention(const void* qkv, void* ctx, const int32_t* cu_seqlens, int32_t n_seqs, int32_t max_seq_len,
                     int32_t groups, int32_t n_heads, int32_t head_dim, int32_t group_rows, void* stream) {
   if (!qkv || !ctx || !cu_seqlens) return fail(SP_EINVAL, "null buffer");

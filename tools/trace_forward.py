@@ -1,0 +1,52 @@
+"""Absolute timeline of every GEMM CTA in one batch-1 forward (PDL overlap visible)."""
+import sys, numpy as np, torch
+sys.path.insert(0, ".")
+from paper_2408_12526_b200 import PRESETS, StudentGroup, random_bert_group, _lib
+cfg, K = PRESETS["base"]
+w = random_bert_group(cfg, K, seed=0)
+g = StudentGroup(w, max_tokens=512, max_seqs=1)
+lib = _lib.load()
+fw = torch.empty(256 << 18, device="cuda"); fr = torch.ones(256 << 18, device="cuda")
+logits = torch.empty(1, 2, device="cuda")
+tr = torch.zeros(8 * 20000, dtype=torch.int64, device="cuda")
+names = ["qkv", "o", "ffn1", "ffn2"] * 2 + ["pool"]
+for L in [int(x) for x in sys.argv[1].split(",")]:
+    ids = torch.randint(1000, 30000, (L,), dtype=torch.int32, device="cuda")
+    cu = torch.tensor([0, L], dtype=torch.int32, device="cuda")
+    run = lambda: g.forward_packed_device(ids, cu, 1, L, L, K, None, logits)
+    for _ in range(3): run()
+    torch.cuda.synchronize()
+    lib.sp_debug_set_gemm_trace(tr.data_ptr())
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        run()
+    lib.sp_debug_set_gemm_trace(None)
+    for _ in range(3): graph.replay()
+    fw.zero_(); fr.sum(); torch.cuda.synchronize()
+    tr.zero_()
+    e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(); graph.replay(); e1.record(); torch.cuda.synchronize()
+    t = tr.view(-1, 8).cpu().numpy().astype(np.float64)
+    t = t[t[:, 0] > 0]
+    base = t[:, 0].min()
+    # split CTAs into launches by grid sizes
+    bn = -(-L // (-(-L // 128))) ; bn = ((bn + 15) // 16) * 16; nt = -(-L // 128)
+    def grid(N, splits): return K * (N // 128) * nt * splits
+    import math
+    H, F = 768, 3072
+    def ch(units, nkb):
+        best = 1
+        for s in range(1, 5):
+            if nkb % s: continue
+            if s > 1 and nkb // s < 2: continue
+            best = s
+            if units * s >= 128: break
+        return best
+    so = ch(K * 6 * nt, 12); sf = ch(K * 6 * nt, 48)
+    sizes = [grid(3 * H, 1), grid(H, so), grid(F, 1), grid(H, sf)] * 2 + [K * 6]
+    off = 0
+    print(f"L={L}: event {e0.elapsed_time(e1)*1e3:.1f} us")
+    for nm, n in zip(names, sizes):
+        seg = (t[off:off + n] - base) / 1e3; off += n
+        print(f"  {nm:5s} ctas={n:4d} entry[{seg[:,0].min():6.1f},{seg[:,0].max():6.1f}] wpre={np.median(seg[:,2]):6.1f} mma0={np.median(seg[:,4]):6.1f} "
+              f"last_commit={seg[:,5].max():6.1f} epi0_max={seg[:,6].max():6.1f} end={seg[:,7].max():6.1f}")
