@@ -152,3 +152,53 @@ def test_base_bert_group_batch1_parity():
         _check_logits(grp.logits(ids), z_ref)
         _, z_ref4 = orc.forward(ids, 4)
         _check_logits(grp.logits(ids, 4), z_ref4)
+
+
+@pytest.mark.parametrize("name", ["tiny", "pad", "wide"])
+def test_dense_engine_matches_reference_golden(name):
+    """Reference-built StudentModel groups (tests/golden, made by the unmodified reference) through
+    the engine: logits vs the reference's own logits for every prefix k, argmax identical."""
+    from goldens import load_dense
+    from paper_2408_12526_b200 import StudentGroup, dense_group_from_arrays
+
+    case = load_dense(name)
+    w = dense_group_from_arrays(case["students"], case["alphas"], case["classifier"])
+    grp = StudentGroup(w, max_tokens=256)
+    for k in range(1, case["K"] + 1):
+        z = grp.logits(case["x"], k)
+        if case["engine_precision"]:
+            _check_logits(z, case["logits"][k])
+        else:  # tiny: reference weights are not fp16-representable; compare to the oracle on rounded weights
+            from oracle.dense import group_forward_weights
+
+            _, z_ref = group_forward_weights(w, np.float16(case["x"]).astype(np.float64), k)
+            _check_logits(z, z_ref)
+        np.testing.assert_allclose(grp.rep(case["x"][0], k)[: w.rep_dim].shape, case["rep1"][k].shape)
+
+
+def test_trained_reference_checkpoint_real_data_accuracy():
+    """ensemble-checkpoint-v1 trained and saved by the reference -> engine: prefix accuracies on the
+    reference's gaussian-task validation/test splits equal the reference's prefix_accuracy."""
+    from goldens import GOLDEN, load_trained_task
+    from paper_2408_12526_b200 import StudentGroup
+
+    task = load_trained_task()
+    grp = StudentGroup.from_checkpoint(GOLDEN / "ensemble_trained.json", max_tokens=256)
+    for k in range(1, len(grp) + 1):
+        assert grp.accuracy(task["x_val"], task["y_val"], k) == pytest.approx(task["acc_val"][k - 1], abs=0)
+        assert grp.accuracy(task["x_test"], task["y_test"], k) == pytest.approx(task["acc_test"][k - 1], abs=0)
+        z = grp.logits(task["x_val"], k)
+        ref = task[f"logits_val_k{k}"]
+        assert rel_err_rows(z, ref) <= 5e-3  # reference weights are f64; the engine rounds them to fp16
+
+
+def test_reference_object_snapshot_if_available(ref):
+    """StudentGroup.from_ensemble on a live reference EnsembleState (build container + GPU only)."""
+    from paper_2408_12526_b200 import StudentGroup
+
+    rng = np.random.Generator(np.random.PCG64(0))
+    students = [ref.nn.StudentModel.build(32, 64, 2, rng) for _ in range(3)]
+    state = ref.distill.EnsembleState(students, [1.0, 0.6, 0.3], ref.nn.DenseLayer.init(2, 64, "identity", rng))
+    grp = StudentGroup.from_ensemble(state)
+    x = rng.normal(size=(16, 32))
+    assert rel_err_rows(grp.logits(x, 2), state.classifier.forward(state.rep(x, 2))) <= 5e-3
