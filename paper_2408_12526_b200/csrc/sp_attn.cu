@@ -1,9 +1,11 @@
 // sp_attn.cu — unpadded variable-length multi-head attention for the student group.
 //
 // Sequences are packed back to back (cu_seqlens), no padding tokens and no mask beyond each
-// sequence's own length: every (student, sequence, head, 64-query block) is one CTA; its four
-// warps each own 16 query rows and stream 64-key blocks through shared memory with an online
-// (flash-style) softmax in fp32. QK^T and PV run on mma.sync m16n8k16 (fp16 in, fp32 accumulate).
+// sequence's own length. One CTA per (student, sequence, head, BQ-query block) with NW warps of 16
+// query rows each (BQ = 16 * NW); 64-key K/V blocks stream through a double-buffered cp.async
+// pipeline (next block in flight while the current one is consumed), fragments come from
+// ldmatrix, QK^T and PV run on mma.sync m16n8k16 (fp16 in, fp32 accumulate), and the online
+// softmax is kept in fp32 in the exp2 domain.
 //
 // There is no reference counterpart (SPEC.md:129 puts attention out of the artifact's scope); the
 // semantics are standard BERT self-attention softmax(Q K^T / sqrt(d)) V, restated in
@@ -26,86 +28,118 @@ __device__ __forceinline__ uint32_t pack_half2(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
+__device__ __forceinline__ void ldmatrix_x4(uint32_t (&r)[4], const void* p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(smem_u32(p)));
+}
+
 __device__ __forceinline__ void ldmatrix_x4_trans(uint32_t (&r)[4], const void* p) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
                : "r"(smem_u32(p)));
 }
 
-template <int D>
-__global__ void __launch_bounds__(128)
+// 16-byte async copy global -> shared; src_bytes = 0 zero-fills (rows past the sequence end).
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, uint32_t src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(src_bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+template <int D, int NW>
+__global__ void __launch_bounds__(32 * NW, NW == 8 ? 2 : 4)
     attn_kernel(const half* __restrict__ qkv, half* __restrict__ ctx, const int* __restrict__ cu, int n_heads,
                 int hidden, long long group_rows, float scale_log2) {
-  constexpr int BQ = 64, BK = 64, LD = D + 8;  // +8 halfs: conflict-free fragment loads
-  __shared__ __align__(16) half sQ[BQ * LD];
-  __shared__ __align__(16) half sK[BK * LD];
-  __shared__ __align__(16) half sV[BK * LD];
+  constexpr int BQ = 16 * NW, BK = 64, LD = D + 8;  // +8 halfs: conflict-free ldmatrix rows
+  constexpr int NT = 32 * NW;
+  constexpr int VPR = D / 8;  // 16-byte vectors per row
+  extern __shared__ __align__(16) uint8_t attn_smem[];
+  half* sQ = reinterpret_cast<half*>(attn_smem);
+  half* sK = sQ + BQ * LD;        // [2][BK][LD]
+  half* sV = sK + 2 * BK * LD;    // [2][BK][LD]
 
   pdl_wait();
   pdl_launch_dependents();
   const int b = blockIdx.y;
-  const int s0 = cu[b];
-  const int L = cu[b + 1] - s0;
+  const int s0 = __ldg(cu + b);
+  const int L = __ldg(cu + b + 1) - s0;
   const int q0 = blockIdx.x * BQ;
   if (q0 >= L) return;
   const int g = blockIdx.z / n_heads;
   const int h = blockIdx.z % n_heads;
   const long long row_stride = 3LL * hidden;
-  const half* base = qkv + ((long long)g * group_rows + s0) * row_stride;
+  const half* base = qkv + ((long long)g * group_rows + s0) * row_stride + h * D;
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const int gr = lane >> 2, tq = lane & 3;
-  constexpr int VPR = D / 8;  // 16-byte vectors per row
 
-  // Q tile
-  for (int i = tid; i < BQ * VPR; i += 128) {
+  auto load_kv = [&](int buf, int k0) {
+    half* dk = sK + buf * BK * LD;
+    half* dv = sV + buf * BK * LD;
+    for (int i = tid; i < BK * VPR; i += NT) {
+      const int r = i / VPR, c = (i % VPR) * 8;
+      const bool ok = k0 + r < L;
+      const half* rowp = base + (long long)(ok ? k0 + r : 0) * row_stride + c;
+      cp_async16(dk + r * LD + c, rowp + hidden, ok ? 16u : 0u);
+      cp_async16(dv + r * LD + c, rowp + 2 * hidden, ok ? 16u : 0u);
+    }
+  };
+
+  // Q tile + first K/V block
+  for (int i = tid; i < BQ * VPR; i += NT) {
     const int r = i / VPR, c = (i % VPR) * 8;
-    uint4 v = make_uint4(0, 0, 0, 0);
-    if (q0 + r < L) v = *reinterpret_cast<const uint4*>(base + (long long)(q0 + r) * row_stride + h * D + c);
-    *reinterpret_cast<uint4*>(&sQ[r * LD + c]) = v;
+    const bool ok = q0 + r < L;
+    cp_async16(sQ + r * LD + c, base + (long long)(ok ? q0 + r : 0) * row_stride + c, ok ? 16u : 0u);
   }
-  __syncthreads();
-  uint32_t qa[D / 16][4];
-#pragma unroll
-  for (int kk = 0; kk < D / 16; ++kk) {
-    const int r = warp * 16 + gr, c = kk * 16 + 2 * tq;
-    qa[kk][0] = *reinterpret_cast<const uint32_t*>(&sQ[r * LD + c]);
-    qa[kk][1] = *reinterpret_cast<const uint32_t*>(&sQ[(r + 8) * LD + c]);
-    qa[kk][2] = *reinterpret_cast<const uint32_t*>(&sQ[r * LD + c + 8]);
-    qa[kk][3] = *reinterpret_cast<const uint32_t*>(&sQ[(r + 8) * LD + c + 8]);
-  }
+  load_kv(0, 0);
+  cp_async_commit();
 
+  uint32_t qa[D / 16][4];
   float o[D / 8][4];
 #pragma unroll
   for (int i = 0; i < D / 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
   float m_run[2] = {-INFINITY, -INFINITY};
   float l_run[2] = {0.f, 0.f};
+  const int n_blocks = (L + BK - 1) / BK;
 
-  for (int k0 = 0; k0 < L; k0 += BK) {
+  for (int kb = 0; kb < n_blocks; ++kb) {
+    const int buf = kb & 1;
+    if (kb + 1 < n_blocks) load_kv(buf ^ 1, (kb + 1) * BK);  // prefetch the next block
+    cp_async_commit();
+    cp_async_wait<1>();  // everything but the just-issued prefetch has landed
     __syncthreads();
-    for (int i = tid; i < BK * VPR; i += 128) {
-      const int r = i / VPR, c = (i % VPR) * 8;
-      uint4 kv = make_uint4(0, 0, 0, 0), vv = make_uint4(0, 0, 0, 0);
-      if (k0 + r < L) {
-        const half* rowp = base + (long long)(k0 + r) * row_stride + h * D + c;
-        kv = *reinterpret_cast<const uint4*>(rowp + hidden);
-        vv = *reinterpret_cast<const uint4*>(rowp + 2 * hidden);
+    if (kb == 0) {
+      // Q fragments (A operand, row-major 16 x 16 per k-step) via ldmatrix
+#pragma unroll
+      for (int kk = 0; kk < D / 16; ++kk) {
+        const int r = warp * 16 + (lane & 15);
+        const int c = kk * 16 + (lane >> 4) * 8;
+        ldmatrix_x4(qa[kk], sQ + r * LD + c);
       }
-      *reinterpret_cast<uint4*>(&sK[r * LD + c]) = kv;
-      *reinterpret_cast<uint4*>(&sV[r * LD + c]) = vv;
     }
-    __syncthreads();
+    const half* cK = sK + buf * BK * LD;
+    const half* cV = sV + buf * BK * LD;
+    const int k0 = kb * BK;
 
+    // S = Q K^T for 64 keys: 8 n-tiles of 8 keys
     float s[BK / 8][4];
 #pragma unroll
     for (int nt = 0; nt < BK / 8; ++nt) {
       s[nt][0] = s[nt][1] = s[nt][2] = s[nt][3] = 0.f;
 #pragma unroll
-      for (int kk = 0; kk < D / 16; ++kk) {
-        const int kr = nt * 8 + gr, c = kk * 16 + 2 * tq;
-        const uint32_t b0 = *reinterpret_cast<const uint32_t*>(&sK[kr * LD + c]);
-        const uint32_t b1 = *reinterpret_cast<const uint32_t*>(&sK[kr * LD + c + 8]);
-        mma_16816(s[nt], qa[kk], b0, b1);
+      for (int kk = 0; kk < D / 16; kk += 2) {
+        // matrices: (keys nt*8.., d kk*16+0..7), (.., +8..15), (.., (kk+1)*16+0..7), (.., +8..15)
+        uint32_t kf[4];
+        const int r = nt * 8 + (lane & 7);
+        const int c = kk * 16 + (lane >> 3) * 8;
+        ldmatrix_x4(kf, cK + r * LD + c);
+        mma_16816(s[nt], qa[kk], kf[0], kf[1]);
+        if (kk + 1 < D / 16) mma_16816(s[nt], qa[kk + 1], kf[2], kf[3]);
       }
     }
     // scale (log2 domain) + key mask, row max
@@ -157,15 +191,16 @@ __global__ void __launch_bounds__(128)
       pa[3] = pack_half2(s[2 * kc + 1][2], s[2 * kc + 1][3]);
 #pragma unroll
       for (int dt = 0; dt < D / 8; dt += 2) {
-        const int mi = lane >> 3;  // which 8x8 matrix this lane addresses
+        const int mi = lane >> 3;
         const int vr = kc * 16 + (mi & 1) * 8 + (lane & 7);
         const int vc = (dt + (mi >> 1)) * 8;
         uint32_t vb[4];
-        ldmatrix_x4_trans(vb, &sV[vr * LD + vc]);
+        ldmatrix_x4_trans(vb, cV + vr * LD + vc);
         mma_16816(o[dt], pa, vb[0], vb[1]);
         mma_16816(o[dt + 1], pa, vb[2], vb[3]);
       }
     }
+    __syncthreads();  // everyone is done with this buffer before it is refilled
   }
 
 #pragma unroll
@@ -187,17 +222,33 @@ __global__ void __launch_bounds__(128)
   }
 }
 
+template <int D, int NW>
+static void launch_attn_t(const half* qkv, half* ctx, const int* cu, int n_seqs, int max_len, int groups,
+                          int n_heads, int hidden, long long group_rows, float scale_log2, cudaStream_t stream) {
+  constexpr int BQ = 16 * NW, LD = D + 8;
+  const size_t smem = (size_t)(BQ + 4 * 64) * LD * sizeof(half);
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(attn_kernel<D, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr_set = true;
+  }
+  dim3 grid((max_len + BQ - 1) / BQ, n_seqs, groups * n_heads);
+  launch_pdl(attn_kernel<D, NW>, grid, dim3(32 * NW), smem, stream, qkv, ctx, cu, n_heads, hidden, group_rows,
+             scale_log2);
+}
+
 void launch_attention(const half* qkv, half* ctx, const int* cu_seqlens, int n_seqs, int max_len, int groups,
                       int n_heads, int head_dim, int hidden, long long group_rows, cudaStream_t stream) {
   if (n_seqs <= 0 || max_len <= 0 || groups <= 0) return;
-  dim3 grid((max_len + 63) / 64, n_seqs, groups * n_heads);
   const float scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(head_dim));
-  if (head_dim == 64)
-    launch_pdl(attn_kernel<64>, grid, dim3(128), 0, stream, qkv, ctx, cu_seqlens, n_heads, hidden, group_rows,
-               scale_log2);
-  else
-    launch_pdl(attn_kernel<32>, grid, dim3(128), 0, stream, qkv, ctx, cu_seqlens, n_heads, hidden, group_rows,
-               scale_log2);
+  const bool big = max_len > 128;  // 128-query CTAs halve K/V re-reads on long sequences
+  if (head_dim == 64) {
+    if (big) launch_attn_t<64, 8>(qkv, ctx, cu_seqlens, n_seqs, max_len, groups, n_heads, hidden, group_rows, scale_log2, stream);
+    else launch_attn_t<64, 4>(qkv, ctx, cu_seqlens, n_seqs, max_len, groups, n_heads, hidden, group_rows, scale_log2, stream);
+  } else {
+    if (big) launch_attn_t<32, 8>(qkv, ctx, cu_seqlens, n_seqs, max_len, groups, n_heads, hidden, group_rows, scale_log2, stream);
+    else launch_attn_t<32, 4>(qkv, ctx, cu_seqlens, n_seqs, max_len, groups, n_heads, hidden, group_rows, scale_log2, stream);
+  }
 }
 
 }  // namespace sp

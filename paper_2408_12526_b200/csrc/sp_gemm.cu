@@ -18,7 +18,9 @@
 // previous kernel (attention / LayerNorm / another projection).
 //
 // Reference op: DenseLayer.forward, z = x @ W.T + b then act (nnkernel.py:66-76).
+#include <cstdlib>
 #include <type_traits>
+#include <vector>
 
 #include "sp_kernels.cuh"
 #include "sp_ptx.cuh"
@@ -28,10 +30,10 @@ namespace sp {
 static constexpr int kBlockM = 128;
 static constexpr int kBlockK = 64;                         // one 128-byte swizzle row of fp16
 static constexpr int kATileBytes = kBlockM * kBlockK * 2;  // 16 KiB
-static constexpr int kTmemCols = 128;                      // bn <= 128 fp32 columns
+static constexpr int kTmemCols = 256;                      // bn <= 256 fp32 columns
 static constexpr int kEpiWarps = 8;
 static constexpr int kThreads = 64 + 32 * kEpiWarps;
-static constexpr int kMaxBn = 128;
+static constexpr int kMaxBn = 256;
 
 template <int ACT>
 __device__ __forceinline__ float apply_act(float y) {
@@ -52,11 +54,14 @@ __global__ void __launch_bounds__(kThreads, 2)
   uint64_t* tmem_full = empty + p.stages;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
 
+  // m-tile fastest: the two CTAs of a cluster are neighbouring m-tiles of the same token tile
   int bid = blockIdx.x;
-  const int split = bid % p.splits;
-  bid /= p.splits;
+  const int mt = bid % p.m_tiles;
+  bid /= p.m_tiles;
   const int nt = bid % p.n_tiles;
-  const int mt = bid / p.n_tiles;
+  const int split = bid / p.n_tiles;
+  const bool pair = p.cluster == 2;
+  const uint32_t crank = pair ? cluster_ctarank() : 0u;
   const int g = blockIdx.y;
   const int m0 = mt * kBlockM;
   const int n0 = nt * p.bn;
@@ -72,7 +77,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < p.stages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], pair ? 2 : 1);  // a stage is free once every consumer in the pair released it
     }
     mbar_init(tmem_full, 1);
     fence_barrier_init();
@@ -86,6 +91,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   }
   tc_fence_before();
   __syncthreads();
+  if (pair) cluster_sync();  // peer barriers initialised before any multicast lands in them
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   pdl_launch_dependents();
@@ -93,16 +99,26 @@ __global__ void __launch_bounds__(kThreads, 2)
 
   if (warp == 0) {
     if (elect_one()) {
-      const uint64_t pol_w = policy_evict_first();  // weights: streamed once per request
+      // weights: streamed once per request -> evict_first, unless several token tiles re-read them
+      const uint64_t pol_w = (p.n_tiles > 1 && p.w_keep) ? policy_evict_last() : policy_evict_first();
       const uint64_t pol_x = policy_evict_last();   // activations: re-read by every M tile
       const int wrow = g * p.n_out + m0;
       const int xrow = g * p.x_group_rows + n0;
+      // token tile: alone, or (pair) this CTA's half multicast into both CTAs of the cluster
+      const int r_begin = pair ? static_cast<int>(crank) * (p.bn >> 1) : 0;
+      const int r_end = pair ? r_begin + (p.bn >> 1) : p.bn;
       auto load_x = [&](int s, int kb) {
         uint8_t* sb = smem + s * stage_bytes + kATileBytes;
         const int kc = kb * kBlockK;
-        int r = 0;
-        for (; r + 64 <= p.bn; r += 64) tma_load_2d(&map_x64, &full[s], sb + r * 128, kc, xrow + r, pol_x);
-        for (; r < p.bn; r += 16) tma_load_2d(&map_x16, &full[s], sb + r * 128, kc, xrow + r, pol_x);
+        int r = r_begin;
+        if (pair) {
+          for (; r + 64 <= r_end; r += 64)
+            tma_load_2d_mc(&map_x64, &full[s], sb + r * 128, kc, xrow + r, 0x3, pol_x);
+          for (; r < r_end; r += 16) tma_load_2d_mc(&map_x16, &full[s], sb + r * 128, kc, xrow + r, 0x3, pol_x);
+        } else {
+          for (; r + 64 <= r_end; r += 64) tma_load_2d(&map_x64, &full[s], sb + r * 128, kc, xrow + r, pol_x);
+          for (; r < r_end; r += 16) tma_load_2d(&map_x16, &full[s], sb + r * 128, kc, xrow + r, pol_x);
+        }
       };
       // 1) weight prefetch of the first stages: independent of the previous kernel
       const int n_pre = min(p.stages, kb1 - kb0);
@@ -145,7 +161,8 @@ __global__ void __launch_bounds__(kThreads, 2)
           // +32 bytes per K=16 slice inside the 128-byte swizzle row (address field in 16-byte units)
           umma_f16_ss(tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
         }
-        umma_commit(&empty[s]);
+        if (pair) umma_commit_mc(&empty[s], 0x3);
+        else umma_commit(&empty[s]);
         if (++s == p.stages) {
           s = 0;
           ph ^= 1;
@@ -187,14 +204,17 @@ __global__ void __launch_bounds__(kThreads, 2)
         for (int i = 0; i < n; i += 8) tmem_ld8_nowait(taddr + c + i, r + i);
       }
       tmem_wait_ld();
+      // all 32 columns unconditionally: independent chains interleave (rows >= n are never stored)
+      float y[32];
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
-        if (j < n) {
-          float y = has_k ? __uint_as_float(r[j]) : 0.f;
-          if (!partial) y = apply_act<ACT>(y + bias);
-          if constexpr (OUT_F32) stage[j * 32 + lane] = y;
-          else stage[j * 32 + lane] = __float2half_rn(y);
-        }
+        y[j] = has_k ? __uint_as_float(r[j]) : 0.f;
+        if (!partial) y[j] = apply_act<ACT>(y[j] + bias);
+      }
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        if constexpr (OUT_F32) stage[j * 32 + lane] = y[j];
+        else stage[j * 32 + lane] = __float2half_rn(y[j]);
       }
       __syncwarp();
       const int sub = lane % kLanesPerRow;
@@ -214,6 +234,7 @@ __global__ void __launch_bounds__(kThreads, 2)
 
   tc_fence_before();
   __syncthreads();
+  if (pair) cluster_sync();  // no CTA leaves while its peer may still signal its barriers
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem, kTmemCols);
@@ -224,26 +245,44 @@ __global__ void __launch_bounds__(kThreads, 2)
 // holds the number of CTAs recorded so far, host-side mirror in g_trace_used).
 static unsigned long long* g_trace = nullptr;
 static size_t g_trace_used = 0;
+static std::vector<int> g_trace_counts;
 void set_gemm_trace(unsigned long long* buf) {
   g_trace = buf;
   g_trace_used = 0;
+  g_trace_counts.clear();
+}
+int gemm_trace_counts(int* out, int max) {
+  const int n = static_cast<int>(g_trace_counts.size());
+  for (int i = 0; i < n && i < max; ++i) out[i] = g_trace_counts[i];
+  return n;
 }
 
 size_t gemm_smem_bytes(int bn, int stages) {
   return static_cast<size_t>(stages) * (kATileBytes + bn * 128) + 1024 /*align*/ + 256 /*barriers*/;
 }
 
-void gemm_configure_tiles(int t_rows, int* bn, int* n_tiles, int* stages) {
-  int tiles = (t_rows + kMaxBn - 1) / kMaxBn;
+// Tile policy knobs (tuning sweeps): SP_GEMM_MAXBN (16..256, default 128), SP_GEMM_SMEM_KB.
+static int env_int(const char* name, int dflt, int lo, int hi) {
+  const char* v = getenv(name);
+  if (!v) return dflt;
+  int x = atoi(v);
+  return x < lo ? lo : (x > hi ? hi : x);
+}
+
+void gemm_configure_tiles(int t_rows, bool cluster2, int* bn, int* n_tiles, int* stages) {
+  static const int max_bn = env_int("SP_GEMM_MAXBN", 128, 16, kMaxBn);
+  static const int smem_kb = env_int("SP_GEMM_SMEM_KB", 96, 40, 200);
+  int tiles = (t_rows + max_bn - 1) / max_bn;
   if (tiles < 1) tiles = 1;
   const int per = (t_rows + tiles - 1) / tiles;
-  int b = ((per + 15) / 16) * 16;
-  if (b < 16) b = 16;
+  const int gran = cluster2 ? 32 : 16;  // a pair splits the tile in halves of whole 16-row boxes
+  int b = ((per + gran - 1) / gran) * gran;
+  if (b < gran) b = gran;
   *bn = b;
   *n_tiles = tiles;
   // ~96 KiB per CTA so that two CTAs (e.g. the tail of one projection and the prefetching head
-  // of the next) share an SM: smem 2 x ~97 KiB, TMEM 2 x 128 columns.
-  int st = (96 * 1024) / (kATileBytes + b * 128);
+  // of the next, or two tiles of one projection) share an SM: smem 2 x ~97 KiB, TMEM 2 x 256 cols.
+  int st = (smem_kb * 1024) / (kATileBytes + b * 128);
   if (st > 6) st = 6;
   if (st < 2) st = 2;
   *stages = st;
@@ -261,14 +300,21 @@ static void launch_gemm_t(const GemmMaps& maps, const GemmParams& p, int groups,
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = gemm_smem_bytes(p.bn, p.stages);
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = p.cluster;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   GemmParams q = p;
   q.trace = g_trace ? g_trace + 8 * g_trace_used : nullptr;
-  if (g_trace) g_trace_used += (size_t)cfg.gridDim.x * cfg.gridDim.y;
+  if (g_trace) {
+    g_trace_used += (size_t)cfg.gridDim.x * cfg.gridDim.y;
+    g_trace_counts.push_back(static_cast<int>(cfg.gridDim.x * cfg.gridDim.y));
+  }
   cudaLaunchKernelEx(&cfg, gemm_kernel<ACT, OUT_F32>, maps.w, maps.x64, maps.x16, q);
 }
 

@@ -56,10 +56,13 @@ struct GemmParams {
   int act;
   int out_f32;
   unsigned long long* trace;  // debug: 8 globaltimer stamps per CTA, or null
+  int cluster;                // 1, or 2: CTA pairs along M share the token tile via TMA multicast
+  int w_keep;                 // keep weight tiles in L2 (evict_last) when n_tiles > 1
 };
 
 // Debug hook: when set, every GEMM launch records a per-CTA timeline into this device buffer.
 void set_gemm_trace(unsigned long long* buf);
+int gemm_trace_counts(int* out, int max);
 
 struct GemmMaps {
   CUtensorMap w;    // box {64, 128}
@@ -69,7 +72,7 @@ struct GemmMaps {
 
 void launch_gemm(const GemmMaps& maps, const GemmParams& p, int groups, cudaStream_t stream);
 size_t gemm_smem_bytes(int bn, int stages);
-void gemm_configure_tiles(int t_rows, int* bn, int* n_tiles, int* stages);
+void gemm_configure_tiles(int t_rows, bool cluster2, int* bn, int* n_tiles, int* stages);
 
 // Unpadded multi-head attention over cu_seqlens-packed sequences.
 //   qkv: fp16 [groups][x_group_rows][3H] (Q | K | V, head h at columns h*D within each third)

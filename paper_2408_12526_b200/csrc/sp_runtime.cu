@@ -326,8 +326,18 @@ int run_gemm(sp_group* grp, int kind, const CUtensorMap& wmap, const XMaps& xm, 
   p.k_dim = k_dim;
   p.t_rows = t_rows;
   p.x_group_rows = x_group_rows;
-  sp::gemm_configure_tiles(t_rows, &p.bn, &p.n_tiles, &p.stages);
   p.m_tiles = n_out / 128;
+  static const bool cluster_on = [] {
+    const char* v = getenv("SP_GEMM_CLUSTER");
+    return v != nullptr && atoi(v) != 0;  // measured slower at every length: off by default
+  }();
+  p.cluster = (cluster_on && p.m_tiles % 2 == 0 && t_rows > 16) ? 2 : 1;
+  static const int w_keep = [] {
+    const char* v = getenv("SP_GEMM_WKEEP");
+    return v == nullptr ? 1 : atoi(v);
+  }();
+  p.w_keep = w_keep;
+  sp::gemm_configure_tiles(t_rows, p.cluster == 2, &p.bn, &p.n_tiles, &p.stages);
   p.splits = splits;
   p.kb_per_split = (k_dim / 64) / splits;
   p.out = out;
@@ -371,7 +381,7 @@ int bert_forward(sp_group* g, const int32_t* ids, const int32_t* cu, int n_seqs,
     g->rec_end();
     ++launches;
     int bn, n_tiles, stages;
-    sp::gemm_configure_tiles(n_tokens, &bn, &n_tiles, &stages);
+    sp::gemm_configure_tiles(n_tokens, false, &bn, &n_tiles, &stages);
     const int s_o = choose_splits(k * (H / 128) * n_tiles, H / 64, kMaxSplits);
     const int s_f = choose_splits(k * (H / 128) * n_tiles, F / 64, kMaxSplits);
     const long long part_ss = (long long)S * xgs;
@@ -557,6 +567,10 @@ int sp_op_gemm(const void* w, const void* x, int32_t groups, int32_t n_out, int3
 int sp_debug_set_gemm_trace(void* device_buf) {
   sp::set_gemm_trace(static_cast<unsigned long long*>(device_buf));
   return SP_OK;
+}
+
+int sp_debug_gemm_trace_launches(int32_t* ctas_per_launch, int32_t max_launches) {
+  return sp::gemm_trace_counts(ctas_per_launch, max_launches);
 }
 
 int sp_op_attention(const void* qkv, void* ctx, const int32_t* cu_seqlens, int32_t n_seqs, int32_t max_seq_len,

@@ -20,6 +20,9 @@ for L in [int(x) for x in sys.argv[1].split(",")]:
     graph = torch.cuda.CUDAGraph()
     with torch.cuda.graph(graph):
         run()
+    import ctypes
+    cnt = (ctypes.c_int32 * 64)()
+    sizes = list(cnt[:lib.sp_debug_gemm_trace_launches(cnt, 64)])
     lib.sp_debug_set_gemm_trace(None)
     for _ in range(3): graph.replay()
     fw.zero_(); fr.sum(); torch.cuda.synchronize()
@@ -29,21 +32,6 @@ for L in [int(x) for x in sys.argv[1].split(",")]:
     t = tr.view(-1, 8).cpu().numpy().astype(np.float64)
     t = t[t[:, 0] > 0]
     base = t[:, 0].min()
-    # split CTAs into launches by grid sizes
-    bn = -(-L // (-(-L // 128))) ; bn = ((bn + 15) // 16) * 16; nt = -(-L // 128)
-    def grid(N, splits): return K * (N // 128) * nt * splits
-    import math
-    H, F = 768, 3072
-    def ch(units, nkb):
-        best = 1
-        for s in range(1, 5):
-            if nkb % s: continue
-            if s > 1 and nkb // s < 2: continue
-            best = s
-            if units * s >= 128: break
-        return best
-    so = ch(K * 6 * nt, 12); sf = ch(K * 6 * nt, 48)
-    sizes = [grid(3 * H, 1), grid(H, so), grid(F, 1), grid(H, sf)] * 2 + [K * 6]
     off = 0
     print(f"L={L}: event {e0.elapsed_time(e1)*1e3:.1f} us")
     for nm, n in zip(names, sizes):
