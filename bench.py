@@ -51,6 +51,8 @@ def parse_args():
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="bounded CPU-baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-steps", type=int, default=200)
+    ap.add_argument("--batch", type=int, default=1,
+                    help="requests per step, packed unpadded with cu_seqlens (1 = batch-1 streaming)")
     return ap.parse_args()
 
 
@@ -77,10 +79,11 @@ def make_requests(n, seed, lo, hi, vocab):
 def workload_config(args, cfg, K, world):
     return {
         "workload": f"{args.config}: K={K} BERT-style 2-layer students, H={cfg.hidden}, {cfg.n_heads} heads, "
-                    f"F={cfg.ffn}, batch-1 ragged L~U{{{args.len_min}..{args.len_max}}}, random-init",
+                    f"F={cfg.ffn}, {'batch-1' if args.batch == 1 else f'batches of {args.batch}'} ragged "
+                    f"L~U{{{args.len_min}..{args.len_max}}} (unpadded), random-init",
         "model": "student group (boosting sum of K flat BERT-style students)",
         "K": K, "hidden": cfg.hidden, "heads": cfg.n_heads, "layers": cfg.n_layers, "ffn": cfg.ffn,
-        "global_batch": 1, "seq_len": [args.len_min, args.len_max], "k_active": K,
+        "global_batch": args.batch, "seq_len": [args.len_min, args.len_max], "k_active": K,
         "students_per_gpu": [len(s) for s in __import__("paper_2408_12526_b200.parallel", fromlist=["x"]).placement(K, world)],
         "parallelism": f"student-parallel x{world}" if world > 1 else "single GPU",
         "l2": "flushed before every timed request: 256 MiB write + 256 MiB read (> 126 MB L2)",
@@ -221,16 +224,24 @@ def run_engine(args):
 
     cfg, K = PRESETS[args.config]
     dev = torch.device("cuda", local_rank)
+    B = args.batch
     grp = ShardedStudentGroup(cfg, K, seed=args.seed, rank=rank, world=world, device=local_rank,
-                              max_tokens=args.len_max, max_seqs=1)
-    n_req = args.steps + args.warmup
-    reqs = make_requests(n_req, args.seed, args.len_min, args.len_max, cfg.vocab)
-    # inputs resident in HBM before the timed region
-    lens = np.array([len(r) for r in reqs], np.int64)
-    offs = np.concatenate([[0], np.cumsum(lens)])
-    ids_all = torch.from_numpy(np.concatenate(reqs).astype(np.int32)).to(dev)
-    cu_all = torch.from_numpy(np.stack([np.zeros(n_req, np.int32), lens.astype(np.int32)], 1).copy()).to(dev)
-    logits = torch.empty((1, cfg.n_classes), dtype=torch.float32, device=dev)
+                              max_tokens=args.len_max * B, max_seqs=B)
+    n_steps = args.steps + args.warmup
+    reqs = make_requests(n_steps * B, args.seed, args.len_min, args.len_max, cfg.vocab)
+    # one step = B requests packed back to back (no padding); inputs resident in HBM before timing
+    step_ids, step_cu, step_tok, step_max = [], [], [], []
+    for i in range(n_steps):
+        batch = reqs[i * B:(i + 1) * B]
+        ln = np.array([len(r) for r in batch], np.int64)
+        step_ids.append(np.concatenate(batch).astype(np.int32))
+        step_cu.append(np.concatenate([[0], np.cumsum(ln)]).astype(np.int32))
+        step_tok.append(int(ln.sum()))
+        step_max.append(int(ln.max()))
+    offs = np.concatenate([[0], np.cumsum(step_tok)])
+    ids_all = torch.from_numpy(np.concatenate(step_ids)).to(dev)
+    cu_all = torch.from_numpy(np.stack(step_cu)).to(dev)
+    logits = torch.empty((B, cfg.n_classes), dtype=torch.float32, device=dev)
     flush_w = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
     flush_r = torch.ones(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
 
@@ -241,8 +252,8 @@ def run_engine(args):
         flush_r.sum()
 
     def step(i):
-        L = int(lens[i])
-        grp.forward_packed_device(ids_all[offs[i]: offs[i] + L], cu_all[i], 1, L, L, K, logits)
+        T = step_tok[i]
+        grp.forward_packed_device(ids_all[offs[i]: offs[i] + T], cu_all[i], B, T, step_max[i], K, logits)
 
     def barrier():
         if world > 1:
@@ -274,7 +285,7 @@ def run_engine(args):
         dist.all_reduce(step_ms, op=dist.ReduceOp.MAX)
     step_ms = step_ms.cpu().numpy()
     total_s = float(step_ms.sum()) / 1e3
-    value = args.steps / total_s
+    value = args.steps * B / total_s
 
     # ---- roofline: per-launch CUDA events on an instrumented replay of the timed requests
     grp.local.set_profiling(True)
@@ -314,13 +325,19 @@ def run_engine(args):
             traffic = json.loads(tfile.read_text()).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
+    tflops = g_flops / (g_ms / 1e3) / 1e12 if g_ms > 0 else 0.0
+    if B == 1:  # batch-1: weight streaming, HBM-bound
+        bound, ach, peak, unit = "hbm", achieved, hbm_peak, "GB/s"
+    else:  # batched: dense contraction, tensor-bound
+        bound, ach, peak, unit = "tensor", tflops, tc_peak, "TFLOP/s"
     roofline = {
-        "bound": "hbm", "kernel": "gemm_kernel (tcgen05 grouped projection: QKV/O/FFN1/FFN2/pooler)",
-        "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
+        "bound": bound, "kernel": "gemm_kernel / gemm_persistent_kernel (tcgen05 grouped projections)",
+        "achieved": ach, "peak": peak, "unit": unit, "frac": ach / peak,
+        "hbm_achieved_gbs": achieved, "hbm_peak_gbs": hbm_peak,
         "traffic": traffic, "peak_source": peak_src,
         "algorithmic_bytes_per_launch": g_bytes / max(g_launches, 1),
         "avg_launch_us": 1e3 * g_ms / max(g_launches, 1),
-        "tensor_tflops": g_flops / (g_ms / 1e3) / 1e12 if g_ms > 0 else 0.0, "tensor_peak_tflops": tc_peak,
+        "tensor_tflops": tflops, "tensor_peak_tflops": tc_peak,
         "gemm_share_of_step": g_ms / step_total_ms if step_total_ms else None,
         "method": f"CUDA events around every launch on the launching stream, instrumented replay of {n_prof} timed requests",
         "per_kind_ms_per_request": {k: v[0] / n_prof for k, v in sorted(agg.items())},
@@ -333,8 +350,8 @@ def run_engine(args):
     roofline["request_hbm_frac_p50"] = (req_bytes_local / (nearest_rank(step_ms, 50) / 1e3) / 1e9) / hbm_peak
 
     # ---- e2e through the public API with host buffers
-    pinned_ids = [torch.from_numpy(r).pin_memory() for r in reqs]
-    pinned_cu = [torch.tensor([0, len(r)], dtype=torch.int32).pin_memory() for r in reqs]
+    pinned_ids = [torch.from_numpy(r).pin_memory() for r in step_ids]
+    pinned_cu = [torch.from_numpy(c).pin_memory() for c in step_cu]
     e2e_s = []
     barrier()
     for j in range(args.steps):
@@ -351,9 +368,9 @@ def run_engine(args):
     if world > 1:
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
     e2e_s = e2e_t.cpu().numpy()
-    e2e = {"value": args.steps / float(e2e_s.sum()), "unit": UNIT,
-           "h2d_bytes_per_step": float(np.mean([4 * (len(r) + 2) for r in reqs[args.warmup:]])),
-           "d2h_bytes_per_step": 4 * cfg.n_classes,
+    e2e = {"value": args.steps * B / float(e2e_s.sum()), "unit": UNIT,
+           "h2d_bytes_per_step": float(np.mean([4 * (t + B + 1) for t in step_tok[args.warmup:]])),
+           "d2h_bytes_per_step": 4 * cfg.n_classes * B,
            "p50_ms": 1e3 * nearest_rank(e2e_s, 50), "p99_ms": 1e3 * nearest_rank(e2e_s, 99),
            "api": "StudentGroup.forward_host (C ABI sp_group_forward_host)" if world == 1 else
                   "ShardedStudentGroup.forward_host (pinned H2D, engine, NCCL all-reduce, D2H)"}

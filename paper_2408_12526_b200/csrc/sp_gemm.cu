@@ -243,6 +243,273 @@ __global__ void __launch_bounds__(kThreads, 2)
 
 // Debug trace: launches append their per-CTA stamps one after another (slot 0 of the buffer
 // holds the number of CTAs recorded so far, host-side mirror in g_trace_used).
+static void g_trace_counts_push(int n);
+static bool trace_on();
+
+// ============================================================================ persistent variant
+// For large token counts (T > 128: long batch-1 requests, batched load) one CTA per SM loops over
+// output tiles (128 features x bn tokens, bn <= 256) with a continuous TMA ring and two TMEM
+// accumulators: the MMAs of tile i+1 run while the 8 epilogue warps drain tile i, so neither the
+// pipeline fill nor the epilogue is paid per tile, and there are no partial waves. Tiles are
+// ordered m-tile fastest, so concurrently running CTAs share one token tile (L2 hits).
+static constexpr int kPersistTmemCols = 512;  // 2 accumulators x 256 columns
+
+template <int ACT, bool OUT_F32>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_persistent_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_x64,
+                           const __grid_constant__ CUtensorMap map_x16, const GemmParams p) {
+  using OutT = typename std::conditional<OUT_F32, float, half>::type;
+  constexpr int kRowBytes = 32 * static_cast<int>(sizeof(OutT));
+  constexpr int kLanesPerRow = kRowBytes / 16;
+  constexpr int kRowsPerPass = 32 / kLanesPerRow;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int stage_bytes = kATileBytes + p.bn * 128;
+  uint8_t* staging = smem + p.stages * stage_bytes;  // 8 warps x 32 rows x kRowBytes
+  uint64_t* full = reinterpret_cast<uint64_t*>(staging + kEpiWarps * 32 * kRowBytes);
+  uint64_t* empty = full + p.stages;
+  uint64_t* acc_full = empty + p.stages;  // [2]
+  uint64_t* acc_empty = acc_full + 2;     // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+  const int warp = warp_id();
+  const int lane = lane_id();
+  const int units_per_group = p.m_tiles * p.n_tiles;
+  const int units = units_per_group * p.groups;
+  const int nkb = p.k_dim / kBlockK;
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < p.stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], kEpiWarps);
+    }
+    fence_barrier_init();
+    tma_prefetch_desc(&map_w);
+    tma_prefetch_desc(&map_x64);
+    tma_prefetch_desc(&map_x16);
+  }
+  if (warp == 1) {
+    tmem_alloc(tmem_slot, kPersistTmemCols);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  pdl_launch_dependents();
+
+  auto decode = [&](int u, int& g, int& mt, int& nt) {
+    g = u / units_per_group;
+    const int r = u % units_per_group;
+    nt = r / p.m_tiles;
+    mt = r % p.m_tiles;
+  };
+
+  if (warp == 0) {
+    if (elect_one()) {
+      const uint64_t pol_w = policy_evict_last();  // re-read by the other token tiles
+      const uint64_t pol_x = policy_evict_last();
+      int s = 0;
+      uint32_t ph = 0;
+      bool first = true;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        int g, mt, nt;
+        decode(u, g, mt, nt);
+        const int wrow = g * p.n_out + mt * kBlockM;
+        const int xrow = g * p.x_group_rows + nt * p.bn;
+        int kb = 0;
+        if (first) {  // weight prefetch of the first stages before the dependency wait
+          const int n_pre = min(p.stages, nkb);
+          for (int i = 0; i < n_pre; ++i) {
+            mbar_arrive_expect_tx(&full[i], stage_bytes);
+            tma_load_2d(&map_w, &full[i], smem + i * stage_bytes, i * kBlockK, wrow, pol_w);
+          }
+          pdl_wait();
+          for (int i = 0; i < n_pre; ++i) {
+            uint8_t* sb = smem + i * stage_bytes + kATileBytes;
+            int r = 0;
+            for (; r + 64 <= p.bn; r += 64) tma_load_2d(&map_x64, &full[i], sb + r * 128, i * kBlockK, xrow + r, pol_x);
+            for (; r < p.bn; r += 16) tma_load_2d(&map_x16, &full[i], sb + r * 128, i * kBlockK, xrow + r, pol_x);
+          }
+          kb = n_pre;
+          s = n_pre % p.stages;
+          ph = (n_pre == p.stages) ? 1u : 0u;
+          first = false;
+        }
+        for (; kb < nkb; ++kb) {
+          mbar_wait(&empty[s], ph ^ 1);
+          mbar_arrive_expect_tx(&full[s], stage_bytes);
+          uint8_t* sa = smem + s * stage_bytes;
+          tma_load_2d(&map_w, &full[s], sa, kb * kBlockK, wrow, pol_w);
+          uint8_t* sb = sa + kATileBytes;
+          int r = 0;
+          for (; r + 64 <= p.bn; r += 64) tma_load_2d(&map_x64, &full[s], sb + r * 128, kb * kBlockK, xrow + r, pol_x);
+          for (; r < p.bn; r += 16) tma_load_2d(&map_x16, &full[s], sb + r * 128, kb * kBlockK, xrow + r, pol_x);
+          if (++s == p.stages) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+      }
+      if (first) pdl_wait();  // no work: still honour the dependency
+    }
+  } else if (warp == 1) {
+    if (elect_one()) {
+      const uint32_t idesc = umma_idesc_f16(kBlockM, p.bn);
+      int s = 0;
+      uint32_t ph = 0;
+      int j = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
+        const int b = j & 1;
+        mbar_wait(&acc_empty[b], ((j >> 1) & 1) ^ 1);  // epilogue drained this accumulator
+        tc_fence_after();
+        const uint32_t acc = tmem + static_cast<uint32_t>(b * 256);
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + s * stage_bytes);
+          const uint64_t adesc = umma_sdesc_sw128(sa);
+          const uint64_t bdesc = umma_sdesc_sw128(sa + kATileBytes);
+#pragma unroll
+          for (int k = 0; k < kBlockK / 16; ++k)
+            umma_f16_ss(acc, adesc + 2 * k, bdesc + 2 * k, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+          umma_commit(&empty[s]);
+          if (++s == p.stages) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+        umma_commit(&acc_full[b]);
+      }
+    }
+    __syncwarp();
+  } else {
+    const int e = warp - 2;
+    const int q = warp & 3;
+    const int half_cols = p.bn >> 1;
+    const int c_begin = (e >> 2) * half_cols;
+    OutT* stage = reinterpret_cast<OutT*>(staging + e * 32 * kRowBytes);
+    int j = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
+      int g, mt, nt;
+      decode(u, g, mt, nt);
+      const int b = j & 1;
+      const int m0 = mt * kBlockM, n0 = nt * p.bn;
+      const int feat = m0 + q * 32 + lane;
+      const float bias = p.bias ? __ldg(p.bias + (long long)g * p.bias_group_stride + feat) : 0.f;
+      OutT* out = reinterpret_cast<OutT*>(p.out) + (long long)g * p.out_group_stride + m0 + q * 32;
+      mbar_wait(&acc_full[b], (j >> 1) & 1);
+      tc_fence_after();
+      const uint32_t taddr = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(b * 256);
+      for (int c = c_begin; c < c_begin + half_cols; c += 32) {
+        const int n = min(32, c_begin + half_cols - c);
+        uint32_t r[32];
+        if (n == 32) {
+          tmem_ld32_nowait(taddr + c, r);
+        } else {
+          for (int i = 0; i < n; i += 8) tmem_ld8_nowait(taddr + c + i, r + i);
+        }
+        tmem_wait_ld();
+        if (c + 32 >= c_begin + half_cols) {  // last TMEM read of this tile: hand the accumulator back
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&acc_empty[b]);
+        }
+        float y[32];
+#pragma unroll
+        for (int jj = 0; jj < 32; ++jj) y[jj] = apply_act<ACT>(__uint_as_float(r[jj]) + bias);
+#pragma unroll
+        for (int jj = 0; jj < 32; ++jj) {
+          if constexpr (OUT_F32) stage[jj * 32 + lane] = y[jj];
+          else stage[jj * 32 + lane] = __float2half_rn(y[jj]);
+        }
+        __syncwarp();
+        const int sub = lane % kLanesPerRow;
+        for (int j0 = 0; j0 < n; j0 += kRowsPerPass) {
+          const int jr = j0 + lane / kLanesPerRow;
+          const int t = n0 + c + jr;
+          if (jr < n && t < p.t_rows) {
+            const uint4 v = *reinterpret_cast<const uint4*>(reinterpret_cast<const uint8_t*>(stage) + jr * kRowBytes +
+                                                            sub * 16);
+            *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(out + (long long)t * p.out_ld) + sub * 16) = v;
+          }
+        }
+        __syncwarp();
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, kPersistTmemCols);
+  }
+}
+
+template <int ACT, bool OUT_F32>
+static void launch_persistent_t(const GemmMaps& maps, const GemmParams& p, int groups, cudaStream_t stream) {
+  static int n_sm = 0;
+  if (n_sm == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(gemm_persistent_kernel<ACT, OUT_F32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         227 * 1024);
+  }
+  GemmParams q = p;
+  q.groups = groups;
+  q.trace = nullptr;
+  const int units = groups * p.m_tiles * p.n_tiles;
+  const int row_bytes = 32 * (OUT_F32 ? 4 : 2);
+  const size_t smem = static_cast<size_t>(p.stages) * (kATileBytes + p.bn * 128) + kEpiWarps * 32 * row_bytes +
+                      1024 + 256;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(units < n_sm ? units : n_sm);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (trace_on()) g_trace_counts_push(static_cast<int>(cfg.gridDim.x));
+  cudaLaunchKernelEx(&cfg, gemm_persistent_kernel<ACT, OUT_F32>, maps.w, maps.x64, maps.x16, q);
+}
+
+// Tile policy of the persistent path: bn <= 256, ring as deep as the smem left after staging.
+void gemm_configure_persistent(int t_rows, bool out_f32, int* bn, int* n_tiles, int* stages) {
+  int tiles = (t_rows + 255) / 256;
+  const int per = (t_rows + tiles - 1) / tiles;
+  int b = ((per + 15) / 16) * 16;
+  *bn = b;
+  *n_tiles = tiles;
+  const int staging = kEpiWarps * 32 * 32 * (out_f32 ? 4 : 2);
+  int st = (224 * 1024 - staging) / (kATileBytes + b * 128);
+  if (st > 8) st = 8;
+  if (st < 2) st = 2;
+  *stages = st;
+}
+
+void launch_gemm_persistent(const GemmMaps& maps, const GemmParams& p, int groups, cudaStream_t stream) {
+  const bool f32 = p.out_f32 != 0;
+  if (p.act == ACT_GELU) {
+    if (f32) launch_persistent_t<ACT_GELU, true>(maps, p, groups, stream);
+    else launch_persistent_t<ACT_GELU, false>(maps, p, groups, stream);
+  } else if (p.act == ACT_TANH) {
+    if (f32) launch_persistent_t<ACT_TANH, true>(maps, p, groups, stream);
+    else launch_persistent_t<ACT_TANH, false>(maps, p, groups, stream);
+  } else {
+    if (f32) launch_persistent_t<ACT_NONE, true>(maps, p, groups, stream);
+    else launch_persistent_t<ACT_NONE, false>(maps, p, groups, stream);
+  }
+}
+
 static unsigned long long* g_trace = nullptr;
 static size_t g_trace_used = 0;
 static std::vector<int> g_trace_counts;
@@ -251,6 +518,8 @@ void set_gemm_trace(unsigned long long* buf) {
   g_trace_used = 0;
   g_trace_counts.clear();
 }
+static void g_trace_counts_push(int n) { g_trace_counts.push_back(n); }
+static bool trace_on() { return g_trace != nullptr; }
 int gemm_trace_counts(int* out, int max) {
   const int n = static_cast<int>(g_trace_counts.size());
   for (int i = 0; i < n && i < max; ++i) out[i] = g_trace_counts[i];

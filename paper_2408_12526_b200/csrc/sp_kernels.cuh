@@ -58,6 +58,7 @@ struct GemmParams {
   unsigned long long* trace;  // debug: 8 globaltimer stamps per CTA, or null
   int cluster;                // 1, or 2: CTA pairs along M share the token tile via TMA multicast
   int w_keep;                 // keep weight tiles in L2 (evict_last) when n_tiles > 1
+  int groups;                 // students in the launch (persistent path)
 };
 
 // Debug hook: when set, every GEMM launch records a per-CTA timeline into this device buffer.
@@ -71,6 +72,9 @@ struct GemmMaps {
 };
 
 void launch_gemm(const GemmMaps& maps, const GemmParams& p, int groups, cudaStream_t stream);
+// Persistent variant for large token counts (splits must be 1).
+void launch_gemm_persistent(const GemmMaps& maps, const GemmParams& p, int groups, cudaStream_t stream);
+void gemm_configure_persistent(int t_rows, bool out_f32, int* bn, int* n_tiles, int* stages);
 size_t gemm_smem_bytes(int bn, int stages);
 void gemm_configure_tiles(int t_rows, bool cluster2, int* bn, int* n_tiles, int* stages);
 
@@ -94,9 +98,11 @@ void launch_reduce_ln(const float* part, int splits, long long part_split_stride
                       long long cls_gs, cudaStream_t stream);
 
 // Boosting sum + shared classifier (distill.py:169-178, :512):
+//   final[m][b] = splits ? tanh(sum_s part[s][m][b] + b_pool[m]) : final_rep[m][b]
 //   rep[b] = sum_{m < groups} alpha[m] * final[m][b];  logits[b] = W_c rep[b] (+ b_c)
-void launch_head(const float* final_rep, long long final_gs, int groups, const float* alpha, const float* w_cls,
-                 const float* b_cls, int n_classes, int hidden, int n_rows, int add_bias, float* rep,
-                 float* logits, cudaStream_t stream);
+void launch_head(const float* final_rep, long long final_gs, long long split_stride, int splits,
+                 const float* b_pool, int groups, const float* alpha, const float* w_cls, const float* b_cls,
+                 int n_classes, int hidden, int n_rows, int add_bias, float* rep, float* logits,
+                 cudaStream_t stream);
 
 }  // namespace sp

@@ -160,46 +160,73 @@ __global__ void __launch_bounds__(128)
                        x16 + row, cls_row);
 }
 
-// One CTA per output row b. rep is accumulated over students in index order (distill.py:174-177);
-// the student loads are batched 8 at a time so they are in flight together.
-__global__ void __launch_bounds__(256)
-    head_kernel(const float* __restrict__ final_rep, long long final_gs, int groups, const float* __restrict__ alpha,
+// One CTA per output row b, one thread per feature j (blockDim = hidden <= 1024).
+// Final representation of student m: either given (`splits == 0`: final_rep already activated), or
+// the pooler's split-K partial sums, finished here: tanh(sum_s part[s][m][b][j] + b_pool[m][j]).
+// rep[b][j] = sum_{m < groups} alpha_m * final_m[b][j] accumulated in student order
+// (distill.py:174-177); logits[b][c] = sum_j W_c[c][j] rep[b][j] (+ b_c once).
+// All student/split loads of a thread are issued together (8 students x up to 4 splits).
+__global__ void __launch_bounds__(1024)
+    head_kernel(const float* __restrict__ final_rep, long long final_gs, long long split_stride, int splits,
+                const float* __restrict__ b_pool, int groups, const float* __restrict__ alpha,
                 const float* __restrict__ w_cls, const float* __restrict__ b_cls, int n_classes, int hidden,
                 int add_bias, float* __restrict__ rep, float* __restrict__ logits) {
   pdl_wait();
   pdl_launch_dependents();
-  extern __shared__ float srep[];
-  __shared__ float red[8];
+  __shared__ float red[32][4];
   const int b = blockIdx.x;
-  for (int j = threadIdx.x; j < hidden; j += blockDim.x) {
-    float r = 0.f;
+  const int j = threadIdx.x;
+  const int nsp = splits > 0 ? splits : 1;
+  float r = 0.f;
+  if (j < hidden) {
     for (int m0 = 0; m0 < groups; m0 += 8) {
-      float vals[8], al[8];
+      float vals[8][kMaxSplitsRow], bp[8], al[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const bool ok = m0 + i < groups;
-        vals[i] = ok ? final_rep[(m0 + i) * final_gs + (long long)b * hidden + j] : 0.f;
+        const long long base = (long long)(m0 + i) * final_gs + (long long)b * hidden + j;
+#pragma unroll
+        for (int s = 0; s < kMaxSplitsRow; ++s) vals[i][s] = (ok && s < nsp) ? final_rep[base + s * split_stride] : 0.f;
+        bp[i] = (ok && splits > 0) ? __ldg(b_pool + (long long)(m0 + i) * hidden + j) : 0.f;
         al[i] = ok ? __ldg(alpha + m0 + i) : 0.f;
       }
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
-        if (m0 + i < groups) r += al[i] * vals[i];
+      for (int i = 0; i < 8; ++i) {
+        if (m0 + i < groups) {
+          float v;
+          if (splits > 0) {
+            v = vals[i][0];
+#pragma unroll
+            for (int s = 1; s < kMaxSplitsRow; ++s)
+              if (s < splits) v += vals[i][s];
+            v = tanhf(v + bp[i]);
+          } else {
+            v = vals[i][0];
+          }
+          r += al[i] * v;
+        }
+      }
     }
-    srep[j] = r;
     if (rep) rep[(long long)b * hidden + j] = r;
   }
-  __syncthreads();
-  for (int c = 0; c < n_classes; ++c) {
-    float acc = 0.f;
-    for (int j = threadIdx.x; j < hidden; j += blockDim.x) acc += __ldg(w_cls + (long long)c * hidden + j) * srep[j];
-    acc = warp_sum(acc);
-    if (lane_id() == 0) red[warp_id()] = acc;
+  const int warps = (blockDim.x + 31) >> 5;
+  for (int c0 = 0; c0 < n_classes; c0 += 4) {
+    float acc[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      acc[c] = (j < hidden && c0 + c < n_classes) ? __ldg(w_cls + (long long)(c0 + c) * hidden + j) * r : 0.f;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[c] = warp_sum(acc[c]);
+    if (lane_id() == 0)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) red[warp_id()][c] = acc[c];
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (threadIdx.x < 4 && c0 + threadIdx.x < n_classes) {
+      const int c = threadIdx.x;
       float z = 0.f;
-      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) z += red[w];
-      if (add_bias) z += b_cls[c];
-      logits[(long long)b * n_classes + c] = z;
+      for (int w = 0; w < warps; ++w) z += red[w][c];
+      if (add_bias) z += b_cls[c0 + c];
+      logits[(long long)b * n_classes + c0 + c] = z;
     }
     __syncthreads();
   }
@@ -259,12 +286,14 @@ void launch_reduce_ln(const float* part, int splits, long long part_split_stride
 #undef SP_REDUCE
 }
 
-void launch_head(const float* final_rep, long long final_gs, int groups, const float* alpha, const float* w_cls,
-                 const float* b_cls, int n_classes, int hidden, int n_rows, int add_bias, float* rep, float* logits,
+void launch_head(const float* final_rep, long long final_gs, long long split_stride, int splits,
+                 const float* b_pool, int groups, const float* alpha, const float* w_cls, const float* b_cls,
+                 int n_classes, int hidden, int n_rows, int add_bias, float* rep, float* logits,
                  cudaStream_t stream) {
   if (n_rows <= 0) return;
-  launch_pdl(head_kernel, dim3(n_rows), dim3(256), hidden * sizeof(float), stream, final_rep, final_gs, groups,
-             alpha, w_cls, b_cls, n_classes, hidden, add_bias, rep, logits);
+  const int threads = ((hidden + 31) / 32) * 32;
+  launch_pdl(head_kernel, dim3(n_rows), dim3(threads), 0, stream, final_rep, final_gs, split_stride, splits, b_pool,
+             groups, alpha, w_cls, b_cls, n_classes, hidden, add_bias, rep, logits);
 }
 
 }  // namespace sp

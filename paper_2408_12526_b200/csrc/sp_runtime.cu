@@ -171,7 +171,8 @@ void free_all(sp_group* g) {
 int validate_config(const sp_config& c) {
   if (c.kind != SP_KIND_DENSE && c.kind != SP_KIND_BERT) return fail(SP_EINVAL, "unknown student kind %d", c.kind);
   if (c.n_students < 1) return fail(SP_EINVAL, "n_students must be >= 1");
-  if (c.hidden < 128 || c.hidden % 128) return fail(SP_EINVAL, "hidden=%d must be a multiple of 128", c.hidden);
+  if (c.hidden < 128 || c.hidden % 128 || c.hidden > 1024)
+    return fail(SP_EINVAL, "hidden=%d must be a multiple of 128 in [128, 1024]", c.hidden);
   if (c.kind == SP_KIND_BERT && !sp::rowops_supported_hidden(c.hidden))
     return fail(SP_EINVAL, "BERT hidden=%d must be one of 128, 256, 512, 768, 1024", c.hidden);
   if (c.n_classes < 1) return fail(SP_EINVAL, "n_classes must be >= 1");
@@ -219,7 +220,7 @@ int sp_group_create(const sp_config* cfg, const sp_weights* weights, int device,
     delete g;
     return code;
   };
-  if ((rc = dev_alloc(g, &g->final32, S * R * H))) return bail(rc);
+  if ((rc = dev_alloc(g, &g->final32, (size_t)kMaxSplits * S * R * H))) return bail(rc);  // pooler split-K partials
   if ((rc = dev_alloc(g, &g->d_ids, T))) return bail(rc);
   if ((rc = dev_alloc(g, &g->d_cu, B + 1))) return bail(rc);
   if ((rc = dev_alloc(g, &g->d_logits, R * c.n_classes))) return bail(rc);
@@ -321,6 +322,42 @@ namespace {
 int run_gemm(sp_group* grp, int kind, const CUtensorMap& wmap, const XMaps& xm, int groups, int n_out, int k_dim,
              int t_rows, int x_group_rows, const float* bias, int bias_gs, int act, void* out, long long out_gs,
              int out_f32, int splits, long long split_stride, cudaStream_t st) {
+  static const int persist_min_rows = [] {
+    const char* v = getenv("SP_GEMM_PERSIST_MIN_ROWS");  // tuning knob; default: beyond one 128-token tile
+    return v ? atoi(v) : 129;
+  }();
+  if (splits == 1 && t_rows >= persist_min_rows) {
+    sp::GemmParams p{};
+    p.n_out = n_out;
+    p.k_dim = k_dim;
+    p.t_rows = t_rows;
+    p.x_group_rows = x_group_rows;
+    p.m_tiles = n_out / 128;
+    p.splits = 1;
+    p.kb_per_split = k_dim / 64;
+    p.cluster = 1;
+    sp::gemm_configure_persistent(t_rows, out_f32 != 0, &p.bn, &p.n_tiles, &p.stages);
+    p.out = out;
+    p.out_group_stride = out_gs;
+    p.out_ld = n_out;
+    p.bias = bias;
+    p.bias_group_stride = bias_gs;
+    p.act = act;
+    p.out_f32 = out_f32;
+    sp::GemmMaps maps;
+    maps.w = wmap;
+    maps.x64 = xm.x64;
+    maps.x16 = xm.x16;
+    if (grp) {
+      const double G = groups, N = n_out, K = k_dim, T = t_rows;
+      const double xin = (x_group_rows == 0 ? 1.0 : G) * T * K * 2.0;
+      grp->rec_begin(kind, G * N * K * 2.0 + xin + G * T * N * (out_f32 ? 4.0 : 2.0) + (bias ? G * N * 4.0 : 0.0),
+                     2.0 * G * N * K * T);
+    }
+    sp::launch_gemm_persistent(maps, p, groups, st);
+    if (grp) grp->rec_end();
+    return 1;
+  }
   sp::GemmParams p{};
   p.n_out = n_out;
   p.k_dim = k_dim;
@@ -370,6 +407,7 @@ int bert_forward(sp_group* g, const int32_t* ids, const int32_t* cu, int n_seqs,
   const int S = c.n_students, H = c.hidden, F = c.ffn, T = c.max_tokens, B = c.max_seqs;
   const long long xgs = (long long)T * H;
   int launches = 0;
+  int pool_splits = 1;
   g->rec_reset(st);
   const double GTH = (double)k * n_tokens * H;
   if (k > 0) {
@@ -413,12 +451,18 @@ int bert_forward(sp_group* g, const int32_t* ids, const int32_t* cu, int n_seqs,
       g->rec_end();
       ++launches;
     }
-    // pooler on the CLS rows: tanh(W_p h_CLS + b_p), fp32 out
-    launches += run_gemm(g, SP_LAUNCH_GEMM_POOL, g->m_pool, g->xm_cls, k, H, H, n_seqs, B, w.b_pool, H, sp::ACT_TANH, g->final32,
-                         (long long)g->rows_cap * H, 1, 1, 0, st);
+    // pooler on the CLS rows: tanh(W_p h_CLS + b_p). Few rows: split-K partials (more CTAs stream the
+    // pooler weights), finished by the head kernel; many rows: one pass with the tanh epilogue.
+    const int s_p = n_seqs <= 128 ? choose_splits(k * (H / 128), H / 64, kMaxSplits) : 1;
+    pool_splits = s_p;
+    launches += run_gemm(g, SP_LAUNCH_GEMM_POOL, g->m_pool, g->xm_cls, k, H, H, n_seqs, B, s_p > 1 ? nullptr : w.b_pool,
+                         H, sp::ACT_TANH, g->final32, (long long)g->rows_cap * H, 1, s_p,
+                         (long long)S * g->rows_cap * H, st);
   }
-  g->rec_begin(SP_LAUNCH_HEAD, (double)k * n_seqs * H * 4.0 + (double)c.n_classes * H * 4.0 + n_seqs * H * 4.0, 0.0);
-  sp::launch_head(g->final32, (long long)g->rows_cap * H, k, w.alpha, w.w_cls, w.b_cls, c.n_classes, H, n_seqs,
+  g->rec_begin(SP_LAUNCH_HEAD, (double)k * n_seqs * H * 4.0 * (pool_splits > 1 ? pool_splits : 1) +
+                                   (double)c.n_classes * H * 4.0 + n_seqs * H * 4.0, 0.0);
+  sp::launch_head(g->final32, (long long)g->rows_cap * H, (long long)S * g->rows_cap * H,
+                  pool_splits > 1 ? pool_splits : 0, w.b_pool, k, w.alpha, w.w_cls, w.b_cls, c.n_classes, H, n_seqs,
                   add_bias, rep, logits, st);
   g->rec_end();
   ++launches;
@@ -451,7 +495,8 @@ int dense_forward(sp_group* g, const half* x, int n_rows, int k, float* rep, flo
     }
   }
   g->rec_begin(SP_LAUNCH_HEAD, (double)k * n_rows * H * 4.0 + (double)c.n_classes * H * 4.0, 0.0);
-  sp::launch_head(g->final32, fgs, k, w.alpha, w.w_cls, w.b_cls, c.n_classes, H, n_rows, add_bias, rep, logits, st);
+  sp::launch_head(g->final32, fgs, 0, 0, nullptr, k, w.alpha, w.w_cls, w.b_cls, c.n_classes, H, n_rows, add_bias, rep,
+                  logits, st);
   g->rec_end();
   ++launches;
   g->last_launches = launches;
