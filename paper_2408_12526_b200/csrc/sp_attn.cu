@@ -54,7 +54,7 @@ __device__ __forceinline__ void cp_async_wait() {
 template <int D, int NW>
 __global__ void __launch_bounds__(32 * NW, NW == 8 ? 2 : 4)
     attn_kernel(const half* __restrict__ qkv, half* __restrict__ ctx, const int* __restrict__ cu, int n_heads,
-                int hidden, long long group_rows, float scale_log2) {
+                int hidden, long long group_rows, float scale_log2, const void* pf_ptr, unsigned long long pf_bytes) {
   constexpr int BQ = 16 * NW, BK = 64, LD = D + 8;  // +8 halfs: conflict-free ldmatrix rows
   constexpr int NT = 32 * NW;
   constexpr int VPR = D / 8;  // 16-byte vectors per row
@@ -63,6 +63,7 @@ __global__ void __launch_bounds__(32 * NW, NW == 8 ? 2 : 4)
   half* sK = sQ + BQ * LD;        // [2][BK][LD]
   half* sV = sK + 2 * BK * LD;    // [2][BK][LD]
 
+  prefetch_share_l2(pf_ptr, pf_bytes);  // next projection's weights, while attention runs
   pdl_wait();
   pdl_launch_dependents();
   const int b = blockIdx.y;
@@ -224,7 +225,8 @@ __global__ void __launch_bounds__(32 * NW, NW == 8 ? 2 : 4)
 
 template <int D, int NW>
 static void launch_attn_t(const half* qkv, half* ctx, const int* cu, int n_seqs, int max_len, int groups,
-                          int n_heads, int hidden, long long group_rows, float scale_log2, cudaStream_t stream) {
+                          int n_heads, int hidden, long long group_rows, float scale_log2, const void* pf_ptr,
+                          unsigned long long pf_bytes, cudaStream_t stream) {
   constexpr int BQ = 16 * NW, LD = D + 8;
   const size_t smem = (size_t)(BQ + 4 * 64) * LD * sizeof(half);
   static bool attr_set = false;
@@ -234,20 +236,21 @@ static void launch_attn_t(const half* qkv, half* ctx, const int* cu, int n_seqs,
   }
   dim3 grid((max_len + BQ - 1) / BQ, n_seqs, groups * n_heads);
   launch_pdl(attn_kernel<D, NW>, grid, dim3(32 * NW), smem, stream, qkv, ctx, cu, n_heads, hidden, group_rows,
-             scale_log2);
+             scale_log2, pf_ptr, pf_bytes);
 }
 
 void launch_attention(const half* qkv, half* ctx, const int* cu_seqlens, int n_seqs, int max_len, int groups,
-                      int n_heads, int head_dim, int hidden, long long group_rows, cudaStream_t stream) {
+                      int n_heads, int head_dim, int hidden, long long group_rows, cudaStream_t stream,
+                      const void* pf_ptr, unsigned long long pf_bytes) {
   if (n_seqs <= 0 || max_len <= 0 || groups <= 0) return;
   const float scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(head_dim));
   const bool big = max_len > 128;  // 128-query CTAs halve K/V re-reads on long sequences
   if (head_dim == 64) {
-    if (big) launch_attn_t<64, 8>(qkv, ctx, cu_seqlens, n_seqs, max_len, groups, n_heads, hidden, group_rows, scale_log2, stream);
-    else launch_attn_t<64, 4>(qkv, ctx, cu_seqlens, n_seqs, max_len, groups, n_heads, hidden, group_rows, scale_log2, stream);
+    if (big) launch_attn_t<64, 8>(qkv, ctx, cu_seqlens, n_seqs, max_len, groups, n_heads, hidden, group_rows, scale_log2, pf_ptr, pf_bytes, stream);
+    else launch_attn_t<64, 4>(qkv, ctx, cu_seqlens, n_seqs, max_len, groups, n_heads, hidden, group_rows, scale_log2, pf_ptr, pf_bytes, stream);
   } else {
-    if (big) launch_attn_t<32, 8>(qkv, ctx, cu_seqlens, n_seqs, max_len, groups, n_heads, hidden, group_rows, scale_log2, stream);
-    else launch_attn_t<32, 4>(qkv, ctx, cu_seqlens, n_seqs, max_len, groups, n_heads, hidden, group_rows, scale_log2, stream);
+    if (big) launch_attn_t<32, 8>(qkv, ctx, cu_seqlens, n_seqs, max_len, groups, n_heads, hidden, group_rows, scale_log2, pf_ptr, pf_bytes, stream);
+    else launch_attn_t<32, 4>(qkv, ctx, cu_seqlens, n_seqs, max_len, groups, n_heads, hidden, group_rows, scale_log2, pf_ptr, pf_bytes, stream);
   }
 }
 

@@ -120,12 +120,16 @@ __global__ void __launch_bounds__(kThreads, 2)
           for (; r < r_end; r += 16) tma_load_2d(&map_x16, &full[s], sb + r * 128, kc, xrow + r, pol_x);
         }
       };
-      // 1) weight prefetch of the first stages: independent of the previous kernel
+      // 1) weight prefetch: independent of the previous kernel. The first stages go straight to
+      //    smem; the rest of this CTA's weight slab is pulled into L2 so the HBM stream continues
+      //    across the kernel boundary while the previous kernel finishes.
       const int n_pre = min(p.stages, kb1 - kb0);
       for (int i = 0; i < n_pre; ++i) {
         mbar_arrive_expect_tx(&full[i], stage_bytes);
         tma_load_2d(&map_w, &full[i], smem + i * stage_bytes, (kb0 + i) * kBlockK, wrow, pol_w);
       }
+      if (p.l2_prefetch)
+        for (int kb = kb0 + n_pre; kb < kb1; ++kb) tma_prefetch_l2_2d(&map_w, kb * kBlockK, wrow);
       if (tr) tr[2] = globaltimer();
       // 2) activations are produced by the previous kernel
       pdl_wait();
@@ -328,6 +332,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_arrive_expect_tx(&full[i], stage_bytes);
             tma_load_2d(&map_w, &full[i], smem + i * stage_bytes, i * kBlockK, wrow, pol_w);
           }
+          if (p.l2_prefetch)
+            for (int i = n_pre; i < nkb; ++i) tma_prefetch_l2_2d(&map_w, i * kBlockK, wrow);
           pdl_wait();
           for (int i = 0; i < n_pre; ++i) {
             uint8_t* sb = smem + i * stage_bytes + kATileBytes;

@@ -59,6 +59,7 @@ struct GemmParams {
   int cluster;                // 1, or 2: CTA pairs along M share the token tile via TMA multicast
   int w_keep;                 // keep weight tiles in L2 (evict_last) when n_tiles > 1
   int groups;                 // students in the launch (persistent path)
+  int l2_prefetch;            // pull the rest of the weight slab into L2 before griddepcontrol.wait
 };
 
 // Debug hook: when set, every GEMM launch records a per-CTA timeline into this device buffer.
@@ -81,21 +82,30 @@ void gemm_configure_tiles(int t_rows, bool cluster2, int* bn, int* n_tiles, int*
 // Unpadded multi-head attention over cu_seqlens-packed sequences.
 //   qkv: fp16 [groups][x_group_rows][3H] (Q | K | V, head h at columns h*D within each third)
 //   ctx: fp16 [groups][x_group_rows][H]
+// (pf_ptr, pf_bytes): weights of the NEXT projection, pulled into L2 while this kernel runs.
 void launch_attention(const half* qkv, half* ctx, const int* cu_seqlens, int n_seqs, int max_len, int groups,
-                      int n_heads, int head_dim, int hidden, long long group_rows, cudaStream_t stream);
+                      int n_heads, int head_dim, int hidden, long long group_rows, cudaStream_t stream,
+                      const void* pf_ptr = nullptr, unsigned long long pf_bytes = 0);
+
+// Tensor-core attention (head_dim 64, L <= 512). map_qkv: 2-D map over the qkv buffer
+// [groups * group_rows, 3H] fp16 with a {64, 128} box and 128-byte swizzle.
+void launch_attention_tc(const CUtensorMap& map_qkv, half* ctx, const int* cu_seqlens, int n_seqs, int max_len,
+                         int groups, int n_heads, int hidden, long long group_rows, cudaStream_t stream);
 
 // Embedding gather + LayerNorm: x = LN(E_word[g][id_t] + E_pos[g][pos_t] + E_type[g][0]).
 void launch_embed_ln(const int* ids, const int* cu_seqlens, int n_seqs, int n_tokens, int groups,
                      const half* word, const half* pos, const half* type, long long word_gs, long long pos_gs,
                      const float* gamma, const float* beta, int hidden, float eps, float* x32, half* x16,
-                     long long x_gs, cudaStream_t stream);
+                     long long x_gs, cudaStream_t stream, const void* pf_ptr = nullptr,
+                     unsigned long long pf_bytes = 0);
 
 // Split-K reduce + bias + residual + LayerNorm:
 //   x = LN(x + b + sum_s part[s]); optional CLS rows copied to cls16[g][seq].
 void launch_reduce_ln(const float* part, int splits, long long part_split_stride, const float* bias,
                       const float* gamma, const float* beta, int hidden, float eps, float* x32, half* x16,
                       long long x_gs, int n_tokens, int groups, const int* cu_seqlens, int n_seqs, half* cls16,
-                      long long cls_gs, cudaStream_t stream);
+                      long long cls_gs, cudaStream_t stream, const void* pf_ptr = nullptr,
+                      unsigned long long pf_bytes = 0);
 
 // Boosting sum + shared classifier (distill.py:169-178, :512):
 //   final[m][b] = splits ? tanh(sum_s part[s][m][b] + b_pool[m]) : final_rep[m][b]

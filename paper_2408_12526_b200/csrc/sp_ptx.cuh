@@ -80,6 +80,35 @@ __device__ __forceinline__ void tma_load_2d_mc(const CUtensorMap* map, uint64_t*
       : "memory");
 }
 
+// Bring a tensor box into L2 only (no smem destination, no completion tracking).
+__device__ __forceinline__ void tma_prefetch_l2_2d(const CUtensorMap* map, int c0, int c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1)
+               : "memory");
+}
+
+// Bring a contiguous byte range into L2 (bulk, fire-and-forget). size: multiple of 16.
+__device__ __forceinline__ void bulk_prefetch_l2(const void* ptr, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<uint64_t>(ptr)), "r"(bytes)
+               : "memory");
+}
+
+// Each CTA of a grid pulls its share of [ptr, ptr + bytes) into L2 (the next projection's weights
+// while a latency-bound kernel runs). One thread per CTA issues 64 KiB bulk prefetches.
+__device__ __forceinline__ void prefetch_share_l2(const void* ptr, unsigned long long bytes) {
+  if (ptr == nullptr || bytes == 0 || threadIdx.x != 0) return;
+  const unsigned long long n_cta = (unsigned long long)gridDim.x * gridDim.y * gridDim.z;
+  const unsigned long long cta = blockIdx.x + (unsigned long long)gridDim.x * (blockIdx.y + (unsigned long long)gridDim.y * blockIdx.z);
+  const unsigned long long chunk = 65536ull;
+  const unsigned long long n_chunks = (bytes + chunk - 1) / chunk;
+  for (unsigned long long c = cta; c < n_chunks; c += n_cta) {
+    const unsigned long long off = c * chunk;
+    const unsigned long long len = (bytes - off < chunk) ? (bytes - off) : chunk;
+    bulk_prefetch_l2(static_cast<const uint8_t*>(ptr) + off, static_cast<uint32_t>(len & ~15ull));
+  }
+}
+
 __device__ __forceinline__ uint32_t cluster_ctarank() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));

@@ -74,7 +74,9 @@ __global__ void __launch_bounds__(128)
     embed_ln_kernel(const int* __restrict__ ids, const int* __restrict__ cu, int n_seqs, int n_tokens,
                     const half* __restrict__ word, const half* __restrict__ pos, const half* __restrict__ type,
                     long long word_gs, long long pos_gs, const float* __restrict__ gamma,
-                    const float* __restrict__ beta, int hidden, float eps, float* x32, half* x16, long long x_gs) {
+                    const float* __restrict__ beta, int hidden, float eps, float* x32, half* x16, long long x_gs,
+                    const void* pf_ptr, unsigned long long pf_bytes) {
+  prefetch_share_l2(pf_ptr, pf_bytes);
   pdl_wait();
   pdl_launch_dependents();
   const int t = blockIdx.x * 4 + warp_id();
@@ -115,7 +117,9 @@ __global__ void __launch_bounds__(128)
     reduce_ln_kernel(const float* __restrict__ part, int splits, long long part_split_stride,
                      const float* __restrict__ bias, const float* __restrict__ gamma, const float* __restrict__ beta,
                      int hidden, float eps, float* x32, half* x16, long long x_gs, int n_tokens,
-                     const int* __restrict__ cu, int n_seqs, half* cls16, long long cls_gs) {
+                     const int* __restrict__ cu, int n_seqs, half* cls16, long long cls_gs, const void* pf_ptr,
+                     unsigned long long pf_bytes) {
+  prefetch_share_l2(pf_ptr, pf_bytes);
   pdl_wait();
   pdl_launch_dependents();
   const int t = blockIdx.x * 4 + warp_id();
@@ -241,20 +245,20 @@ template <int NC>
 static void embed_ln_t(dim3 grid, cudaStream_t st, const int* ids, const int* cu, int n_seqs, int n_tokens,
                        const half* word, const half* pos, const half* type, long long word_gs, long long pos_gs,
                        const float* gamma, const float* beta, int hidden, float eps, float* x32, half* x16,
-                       long long x_gs) {
+                       long long x_gs, const void* pf_ptr, unsigned long long pf_bytes) {
   launch_pdl(embed_ln_kernel<NC>, grid, dim3(128), 0, st, ids, cu, n_seqs, n_tokens, word, pos, type, word_gs,
-             pos_gs, gamma, beta, hidden, eps, x32, x16, x_gs);
+             pos_gs, gamma, beta, hidden, eps, x32, x16, x_gs, pf_ptr, pf_bytes);
 }
 
 void launch_embed_ln(const int* ids, const int* cu_seqlens, int n_seqs, int n_tokens, int groups, const half* word,
                      const half* pos, const half* type, long long word_gs, long long pos_gs, const float* gamma,
                      const float* beta, int hidden, float eps, float* x32, half* x16, long long x_gs,
-                     cudaStream_t stream) {
+                     cudaStream_t stream, const void* pf_ptr, unsigned long long pf_bytes) {
   if (n_tokens <= 0 || groups <= 0) return;
   dim3 grid((n_tokens + 3) / 4, groups);
 #define SP_EMBED(NC_)                                                                                      \
   embed_ln_t<NC_>(grid, stream, ids, cu_seqlens, n_seqs, n_tokens, word, pos, type, word_gs, pos_gs, gamma, \
-                  beta, hidden, eps, x32, x16, x_gs)
+                  beta, hidden, eps, x32, x16, x_gs, pf_ptr, pf_bytes)
   switch (hidden / 128) {
     case 1: SP_EMBED(1); break;
     case 2: SP_EMBED(2); break;
@@ -269,12 +273,12 @@ void launch_embed_ln(const int* ids, const int* cu_seqlens, int n_seqs, int n_to
 void launch_reduce_ln(const float* part, int splits, long long part_split_stride, const float* bias,
                       const float* gamma, const float* beta, int hidden, float eps, float* x32, half* x16,
                       long long x_gs, int n_tokens, int groups, const int* cu_seqlens, int n_seqs, half* cls16,
-                      long long cls_gs, cudaStream_t stream) {
+                      long long cls_gs, cudaStream_t stream, const void* pf_ptr, unsigned long long pf_bytes) {
   if (n_tokens <= 0 || groups <= 0) return;
   dim3 grid((n_tokens + 3) / 4, groups);
 #define SP_REDUCE(NC_)                                                                                          \
   launch_pdl(reduce_ln_kernel<NC_>, grid, dim3(128), 0, stream, part, splits, part_split_stride, bias, gamma, \
-             beta, hidden, eps, x32, x16, x_gs, n_tokens, cu_seqlens, n_seqs, cls16, cls_gs)
+             beta, hidden, eps, x32, x16, x_gs, n_tokens, cu_seqlens, n_seqs, cls16, cls_gs, pf_ptr, pf_bytes)
   switch (hidden / 128) {
     case 1: SP_REDUCE(1); break;
     case 2: SP_REDUCE(2); break;

@@ -107,6 +107,7 @@ struct sp_group {
   // tensor maps
   std::vector<CUtensorMap> m_qkv, m_o, m_f1, m_f2, m_layers;
   CUtensorMap m_pool, m_in;
+  CUtensorMap m_qkv_attn;  // qkv buffer viewed with a {64, 128} box (tensor-core attention)
   XMaps xm_x16, xm_ctx, xm_ffn, xm_cls, xm_ha, xm_hb;
   int last_launches = 0;
   double sum_len_sq = 0.0;  // sum_b L_b^2 of the current request (attention flops)
@@ -257,6 +258,9 @@ int sp_group_create(const sp_config* cfg, const sp_weights* weights, int device,
     ok &= make_xmaps(&g->xm_ctx, g->ctx, S * T, H);
     ok &= make_xmaps(&g->xm_ffn, g->ffn, S * T, F);
     ok &= make_xmaps(&g->xm_cls, g->cls16, S * B, H);
+    ok &= make_map(&g->m_qkv_attn, g->qkv, S * T, 3 * H, 128);
+    // rows past a request's tokens are read (masked) by the attention tiles: keep them finite
+    if (cudaMemset(g->qkv, 0, S * T * 3 * H * sizeof(half)) != cudaSuccess) ok = false;
     if (!ok) return bail(fail(SP_EINVAL, "tensor-map creation failed (pointer alignment / shape)"));
   } else {
     if (!w.w_in || !w.b_in || !w.w_layers || !w.b_layers || !w.alpha || !w.w_cls || !w.b_cls)
@@ -318,6 +322,17 @@ int sp_group_profile_read(sp_group* g, sp_launch_record* out, int max_records) {
 
 namespace {
 
+#define PF(x) (x).p, (x).n
+
+// Tensor-core attention for head_dim 64 and L <= 512 (SP_ATTN_TC=0 forces the mma.sync kernel).
+bool use_attn_tc(int head_dim, int max_len) {
+  static const bool on = [] {
+    const char* v = getenv("SP_ATTN_TC");
+    return v == nullptr || atoi(v) != 0;
+  }();
+  return on && head_dim == 64 && max_len <= 512;
+}
+
 // Launch one grouped projection. Returns the number of kernels launched (1).
 int run_gemm(sp_group* grp, int kind, const CUtensorMap& wmap, const XMaps& xm, int groups, int n_out, int k_dim,
              int t_rows, int x_group_rows, const float* bias, int bias_gs, int act, void* out, long long out_gs,
@@ -326,8 +341,13 @@ int run_gemm(sp_group* grp, int kind, const CUtensorMap& wmap, const XMaps& xm, 
     const char* v = getenv("SP_GEMM_PERSIST_MIN_ROWS");  // tuning knob; default: beyond one 128-token tile
     return v ? atoi(v) : 129;
   }();
+  static const int l2_prefetch = [] {
+    const char* v = getenv("SP_GEMM_L2PREFETCH");  // measured neutral-to-slower: opt-in
+    return v ? atoi(v) : 0;
+  }();
   if (splits == 1 && t_rows >= persist_min_rows) {
     sp::GemmParams p{};
+    p.l2_prefetch = l2_prefetch;
     p.n_out = n_out;
     p.k_dim = k_dim;
     p.t_rows = t_rows;
@@ -359,6 +379,7 @@ int run_gemm(sp_group* grp, int kind, const CUtensorMap& wmap, const XMaps& xm, 
     return 1;
   }
   sp::GemmParams p{};
+  p.l2_prefetch = l2_prefetch;
   p.n_out = n_out;
   p.k_dim = k_dim;
   p.t_rows = t_rows;
@@ -408,6 +429,19 @@ int bert_forward(sp_group* g, const int32_t* ids, const int32_t* cu, int n_seqs,
   const long long xgs = (long long)T * H;
   int launches = 0;
   int pool_splits = 1;
+  const half* wq = static_cast<const half*>(w.w_qkv);
+  const half* wo = static_cast<const half*>(w.w_o);
+  const half* w1 = static_cast<const half*>(w.w_ffn1);
+  static const bool pf_on = [] {
+    const char* v = getenv("SP_L2_PREFETCH_NEXT");  // measured slower (latency-bound chain): opt-in
+    return v != nullptr && atoi(v) != 0;
+  }();
+  // (ptr, bytes) of fp16 weights the next projection will stream: pulled into L2 by the kernel in between
+  struct Pf {
+    const void* p;
+    unsigned long long n;
+  };
+  auto pf = [&](const void* p, size_t elems) { return pf_on ? Pf{p, (unsigned long long)elems * 2} : Pf{nullptr, 0}; };
   g->rec_reset(st);
   const double GTH = (double)k * n_tokens * H;
   if (k > 0) {
@@ -415,7 +449,7 @@ int bert_forward(sp_group* g, const int32_t* ids, const int32_t* cu, int n_seqs,
     sp::launch_embed_ln(ids, cu, n_seqs, n_tokens, k, static_cast<const half*>(w.word_emb),
                         static_cast<const half*>(w.pos_emb), static_cast<const half*>(w.type_emb),
                         (long long)c.vocab * H, (long long)c.max_pos * H, w.emb_ln_gamma, w.emb_ln_beta, H, c.ln_eps,
-                        g->x32, g->x16, xgs, st);
+                        g->x32, g->x16, xgs, st, PF(pf(w.w_qkv, (size_t)k * 3 * H * H)));
     g->rec_end();
     ++launches;
     int bn, n_tiles, stages;
@@ -428,7 +462,11 @@ int bert_forward(sp_group* g, const int32_t* ids, const int32_t* cu, int n_seqs,
       launches += run_gemm(g, SP_LAUNCH_GEMM_QKV, g->m_qkv[l], g->xm_x16, k, 3 * H, H, n_tokens, T, w.b_qkv + lS * 3 * H, 3 * H,
                            sp::ACT_NONE, g->qkv, (long long)T * 3 * H, 0, 1, 0, st);
       g->rec_begin(SP_LAUNCH_ATTENTION, GTH * 8.0, 4.0 * k * H * g->sum_len_sq);
-      sp::launch_attention(g->qkv, g->ctx, cu, n_seqs, max_len, k, c.n_heads, H / c.n_heads, H, T, st);
+      if (use_attn_tc(H / c.n_heads, max_len))
+        sp::launch_attention_tc(g->m_qkv_attn, g->ctx, cu, n_seqs, max_len, k, c.n_heads, H, T, st);
+      else
+        sp::launch_attention(g->qkv, g->ctx, cu, n_seqs, max_len, k, c.n_heads, H / c.n_heads, H, T, st,
+                             PF(pf(wo + lS * H * H, (size_t)k * H * H)));
       g->rec_end();
       ++launches;
       // O and FFN2 write raw partial sums; the reduce+LN kernel owns bias, residual and LayerNorm
@@ -436,7 +474,8 @@ int bert_forward(sp_group* g, const int32_t* ids, const int32_t* cu, int n_seqs,
                            s_o, part_ss, st);
       g->rec_begin(SP_LAUNCH_REDUCE_LN, GTH * (4.0 * s_o + 10.0), 0.0);
       sp::launch_reduce_ln(g->part, s_o, part_ss, w.b_o + lS * H, w.ln1_gamma + lS * H, w.ln1_beta + lS * H, H,
-                           c.ln_eps, g->x32, g->x16, xgs, n_tokens, k, cu, n_seqs, nullptr, 0, st);
+                           c.ln_eps, g->x32, g->x16, xgs, n_tokens, k, cu, n_seqs, nullptr, 0, st,
+                           PF(pf(w1 + lS * F * H, (size_t)k * F * H)));
       g->rec_end();
       ++launches;
       launches += run_gemm(g, SP_LAUNCH_GEMM_FFN1, g->m_f1[l], g->xm_x16, k, F, H, n_tokens, T, w.b_ffn1 + lS * F, F, sp::ACT_GELU, g->ffn,
@@ -447,7 +486,8 @@ int bert_forward(sp_group* g, const int32_t* ids, const int32_t* cu, int n_seqs,
       g->rec_begin(SP_LAUNCH_REDUCE_LN, GTH * (4.0 * s_f + 10.0), 0.0);
       sp::launch_reduce_ln(g->part, s_f, part_ss, w.b_ffn2 + lS * H, w.ln2_gamma + lS * H, w.ln2_beta + lS * H, H,
                            c.ln_eps, g->x32, g->x16, xgs, n_tokens, k, cu, n_seqs, last ? g->cls16 : nullptr,
-                           (long long)B * H, st);
+                           (long long)B * H, st,
+                           PF(last ? pf(w.w_pool, (size_t)k * H * H) : pf(wq + (lS + S) * 3 * H * H, (size_t)k * 3 * H * H)));
       g->rec_end();
       ++launches;
     }
@@ -623,8 +663,17 @@ int sp_op_attention(const void* qkv, void* ctx, const int32_t* cu_seqlens, int32
   if (!qkv || !ctx || !cu_seqlens) return fail(SP_EINVAL, "null buffer");
   if (head_dim != 32 && head_dim != 64) return fail(SP_EINVAL, "head_dim must be 32 or 64");
   if (n_seqs < 1 || groups < 1 || n_heads < 1 || max_seq_len < 1) return fail(SP_EINVAL, "bad attention shape");
-  sp::launch_attention(static_cast<const half*>(qkv), static_cast<half*>(ctx), cu_seqlens, n_seqs, max_seq_len,
-                       groups, n_heads, head_dim, n_heads * head_dim, group_rows, static_cast<cudaStream_t>(stream));
+  const int hidden = n_heads * head_dim;
+  if (use_attn_tc(head_dim, max_seq_len)) {
+    CUtensorMap m;
+    if (!make_map(&m, qkv, (uint64_t)groups * group_rows, 3 * hidden, 128))
+      return fail(SP_EINVAL, "attention tensor map failed");
+    sp::launch_attention_tc(m, static_cast<half*>(ctx), cu_seqlens, n_seqs, max_seq_len, groups, n_heads, hidden,
+                            group_rows, static_cast<cudaStream_t>(stream));
+  } else {
+    sp::launch_attention(static_cast<const half*>(qkv), static_cast<half*>(ctx), cu_seqlens, n_seqs, max_seq_len,
+                         groups, n_heads, head_dim, hidden, group_rows, static_cast<cudaStream_t>(stream));
+  }
   SP_CUDA(cudaGetLastError());
   return SP_OK;
 }
