@@ -125,6 +125,11 @@ int sp_group_forward_dense(sp_group* group, const void* x, int32_t n_rows, int32
 int sp_group_forward_host(sp_group* group, const int32_t* ids, const int32_t* cu_seqlens, int32_t n_seqs,
                           int32_t n_tokens, int32_t k_active, float* logits_out, int32_t add_bias, void* stream);
 
+/* Capture (ahead of serving) the CUDA graphs that sp_group_forward_host replays for
+ * single-sequence requests: one per 16-token bucket up to max_tokens, for this k_active/add_bias.
+ * Optional — buckets are otherwise captured on first use. SP_GRAPHS=0 disables graphs. */
+int sp_group_prepare_graphs(sp_group* group, int32_t max_tokens, int32_t k_active, int32_t add_bias);
+
 /* Number of kernels the last forward call on this group launched. */
 int sp_group_last_launches(const sp_group* group);
 

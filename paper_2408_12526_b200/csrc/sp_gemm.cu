@@ -195,6 +195,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     OutT* out = reinterpret_cast<OutT*>(p.out) + (long long)g * p.out_group_stride +
                 (long long)split * p.out_split_stride + m0 + q * 32;
 
+    const int t_rows = p.t_dev ? __ldg(p.t_dev) : p.t_rows;  // graph replay: live count from cu_seqlens
     mbar_wait(tmem_full, 0);
     tc_fence_after();
     if (tr && warp == 2 && lane == 0) tr[6] = globaltimer();
@@ -225,7 +226,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       for (int j0 = 0; j0 < n; j0 += kRowsPerPass) {
         const int j = j0 + lane / kLanesPerRow;
         const int t = n0 + c + j;
-        if (j < n && t < p.t_rows) {
+        if (j < n && t < t_rows) {
           const uint4 v = *reinterpret_cast<const uint4*>(reinterpret_cast<const uint8_t*>(stage) + j * kRowBytes +
                                                           sub * 16);
           *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(out + (long long)t * p.out_ld) + sub * 16) = v;
@@ -399,6 +400,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int half_cols = p.bn >> 1;
     const int c_begin = (e >> 2) * half_cols;
     OutT* stage = reinterpret_cast<OutT*>(staging + e * 32 * kRowBytes);
+    const int t_rows = p.t_dev ? __ldg(p.t_dev) : p.t_rows;
     int j = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
       int g, mt, nt;
@@ -438,7 +440,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int j0 = 0; j0 < n; j0 += kRowsPerPass) {
           const int jr = j0 + lane / kLanesPerRow;
           const int t = n0 + c + jr;
-          if (jr < n && t < p.t_rows) {
+          if (jr < n && t < t_rows) {
             const uint4 v = *reinterpret_cast<const uint4*>(reinterpret_cast<const uint8_t*>(stage) + jr * kRowBytes +
                                                             sub * 16);
             *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(out + (long long)t * p.out_ld) + sub * 16) = v;

@@ -60,6 +60,7 @@ struct GemmParams {
   int w_keep;                 // keep weight tiles in L2 (evict_last) when n_tiles > 1
   int groups;                 // students in the launch (persistent path)
   int l2_prefetch;            // pull the rest of the weight slab into L2 before griddepcontrol.wait
+  const int* t_dev;           // if set: live token count (device), t_rows is only the tile bound
 };
 
 // Debug hook: when set, every GEMM launch records a per-CTA timeline into this device buffer.

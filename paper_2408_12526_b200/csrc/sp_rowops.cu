@@ -80,6 +80,7 @@ __global__ void __launch_bounds__(128)
   pdl_wait();
   pdl_launch_dependents();
   const int t = blockIdx.x * 4 + warp_id();
+  if (n_tokens < 0) n_tokens = __ldg(cu + n_seqs);  // graph replay: live count = cu_seqlens[n_seqs]
   if (t >= n_tokens) return;
   const int g = blockIdx.y;
   const int lane = lane_id();
@@ -123,6 +124,7 @@ __global__ void __launch_bounds__(128)
   pdl_wait();
   pdl_launch_dependents();
   const int t = blockIdx.x * 4 + warp_id();
+  if (n_tokens < 0) n_tokens = __ldg(cu + n_seqs);
   if (t >= n_tokens) return;
   const int g = blockIdx.y;
   const int lane = lane_id();
@@ -254,8 +256,10 @@ void launch_embed_ln(const int* ids, const int* cu_seqlens, int n_seqs, int n_to
                      const half* pos, const half* type, long long word_gs, long long pos_gs, const float* gamma,
                      const float* beta, int hidden, float eps, float* x32, half* x16, long long x_gs,
                      cudaStream_t stream, const void* pf_ptr, unsigned long long pf_bytes) {
-  if (n_tokens <= 0 || groups <= 0) return;
-  dim3 grid((n_tokens + 3) / 4, groups);
+  if (n_tokens == 0 || groups <= 0) return;
+  // n_tokens < 0: grid sized for -n_tokens rows, live count read from cu_seqlens (graph replay)
+  dim3 grid(((n_tokens < 0 ? -n_tokens : n_tokens) + 3) / 4, groups);
+  if (n_tokens < 0) n_tokens = -1;
 #define SP_EMBED(NC_)                                                                                      \
   embed_ln_t<NC_>(grid, stream, ids, cu_seqlens, n_seqs, n_tokens, word, pos, type, word_gs, pos_gs, gamma, \
                   beta, hidden, eps, x32, x16, x_gs, pf_ptr, pf_bytes)
@@ -274,8 +278,9 @@ void launch_reduce_ln(const float* part, int splits, long long part_split_stride
                       const float* gamma, const float* beta, int hidden, float eps, float* x32, half* x16,
                       long long x_gs, int n_tokens, int groups, const int* cu_seqlens, int n_seqs, half* cls16,
                       long long cls_gs, cudaStream_t stream, const void* pf_ptr, unsigned long long pf_bytes) {
-  if (n_tokens <= 0 || groups <= 0) return;
-  dim3 grid((n_tokens + 3) / 4, groups);
+  if (n_tokens == 0 || groups <= 0) return;
+  dim3 grid(((n_tokens < 0 ? -n_tokens : n_tokens) + 3) / 4, groups);
+  if (n_tokens < 0) n_tokens = -1;
 #define SP_REDUCE(NC_)                                                                                          \
   launch_pdl(reduce_ln_kernel<NC_>, grid, dim3(128), 0, stream, part, splits, part_split_stride, bias, gamma, \
              beta, hidden, eps, x32, x16, x_gs, n_tokens, cu_seqlens, n_seqs, cls16, cls_gs, pf_ptr, pf_bytes)

@@ -3,6 +3,8 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <map>
+#include <tuple>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -110,6 +112,10 @@ struct sp_group {
   CUtensorMap m_qkv_attn;  // qkv buffer viewed with a {64, 128} box (tensor-core attention)
   XMaps xm_x16, xm_ctx, xm_ffn, xm_cls, xm_ha, xm_hb;
   int last_launches = 0;
+  // CUDA graphs of the batch-1 host path, keyed by (16-token bucket, k_active, add_bias)
+  std::map<std::tuple<int, int, int>, cudaGraphExec_t> graphs;
+  cudaStream_t cap_stream = nullptr;
+  int graph_launches = 0;  // kernels per graph replay
   double sum_len_sq = 0.0;  // sum_b L_b^2 of the current request (attention flops)
   // per-launch profiling (CUDA events around every kernel of the last forward)
   bool profiling = false;
@@ -160,6 +166,10 @@ int dev_alloc(sp_group* g, T** p, size_t count) {
 }
 
 void free_all(sp_group* g) {
+  for (auto& kv : g->graphs) cudaGraphExecDestroy(kv.second);
+  g->graphs.clear();
+  if (g->cap_stream) cudaStreamDestroy(g->cap_stream);
+  g->cap_stream = nullptr;
   for (void* p : g->allocs) cudaFree(p);
   g->allocs.clear();
   for (auto& r : g->recs) {
@@ -293,6 +303,7 @@ int sp_group_destroy(sp_group* g) {
 
 int sp_group_last_launches(const sp_group* g) { return g ? g->last_launches : 0; }
 
+
 int sp_group_set_profiling(sp_group* g, int enable) {
   if (g == nullptr) return fail(SP_EINVAL, "null group");
   cudaSetDevice(g->device);
@@ -336,7 +347,7 @@ bool use_attn_tc(int head_dim, int max_len) {
 // Launch one grouped projection. Returns the number of kernels launched (1).
 int run_gemm(sp_group* grp, int kind, const CUtensorMap& wmap, const XMaps& xm, int groups, int n_out, int k_dim,
              int t_rows, int x_group_rows, const float* bias, int bias_gs, int act, void* out, long long out_gs,
-             int out_f32, int splits, long long split_stride, cudaStream_t st) {
+             int out_f32, int splits, long long split_stride, cudaStream_t st, const int* t_dev = nullptr) {
   static const int persist_min_rows = [] {
     const char* v = getenv("SP_GEMM_PERSIST_MIN_ROWS");  // tuning knob; default: beyond one 128-token tile
     return v ? atoi(v) : 129;
@@ -348,6 +359,7 @@ int run_gemm(sp_group* grp, int kind, const CUtensorMap& wmap, const XMaps& xm, 
   if (splits == 1 && t_rows >= persist_min_rows) {
     sp::GemmParams p{};
     p.l2_prefetch = l2_prefetch;
+    p.t_dev = t_dev;
     p.n_out = n_out;
     p.k_dim = k_dim;
     p.t_rows = t_rows;
@@ -380,6 +392,7 @@ int run_gemm(sp_group* grp, int kind, const CUtensorMap& wmap, const XMaps& xm, 
   }
   sp::GemmParams p{};
   p.l2_prefetch = l2_prefetch;
+  p.t_dev = t_dev;
   p.n_out = n_out;
   p.k_dim = k_dim;
   p.t_rows = t_rows;
@@ -421,8 +434,12 @@ int run_gemm(sp_group* grp, int kind, const CUtensorMap& wmap, const XMaps& xm, 
   return 1;
 }
 
+// dyn = true (graph capture): n_tokens / max_len are bucket bounds used for grids and tiles; every
+// kernel reads the live token count from cu_seqlens[n_seqs] on the device.
 int bert_forward(sp_group* g, const int32_t* ids, const int32_t* cu, int n_seqs, int n_tokens, int max_len, int k,
-                 float* rep, float* logits, int add_bias, cudaStream_t st) {
+                 float* rep, float* logits, int add_bias, cudaStream_t st, bool dyn = false) {
+  const int n_rows_arg = dyn ? -n_tokens : n_tokens;  // row kernels: negative = live count on device
+  const int* t_dev = dyn ? cu + n_seqs : nullptr;
   const sp_config& c = g->cfg;
   const sp_weights& w = g->w;
   const int S = c.n_students, H = c.hidden, F = c.ffn, T = c.max_tokens, B = c.max_seqs;
@@ -446,7 +463,7 @@ int bert_forward(sp_group* g, const int32_t* ids, const int32_t* cu, int n_seqs,
   const double GTH = (double)k * n_tokens * H;
   if (k > 0) {
     g->rec_begin(SP_LAUNCH_EMBED_LN, GTH * 10.0, 0.0);
-    sp::launch_embed_ln(ids, cu, n_seqs, n_tokens, k, static_cast<const half*>(w.word_emb),
+    sp::launch_embed_ln(ids, cu, n_seqs, n_rows_arg, k, static_cast<const half*>(w.word_emb),
                         static_cast<const half*>(w.pos_emb), static_cast<const half*>(w.type_emb),
                         (long long)c.vocab * H, (long long)c.max_pos * H, w.emb_ln_gamma, w.emb_ln_beta, H, c.ln_eps,
                         g->x32, g->x16, xgs, st, PF(pf(w.w_qkv, (size_t)k * 3 * H * H)));
@@ -460,7 +477,7 @@ int bert_forward(sp_group* g, const int32_t* ids, const int32_t* cu, int n_seqs,
     for (int l = 0; l < c.n_layers; ++l) {
       const size_t lS = (size_t)l * S;
       launches += run_gemm(g, SP_LAUNCH_GEMM_QKV, g->m_qkv[l], g->xm_x16, k, 3 * H, H, n_tokens, T, w.b_qkv + lS * 3 * H, 3 * H,
-                           sp::ACT_NONE, g->qkv, (long long)T * 3 * H, 0, 1, 0, st);
+                           sp::ACT_NONE, g->qkv, (long long)T * 3 * H, 0, 1, 0, st, t_dev);
       g->rec_begin(SP_LAUNCH_ATTENTION, GTH * 8.0, 4.0 * k * H * g->sum_len_sq);
       if (use_attn_tc(H / c.n_heads, max_len))
         sp::launch_attention_tc(g->m_qkv_attn, g->ctx, cu, n_seqs, max_len, k, c.n_heads, H, T, st);
@@ -471,21 +488,21 @@ int bert_forward(sp_group* g, const int32_t* ids, const int32_t* cu, int n_seqs,
       ++launches;
       // O and FFN2 write raw partial sums; the reduce+LN kernel owns bias, residual and LayerNorm
       launches += run_gemm(g, SP_LAUNCH_GEMM_O, g->m_o[l], g->xm_ctx, k, H, H, n_tokens, T, nullptr, H, sp::ACT_NONE, g->part, xgs, 1,
-                           s_o, part_ss, st);
+                           s_o, part_ss, st, t_dev);
       g->rec_begin(SP_LAUNCH_REDUCE_LN, GTH * (4.0 * s_o + 10.0), 0.0);
       sp::launch_reduce_ln(g->part, s_o, part_ss, w.b_o + lS * H, w.ln1_gamma + lS * H, w.ln1_beta + lS * H, H,
-                           c.ln_eps, g->x32, g->x16, xgs, n_tokens, k, cu, n_seqs, nullptr, 0, st,
+                           c.ln_eps, g->x32, g->x16, xgs, n_rows_arg, k, cu, n_seqs, nullptr, 0, st,
                            PF(pf(w1 + lS * F * H, (size_t)k * F * H)));
       g->rec_end();
       ++launches;
       launches += run_gemm(g, SP_LAUNCH_GEMM_FFN1, g->m_f1[l], g->xm_x16, k, F, H, n_tokens, T, w.b_ffn1 + lS * F, F, sp::ACT_GELU, g->ffn,
-                           (long long)T * F, 0, 1, 0, st);
+                           (long long)T * F, 0, 1, 0, st, t_dev);
       launches += run_gemm(g, SP_LAUNCH_GEMM_FFN2, g->m_f2[l], g->xm_ffn, k, H, F, n_tokens, T, nullptr, H, sp::ACT_NONE, g->part, xgs, 1,
-                           s_f, part_ss, st);
+                           s_f, part_ss, st, t_dev);
       const bool last = (l == c.n_layers - 1);
       g->rec_begin(SP_LAUNCH_REDUCE_LN, GTH * (4.0 * s_f + 10.0), 0.0);
       sp::launch_reduce_ln(g->part, s_f, part_ss, w.b_ffn2 + lS * H, w.ln2_gamma + lS * H, w.ln2_beta + lS * H, H,
-                           c.ln_eps, g->x32, g->x16, xgs, n_tokens, k, cu, n_seqs, last ? g->cls16 : nullptr,
+                           c.ln_eps, g->x32, g->x16, xgs, n_rows_arg, k, cu, n_seqs, last ? g->cls16 : nullptr,
                            (long long)B * H, st,
                            PF(last ? pf(w.w_pool, (size_t)k * H * H) : pf(wq + (lS + S) * 3 * H * H, (size_t)k * 3 * H * H)));
       g->rec_end();
@@ -507,6 +524,42 @@ int bert_forward(sp_group* g, const int32_t* ids, const int32_t* cu, int n_seqs,
   g->rec_end();
   ++launches;
   g->last_launches = launches;
+  return SP_OK;
+}
+
+bool graphs_enabled() {
+  static const bool on = [] {
+    const char* v = getenv("SP_GRAPHS");
+    return v == nullptr || atoi(v) != 0;
+  }();
+  return on;
+}
+
+// Batch-1 host path: one instantiated graph per 16-token bucket replays the whole forward
+// (17 PDL-chained kernels) with a single launch; kernels read the live length from d_cu.
+int get_graph(sp_group* g, int n_tokens, int k, int add_bias, cudaGraphExec_t* out) {
+  const int bucket = std::min(((n_tokens + 15) / 16) * 16, std::max(16, g->cfg.max_tokens));
+  const auto key = std::make_tuple(bucket, k, add_bias);
+  auto it = g->graphs.find(key);
+  if (it != g->graphs.end()) {
+    *out = it->second;
+    return SP_OK;
+  }
+  if (g->cap_stream == nullptr) SP_CUDA(cudaStreamCreateWithFlags(&g->cap_stream, cudaStreamNonBlocking));
+  SP_CUDA(cudaStreamBeginCapture(g->cap_stream, cudaStreamCaptureModeThreadLocal));
+  const int max_len = std::min(bucket, g->cfg.max_pos);
+  int rc = bert_forward(g, g->d_ids, g->d_cu, 1, bucket, max_len, k, nullptr, g->d_logits, add_bias, g->cap_stream, true);
+  cudaGraph_t graph = nullptr;
+  cudaError_t e = cudaStreamEndCapture(g->cap_stream, &graph);
+  if (rc) return rc;
+  if (e != cudaSuccess) return fail(SP_ECUDA, "graph capture: %s", cudaGetErrorString(e));
+  cudaGraphExec_t exec = nullptr;
+  e = cudaGraphInstantiate(&exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (e != cudaSuccess) return fail(SP_ECUDA, "graph instantiate: %s", cudaGetErrorString(e));
+  g->graph_launches = g->last_launches;
+  g->graphs[key] = exec;
+  *out = exec;
   return SP_OK;
 }
 
@@ -620,10 +673,21 @@ int sp_group_forward_host(sp_group* g, const int32_t* ids, const int32_t* cu, in
     if (ids[t] < 0 || ids[t] >= c.vocab) return fail(SP_EINVAL, "token id %d at %d outside vocab", ids[t], t);
   cudaSetDevice(g->device);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const bool use_graph = graphs_enabled() && n_seqs == 1 && !g->profiling;
+  cudaGraphExec_t exec = nullptr;
+  if (use_graph) {
+    int rc = get_graph(g, n_tokens, k_active, add_bias, &exec);
+    if (rc) return rc;
+  }
   SP_CUDA(cudaMemcpyAsync(g->d_ids, ids, sizeof(int32_t) * n_tokens, cudaMemcpyHostToDevice, st));
   SP_CUDA(cudaMemcpyAsync(g->d_cu, cu, sizeof(int32_t) * (n_seqs + 1), cudaMemcpyHostToDevice, st));
-  int rc = bert_forward(g, g->d_ids, g->d_cu, n_seqs, n_tokens, max_len, k_active, nullptr, g->d_logits, add_bias, st);
-  if (rc) return rc;
+  if (use_graph) {
+    SP_CUDA(cudaGraphLaunch(exec, st));
+    g->last_launches = g->graph_launches;
+  } else {
+    int rc = bert_forward(g, g->d_ids, g->d_cu, n_seqs, n_tokens, max_len, k_active, nullptr, g->d_logits, add_bias, st);
+    if (rc) return rc;
+  }
   SP_CUDA(cudaGetLastError());
   SP_CUDA(cudaMemcpyAsync(logits_out, g->d_logits, sizeof(float) * n_seqs * c.n_classes, cudaMemcpyDeviceToHost, st));
   SP_CUDA(cudaStreamSynchronize(st));
@@ -679,3 +743,19 @@ int sp_op_attention(const void* qkv, void* ctx, const int32_t* cu_seqlens, int32
 }
 
 }  // extern "C"
+
+extern "C" int sp_group_prepare_graphs(sp_group* g, int32_t max_tokens, int32_t k_active, int32_t add_bias) {
+  if (g == nullptr) return fail(SP_EINVAL, "null group");
+  if (g->cfg.kind != SP_KIND_BERT) return fail(SP_EINVAL, "graphs serve BERT-kind groups");
+  if (k_active < 0 || k_active > g->cfg.n_students) return fail(SP_EINVAL, "k out of range");
+  if (!graphs_enabled()) return SP_OK;
+  cudaSetDevice(g->device);
+  const int top = std::min(max_tokens, g->cfg.max_tokens);
+  for (int t = 16; t - 15 <= top; t += 16) {
+    cudaGraphExec_t exec;
+    int rc = get_graph(g, t, k_active, add_bias, &exec);
+    if (rc) return rc;
+  }
+  return SP_OK;
+}
+

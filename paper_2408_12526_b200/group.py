@@ -167,6 +167,14 @@ class StudentGroup:
     def last_launches(self) -> int:
         return int(self._lib.sp_group_last_launches(self._handle))
 
+    def prepare_graphs(self, max_tokens: int | None = None, k: int | None = None, add_bias: bool = True) -> None:
+        """Capture the batch-1 CUDA graphs of forward_host ahead of time (one per 16-token bucket)."""
+        if self.kind != "bert":
+            raise ValueError("graphs serve BERT-kind groups")
+        kl = self.local_k(k)
+        _lib.check(self._lib.sp_group_prepare_graphs(self._handle, int(max_tokens or self.max_tokens), kl,
+                                                     int(add_bias)))
+
     def set_profiling(self, enable: bool) -> None:
         _lib.check(self._lib.sp_group_set_profiling(self._handle, int(enable)))
 

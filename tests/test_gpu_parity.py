@@ -202,3 +202,22 @@ def test_reference_object_snapshot_if_available(ref):
     grp = StudentGroup.from_ensemble(state)
     x = rng.normal(size=(16, 32))
     assert rel_err_rows(grp.logits(x, 2), state.classifier.forward(state.rep(x, 2))) <= 5e-3
+
+
+def test_host_graph_path_bit_identical_to_device_path():
+    """Batch-1 forward_host replays a captured CUDA graph per 16-token bucket (kernels read the live
+    length from cu_seqlens); it must reproduce the eager device path bit for bit, across buckets
+    and across replays of one bucket with different lengths and k."""
+    from paper_2408_12526_b200 import PRESETS, StudentGroup, random_bert_group
+
+    cfg, K = PRESETS["base"]
+    w = random_bert_group(cfg, 3, seed=21)
+    grp = StudentGroup(w, max_tokens=512, max_seqs=4)
+    grp.prepare_graphs(64, 3)
+    rng = np.random.default_rng(4)
+    for L in (1, 15, 16, 17, 33, 48, 130, 300, 512):
+        ids = _seqs(rng, 1, L, L)[0]
+        for k in (3, 2):
+            z_host = grp.forward_host(ids, np.array([0, L], np.int32), k)
+            z_dev = grp.logits([ids], k).astype(np.float32)
+            np.testing.assert_array_equal(z_host, z_dev)
