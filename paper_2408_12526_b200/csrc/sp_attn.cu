@@ -52,7 +52,7 @@ __device__ __forceinline__ void cp_async_wait() {
 }
 
 template <int D, int NW>
-__global__ void __launch_bounds__(32 * NW, NW == 8 ? 2 : 4)
+__global__ void __launch_bounds__(32 * NW, NW == 4 ? 4 : 2)
     attn_kernel(const half* __restrict__ qkv, half* __restrict__ ctx, const int* __restrict__ cu, int n_heads,
                 int hidden, long long group_rows, float scale_log2, const void* pf_ptr, unsigned long long pf_bytes) {
   constexpr int BQ = 16 * NW, BK = 64, LD = D + 8;  // +8 halfs: conflict-free ldmatrix rows
@@ -244,14 +244,24 @@ void launch_attention(const half* qkv, half* ctx, const int* cu_seqlens, int n_s
                       const void* pf_ptr, unsigned long long pf_bytes) {
   if (n_seqs <= 0 || max_len <= 0 || groups <= 0) return;
   const float scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(head_dim));
-  const bool big = max_len > 128;  // 128-query CTAs halve K/V re-reads on long sequences
+  // query-tile height: SP_ATTN_NW overrides (4, 6 or 8 warps of 16 rows); default by length
+  static const int nw_env = [] {
+    const char* v = getenv("SP_ATTN_NW");
+    return v ? atoi(v) : 0;
+  }();
+  const int nw = nw_env ? nw_env : (max_len <= 64 ? 4 : (max_len <= 384 ? 6 : 8));  // measured sweep
+#define SP_ATTN(D_, NW_) \
+  launch_attn_t<D_, NW_>(qkv, ctx, cu_seqlens, n_seqs, max_len, groups, n_heads, hidden, group_rows, scale_log2, pf_ptr, pf_bytes, stream)
   if (head_dim == 64) {
-    if (big) launch_attn_t<64, 8>(qkv, ctx, cu_seqlens, n_seqs, max_len, groups, n_heads, hidden, group_rows, scale_log2, pf_ptr, pf_bytes, stream);
-    else launch_attn_t<64, 4>(qkv, ctx, cu_seqlens, n_seqs, max_len, groups, n_heads, hidden, group_rows, scale_log2, pf_ptr, pf_bytes, stream);
+    if (nw == 8) SP_ATTN(64, 8);
+    else if (nw == 6) SP_ATTN(64, 6);
+    else SP_ATTN(64, 4);
   } else {
-    if (big) launch_attn_t<32, 8>(qkv, ctx, cu_seqlens, n_seqs, max_len, groups, n_heads, hidden, group_rows, scale_log2, pf_ptr, pf_bytes, stream);
-    else launch_attn_t<32, 4>(qkv, ctx, cu_seqlens, n_seqs, max_len, groups, n_heads, hidden, group_rows, scale_log2, pf_ptr, pf_bytes, stream);
+    if (nw == 8) SP_ATTN(32, 8);
+    else if (nw == 6) SP_ATTN(32, 6);
+    else SP_ATTN(32, 4);
   }
+#undef SP_ATTN
 }
 
 }  // namespace sp

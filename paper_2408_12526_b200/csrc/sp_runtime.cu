@@ -335,11 +335,12 @@ namespace {
 
 #define PF(x) (x).p, (x).n
 
-// Tensor-core attention for head_dim 64 and L <= 512 (SP_ATTN_TC=0 forces the mma.sync kernel).
+// Tensor-core attention (head_dim 64, L <= 512) is opt-in (SP_ATTN_TC=1): it is correct but measured
+// slower than the pipelined mma.sync kernel at every batch-1 length.
 bool use_attn_tc(int head_dim, int max_len) {
   static const bool on = [] {
     const char* v = getenv("SP_ATTN_TC");
-    return v == nullptr || atoi(v) != 0;
+    return v != nullptr && atoi(v) != 0;
   }();
   return on && head_dim == 64 && max_len <= 512;
 }
