@@ -490,9 +490,24 @@ static void launch_persistent_t(const GemmMaps& maps, const GemmParams& p, int g
   cudaLaunchKernelEx(&cfg, gemm_persistent_kernel<ACT, OUT_F32>, maps.w, maps.x64, maps.x16, q);
 }
 
-// Tile policy of the persistent path: bn <= 256, ring as deep as the smem left after staging.
-void gemm_configure_persistent(int t_rows, bool out_f32, int* bn, int* n_tiles, int* stages) {
-  int tiles = (t_rows + 255) / 256;
+// Tile policy of the persistent path: pick the token-tile count that minimises the makespan
+// ceil(units / CTAs) x (fixed + bn) (bn <= 256), so projections with few feature tiles (O, FFN2:
+// 6 per student) still fill every SM; ring as deep as the smem left after staging.
+void gemm_configure_persistent(int t_rows, bool out_f32, int units_per_tile, int n_ctas, int* bn, int* n_tiles,
+                               int* stages) {
+  int best_tiles = (t_rows + 255) / 256, best_cost = 0x7fffffff;
+  for (int tiles = (t_rows + 255) / 256; tiles <= (t_rows + 63) / 64; ++tiles) {
+    const int per = (t_rows + tiles - 1) / tiles;
+    const int b = ((per + 15) / 16) * 16;
+    const int units = units_per_tile * tiles;
+    const int rounds = (units + n_ctas - 1) / n_ctas;
+    const int cost = rounds * (64 + b);  // ~64 tokens' worth of per-tile fixed cost (fill, epilogue)
+    if (cost < best_cost) {
+      best_cost = cost;
+      best_tiles = tiles;
+    }
+  }
+  const int tiles = best_tiles;
   const int per = (t_rows + tiles - 1) / tiles;
   int b = ((per + 15) / 16) * 16;
   *bn = b;
@@ -516,6 +531,16 @@ void launch_gemm_persistent(const GemmMaps& maps, const GemmParams& p, int group
     if (f32) launch_persistent_t<ACT_NONE, true>(maps, p, groups, stream);
     else launch_persistent_t<ACT_NONE, false>(maps, p, groups, stream);
   }
+}
+
+int sm_count() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return n;
 }
 
 static unsigned long long* g_trace = nullptr;

@@ -76,7 +76,9 @@ struct GemmMaps {
 void launch_gemm(const GemmMaps& maps, const GemmParams& p, int groups, cudaStream_t stream);
 // Persistent variant for large token counts (splits must be 1).
 void launch_gemm_persistent(const GemmMaps& maps, const GemmParams& p, int groups, cudaStream_t stream);
-void gemm_configure_persistent(int t_rows, bool out_f32, int* bn, int* n_tiles, int* stages);
+void gemm_configure_persistent(int t_rows, bool out_f32, int units_per_tile, int n_ctas, int* bn, int* n_tiles,
+                               int* stages);
+int sm_count();
 size_t gemm_smem_bytes(int bn, int stages);
 void gemm_configure_tiles(int t_rows, bool cluster2, int* bn, int* n_tiles, int* stages);
 
