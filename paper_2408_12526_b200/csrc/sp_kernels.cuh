@@ -74,6 +74,24 @@ struct GemmMaps {
 };
 
 void launch_gemm(const GemmMaps& maps, const GemmParams& p, int groups, cudaStream_t stream);
+
+// Projection + bias + residual + LayerNorm (cluster of the n_out/128 feature-tile CTAs of a row).
+struct LnParams {
+  const float* bias;   // [groups][hidden]
+  const float* gamma;  // [groups][hidden]
+  const float* beta;
+  float eps;
+  float* x32;          // residual in / normalised out, [groups][x_gs]
+  half* x16;           // normalised out (next GEMM operand)
+  long long x_gs;      // elements per student
+  half* cls16;         // optional CLS rows [groups][cls_gs]
+  long long cls_gs;
+  const int* cu;
+  int n_seqs;
+  int hidden;
+};
+void launch_gemm_ln(const GemmMaps& maps, const GemmParams& p, const LnParams& ln, int groups, cudaStream_t stream);
+size_t gemm_ln_smem_bytes(int bn, int stages);
 // Persistent variant for large token counts (splits must be 1).
 void launch_gemm_persistent(const GemmMaps& maps, const GemmParams& p, int groups, cudaStream_t stream);
 void gemm_configure_persistent(int t_rows, bool out_f32, int units_per_tile, int n_ctas, int* bn, int* n_tiles,

@@ -436,6 +436,52 @@ int run_gemm(sp_group* grp, int kind, const CUtensorMap& wmap, const XMaps& xm, 
   return 1;
 }
 
+// Fused projection + bias + residual + LayerNorm (sp_gemm_ln.cu). Returns 1 (launches).
+int run_gemm_ln(sp_group* grp, int kind, const CUtensorMap& wmap, const XMaps& xm, int groups, int n_out, int k_dim,
+                int t_rows, int x_group_rows, const sp::LnParams& ln, const int* t_dev, cudaStream_t st) {
+  sp::GemmParams p{};
+  p.t_dev = t_dev;
+  p.n_out = n_out;
+  p.k_dim = k_dim;
+  p.t_rows = t_rows;
+  p.x_group_rows = x_group_rows;
+  p.m_tiles = n_out / 128;
+  p.splits = 1;
+  p.kb_per_split = k_dim / 64;
+  p.cluster = 1;
+  sp::gemm_configure_tiles(t_rows, false, &p.bn, &p.n_tiles, &p.stages);
+  // the row buffer (bn x 129 fp32) reuses the ring after the main loop
+  while ((size_t)p.stages * (16384 + p.bn * 128) < (size_t)p.bn * 129 * 4) ++p.stages;
+  sp::GemmMaps maps;
+  maps.w = wmap;
+  maps.x64 = xm.x64;
+  maps.x16 = xm.x16;
+  if (grp) {
+    const double G = groups, N = n_out, K = k_dim, T = t_rows;
+    grp->rec_begin(kind, G * N * K * 2.0 + G * T * K * 2.0 + G * T * N * (4.0 + 4.0 + 2.0), 2.0 * G * N * K * T);
+  }
+  sp::launch_gemm_ln(maps, p, ln, groups, st);
+  if (grp) grp->rec_end();
+  return 1;
+}
+
+// Fused LayerNorm epilogue for a projection: opt-in (SP_LN_FUSE=1). Measured slower at every
+// batch-1 length on B200 — one CTA per feature tile with full K leaves only 48-96 CTAs streaming
+// weights, while split-K + reduce_ln keeps 144+ streams in flight.
+bool use_ln_fused(int m_tiles, int n_tiles, int groups, int k_dim, int hidden) {
+  static const int mode = [] {
+    const char* v = getenv("SP_LN_FUSE");
+    return v ? atoi(v) : 0;
+  }();
+  static const int min_ctas_long_k = [] {
+    const char* v = getenv("SP_LN_FUSE_MIN_CTAS");
+    return v ? atoi(v) : 96;
+  }();
+  if (mode == 0 || m_tiles > 8) return false;
+  if (k_dim <= hidden) return true;
+  return m_tiles * n_tiles * groups >= min_ctas_long_k;
+}
+
 // dyn = true (graph capture): n_tokens / max_len are bucket bounds used for grids and tiles; every
 // kernel reads the live token count from cu_seqlens[n_seqs] on the device.
 int bert_forward(sp_group* g, const int32_t* ids, const int32_t* cu, int n_seqs, int n_tokens, int max_len, int k,
@@ -489,26 +535,38 @@ int bert_forward(sp_group* g, const int32_t* ids, const int32_t* cu, int n_seqs,
       g->rec_end();
       ++launches;
       // O and FFN2 write raw partial sums; the reduce+LN kernel owns bias, residual and LayerNorm
-      launches += run_gemm(g, SP_LAUNCH_GEMM_O, g->m_o[l], g->xm_ctx, k, H, H, n_tokens, T, nullptr, H, sp::ACT_NONE, g->part, xgs, 1,
-                           s_o, part_ss, st, t_dev);
-      g->rec_begin(SP_LAUNCH_REDUCE_LN, GTH * (4.0 * s_o + 10.0), 0.0);
-      sp::launch_reduce_ln(g->part, s_o, part_ss, w.b_o + lS * H, w.ln1_gamma + lS * H, w.ln1_beta + lS * H, H,
-                           c.ln_eps, g->x32, g->x16, xgs, n_rows_arg, k, cu, n_seqs, nullptr, 0, st,
-                           PF(pf(w1 + lS * F * H, (size_t)k * F * H)));
-      g->rec_end();
-      ++launches;
+      if (use_ln_fused(H / 128, n_tiles, k, H, H)) {
+        sp::LnParams ln{w.b_o + lS * H, w.ln1_gamma + lS * H, w.ln1_beta + lS * H, c.ln_eps, g->x32, g->x16, xgs,
+                        nullptr, 0, cu, n_seqs, H};
+        launches += run_gemm_ln(g, SP_LAUNCH_GEMM_O, g->m_o[l], g->xm_ctx, k, H, H, n_tokens, T, ln, t_dev, st);
+      } else {
+        launches += run_gemm(g, SP_LAUNCH_GEMM_O, g->m_o[l], g->xm_ctx, k, H, H, n_tokens, T, nullptr, H, sp::ACT_NONE,
+                             g->part, xgs, 1, s_o, part_ss, st, t_dev);
+        g->rec_begin(SP_LAUNCH_REDUCE_LN, GTH * (4.0 * s_o + 10.0), 0.0);
+        sp::launch_reduce_ln(g->part, s_o, part_ss, w.b_o + lS * H, w.ln1_gamma + lS * H, w.ln1_beta + lS * H, H,
+                             c.ln_eps, g->x32, g->x16, xgs, n_rows_arg, k, cu, n_seqs, nullptr, 0, st,
+                             PF(pf(w1 + lS * F * H, (size_t)k * F * H)));
+        g->rec_end();
+        ++launches;
+      }
       launches += run_gemm(g, SP_LAUNCH_GEMM_FFN1, g->m_f1[l], g->xm_x16, k, F, H, n_tokens, T, w.b_ffn1 + lS * F, F, sp::ACT_GELU, g->ffn,
                            (long long)T * F, 0, 1, 0, st, t_dev);
-      launches += run_gemm(g, SP_LAUNCH_GEMM_FFN2, g->m_f2[l], g->xm_ffn, k, H, F, n_tokens, T, nullptr, H, sp::ACT_NONE, g->part, xgs, 1,
-                           s_f, part_ss, st, t_dev);
       const bool last = (l == c.n_layers - 1);
-      g->rec_begin(SP_LAUNCH_REDUCE_LN, GTH * (4.0 * s_f + 10.0), 0.0);
-      sp::launch_reduce_ln(g->part, s_f, part_ss, w.b_ffn2 + lS * H, w.ln2_gamma + lS * H, w.ln2_beta + lS * H, H,
-                           c.ln_eps, g->x32, g->x16, xgs, n_rows_arg, k, cu, n_seqs, last ? g->cls16 : nullptr,
-                           (long long)B * H, st,
-                           PF(last ? pf(w.w_pool, (size_t)k * H * H) : pf(wq + (lS + S) * 3 * H * H, (size_t)k * 3 * H * H)));
-      g->rec_end();
-      ++launches;
+      if (use_ln_fused(H / 128, n_tiles, k, F, H)) {
+        sp::LnParams ln{w.b_ffn2 + lS * H, w.ln2_gamma + lS * H, w.ln2_beta + lS * H, c.ln_eps, g->x32, g->x16, xgs,
+                        last ? g->cls16 : nullptr, (long long)B * H, cu, n_seqs, H};
+        launches += run_gemm_ln(g, SP_LAUNCH_GEMM_FFN2, g->m_f2[l], g->xm_ffn, k, H, F, n_tokens, T, ln, t_dev, st);
+      } else {
+        launches += run_gemm(g, SP_LAUNCH_GEMM_FFN2, g->m_f2[l], g->xm_ffn, k, H, F, n_tokens, T, nullptr, H,
+                             sp::ACT_NONE, g->part, xgs, 1, s_f, part_ss, st, t_dev);
+        g->rec_begin(SP_LAUNCH_REDUCE_LN, GTH * (4.0 * s_f + 10.0), 0.0);
+        sp::launch_reduce_ln(g->part, s_f, part_ss, w.b_ffn2 + lS * H, w.ln2_gamma + lS * H, w.ln2_beta + lS * H, H,
+                             c.ln_eps, g->x32, g->x16, xgs, n_rows_arg, k, cu, n_seqs, last ? g->cls16 : nullptr,
+                             (long long)B * H, st,
+                             PF(last ? pf(w.w_pool, (size_t)k * H * H) : pf(wq + (lS + S) * 3 * H * H, (size_t)k * 3 * H * H)));
+        g->rec_end();
+        ++launches;
+      }
     }
     // pooler on the CLS rows: tanh(W_p h_CLS + b_p). Few rows: split-K partials (more CTAs stream the
     // pooler weights), finished by the head kernel; many rows: one pass with the tanh epilogue.

@@ -221,3 +221,30 @@ def test_host_graph_path_bit_identical_to_device_path():
             z_host = grp.forward_host(ids, np.array([0, L], np.int32), k)
             z_dev = grp.logits([ids], k).astype(np.float32)
             np.testing.assert_array_equal(z_host, z_dev)
+
+
+@pytest.mark.parametrize("env", ["SP_LN_FUSE=1", "SP_ATTN_TC=1", "SP_GEMM_CLUSTER=1"])
+def test_opt_in_kernel_variants_match_oracle(env):
+    """The opt-in kernel variants (fused projection+LayerNorm, tcgen05 attention, cluster-multicast
+    GEMM) stay correct: run a fresh process with the knob set (knobs are read once per process)."""
+    import subprocess
+    import sys
+
+    code = (
+        "import numpy as np, sys; sys.path.insert(0, '.'); sys.path.insert(0, 'tests')\n"
+        "from oracle.bert import OracleBertGroup\n"
+        "from paper_2408_12526_b200 import PRESETS, StudentGroup, random_bert_group\n"
+        "cfg, K = PRESETS['base']; w = random_bert_group(cfg, 3, seed=5)\n"
+        "g = StudentGroup(w, max_tokens=1024, max_seqs=4); o = OracleBertGroup(w)\n"
+        "rng = np.random.default_rng(0)\n"
+        "for L in (16, 200, 512):\n"
+        "    ids = np.r_[101, rng.integers(1000, 30522, size=L - 1)].astype(np.int32)\n"
+        "    z = g.logits([ids]); _, zr = o.forward([ids])\n"
+        "    err = float(np.abs(z - zr).max() / np.abs(zr).max()); assert err <= 1e-3, (L, err)\n"
+        "print('ok')\n")
+    key, val = env.split("=")
+    import os
+
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600,
+                       env={**os.environ, key: val}, cwd=str(__import__("pathlib").Path(__file__).resolve().parents[1]))
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
