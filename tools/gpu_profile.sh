@@ -1,6 +1,7 @@
 # Round profile: bench lines + ncu launch list + full captures of the top kernels.
 set -x
 mkdir -p gpurun_out
+timeout 300 python -m pytest tests/test_gpu_parity.py -q -k opt_in 2>&1 | tail -2
 timeout 600 python bench.py > gpurun_out/bench_b8.json 2> gpurun_out/bench_b8.err; echo "bench b8 rc=$?"
 timeout 900 python bench.py --config large --batch 16 --steps 40 --warmup 4 --no-cpu-baseline --profile-steps 10 > gpurun_out/bench_l12_b16.json 2> gpurun_out/bench_l12_b16.err; echo "bench l12 rc=$?"
 S="python bench.py --steps 20 --warmup 3 --no-cpu-baseline --profile-steps 2"
