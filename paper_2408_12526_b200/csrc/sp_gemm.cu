@@ -248,8 +248,7 @@ __global__ void __launch_bounds__(kThreads, 2)
 
 // Debug trace: launches append their per-CTA stamps one after another (slot 0 of the buffer
 // holds the number of CTAs recorded so far, host-side mirror in g_trace_used).
-static void g_trace_counts_push(int n);
-static bool trace_on();
+static unsigned long long* trace_ptr_advance(int ctas);
 
 // ============================================================================ persistent variant
 // For large token counts (T > 128: long batch-1 requests, batched load) one CTA per SM loops over
@@ -258,9 +257,11 @@ static bool trace_on();
 // pipeline fill nor the epilogue is paid per tile, and there are no partial waves. Tiles are
 // ordered m-tile fastest, so concurrently running CTAs share one token tile (L2 hits).
 static constexpr int kPersistTmemCols = 512;  // 2 accumulators x 256 columns
+static constexpr int kPEpiWarps = 16;          // 4 warps per TMEM lane quadrant, a quarter of the columns each
+static constexpr int kPThreads = 64 + 32 * kPEpiWarps;
 
 template <int ACT, bool OUT_F32>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kPThreads, 1)
     gemm_persistent_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_x64,
                            const __grid_constant__ CUtensorMap map_x16, const GemmParams p) {
   using OutT = typename std::conditional<OUT_F32, float, half>::type;
@@ -270,8 +271,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int stage_bytes = kATileBytes + p.bn * 128;
-  uint8_t* staging = smem + p.stages * stage_bytes;  // 8 warps x 32 rows x kRowBytes
-  uint64_t* full = reinterpret_cast<uint64_t*>(staging + kEpiWarps * 32 * kRowBytes);
+  uint8_t* staging = smem + p.stages * stage_bytes;  // 16 warps x 16 rows x kRowBytes
+  uint64_t* full = reinterpret_cast<uint64_t*>(staging + kPEpiWarps * 16 * kRowBytes);
   uint64_t* empty = full + p.stages;
   uint64_t* acc_full = empty + p.stages;  // [2]
   uint64_t* acc_empty = acc_full + 2;     // [2]
@@ -279,18 +280,27 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = warp_id();
   const int lane = lane_id();
-  const int units_per_group = p.m_tiles * p.n_tiles;
+  unsigned long long* tr = p.trace ? p.trace + 8ull * blockIdx.x : nullptr;
+  if (tr && threadIdx.x == 0) tr[0] = globaltimer();
+  // pair mode (cluster of 2): the CTAs of a pair take neighbouring feature tiles of the same token
+  // tile in lockstep and TMA-multicast half of the token tile each (a third less L2->SM traffic)
+  const bool pair = p.cluster == 2;
+  const uint32_t crank = pair ? cluster_ctarank() : 0u;
+  const int m_per = pair ? (p.m_tiles >> 1) : p.m_tiles;
+  const int units_per_group = m_per * p.n_tiles;
   const int units = units_per_group * p.groups;
+  const int u_first = pair ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int u_stride = pair ? (int)(gridDim.x >> 1) : (int)gridDim.x;
   const int nkb = p.k_dim / kBlockK;
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < p.stages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], pair ? 2 : 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&acc_full[b], 1);
-      mbar_init(&acc_empty[b], kEpiWarps);
+      mbar_init(&acc_empty[b], kPEpiWarps);
     }
     fence_barrier_init();
     tma_prefetch_desc(&map_w);
@@ -303,6 +313,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if (pair) cluster_sync();  // peer barriers initialised before any multicast
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   pdl_launch_dependents();
@@ -310,18 +321,31 @@ __global__ void __launch_bounds__(kThreads, 1)
   auto decode = [&](int u, int& g, int& mt, int& nt) {
     g = u / units_per_group;
     const int r = u % units_per_group;
-    nt = r / p.m_tiles;
-    mt = r % p.m_tiles;
+    nt = r / m_per;
+    mt = pair ? 2 * (r % m_per) + static_cast<int>(crank) : r % m_per;
   };
 
   if (warp == 0) {
     if (elect_one()) {
       const uint64_t pol_w = policy_evict_last();  // re-read by the other token tiles
       const uint64_t pol_x = policy_evict_last();
+      const int r_begin = pair ? static_cast<int>(crank) * (p.bn >> 1) : 0;
+      const int r_end = pair ? r_begin + (p.bn >> 1) : p.bn;
+      auto load_x = [&](int s, int kb, int xrow) {
+        uint8_t* sb = smem + s * stage_bytes + kATileBytes;
+        int r = r_begin;
+        if (pair) {
+          for (; r + 64 <= r_end; r += 64) tma_load_2d_mc(&map_x64, &full[s], sb + r * 128, kb * kBlockK, xrow + r, 0x3, pol_x);
+          for (; r < r_end; r += 16) tma_load_2d_mc(&map_x16, &full[s], sb + r * 128, kb * kBlockK, xrow + r, 0x3, pol_x);
+        } else {
+          for (; r + 64 <= r_end; r += 64) tma_load_2d(&map_x64, &full[s], sb + r * 128, kb * kBlockK, xrow + r, pol_x);
+          for (; r < r_end; r += 16) tma_load_2d(&map_x16, &full[s], sb + r * 128, kb * kBlockK, xrow + r, pol_x);
+        }
+      };
       int s = 0;
       uint32_t ph = 0;
       bool first = true;
-      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      for (int u = u_first; u < units; u += u_stride) {
         int g, mt, nt;
         decode(u, g, mt, nt);
         const int wrow = g * p.n_out + mt * kBlockM;
@@ -335,13 +359,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           if (p.l2_prefetch)
             for (int i = n_pre; i < nkb; ++i) tma_prefetch_l2_2d(&map_w, i * kBlockK, wrow);
+          if (tr) tr[2] = globaltimer();
           pdl_wait();
-          for (int i = 0; i < n_pre; ++i) {
-            uint8_t* sb = smem + i * stage_bytes + kATileBytes;
-            int r = 0;
-            for (; r + 64 <= p.bn; r += 64) tma_load_2d(&map_x64, &full[i], sb + r * 128, i * kBlockK, xrow + r, pol_x);
-            for (; r < p.bn; r += 16) tma_load_2d(&map_x16, &full[i], sb + r * 128, i * kBlockK, xrow + r, pol_x);
-          }
+          for (int i = 0; i < n_pre; ++i) load_x(i, i, xrow);
           kb = n_pre;
           s = n_pre % p.stages;
           ph = (n_pre == p.stages) ? 1u : 0u;
@@ -352,10 +372,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_arrive_expect_tx(&full[s], stage_bytes);
           uint8_t* sa = smem + s * stage_bytes;
           tma_load_2d(&map_w, &full[s], sa, kb * kBlockK, wrow, pol_w);
-          uint8_t* sb = sa + kATileBytes;
-          int r = 0;
-          for (; r + 64 <= p.bn; r += 64) tma_load_2d(&map_x64, &full[s], sb + r * 128, kb * kBlockK, xrow + r, pol_x);
-          for (; r < p.bn; r += 16) tma_load_2d(&map_x16, &full[s], sb + r * 128, kb * kBlockK, xrow + r, pol_x);
+          load_x(s, kb, xrow);
           if (++s == p.stages) {
             s = 0;
             ph ^= 1;
@@ -370,7 +387,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       int s = 0;
       uint32_t ph = 0;
       int j = 0;
-      for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
+      for (int u = u_first; u < units; u += u_stride, ++j) {
         const int b = j & 1;
         mbar_wait(&acc_empty[b], ((j >> 1) & 1) ^ 1);  // epilogue drained this accumulator
         tc_fence_after();
@@ -378,13 +395,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&full[s], ph);
           tc_fence_after();
+          if (tr && j == 0 && kb == 0) tr[4] = globaltimer();
           const uint32_t sa = smem_u32(smem + s * stage_bytes);
           const uint64_t adesc = umma_sdesc_sw128(sa);
           const uint64_t bdesc = umma_sdesc_sw128(sa + kATileBytes);
 #pragma unroll
           for (int k = 0; k < kBlockK / 16; ++k)
             umma_f16_ss(acc, adesc + 2 * k, bdesc + 2 * k, idesc, (kb > 0 || k > 0) ? 1u : 0u);
-          umma_commit(&empty[s]);
+          if (pair) umma_commit_mc(&empty[s], 0x3);
+          else umma_commit(&empty[s]);
           if (++s == p.stages) {
             s = 0;
             ph ^= 1;
@@ -392,17 +411,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         umma_commit(&acc_full[b]);
       }
+      if (tr) tr[5] = globaltimer();
     }
     __syncwarp();
   } else {
     const int e = warp - 2;
     const int q = warp & 3;
-    const int half_cols = p.bn >> 1;
-    const int c_begin = (e >> 2) * half_cols;
-    OutT* stage = reinterpret_cast<OutT*>(staging + e * 32 * kRowBytes);
+    const int part_cols = p.bn >> 2;  // bn is a multiple of 32
+    const int c_begin = (e >> 2) * part_cols;
+    OutT* stage = reinterpret_cast<OutT*>(staging + e * 16 * kRowBytes);
     const int t_rows = p.t_dev ? __ldg(p.t_dev) : p.t_rows;
     int j = 0;
-    for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
+    for (int u = u_first; u < units; u += u_stride, ++j) {
       int g, mt, nt;
       decode(u, g, mt, nt);
       const int b = j & 1;
@@ -412,26 +432,24 @@ __global__ void __launch_bounds__(kThreads, 1)
       OutT* out = reinterpret_cast<OutT*>(p.out) + (long long)g * p.out_group_stride + m0 + q * 32;
       mbar_wait(&acc_full[b], (j >> 1) & 1);
       tc_fence_after();
+      if (tr && j == 0 && warp == 2 && lane == 0) tr[6] = globaltimer();
       const uint32_t taddr = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(b * 256);
-      for (int c = c_begin; c < c_begin + half_cols; c += 32) {
-        const int n = min(32, c_begin + half_cols - c);
-        uint32_t r[32];
-        if (n == 32) {
-          tmem_ld32_nowait(taddr + c, r);
-        } else {
-          for (int i = 0; i < n; i += 8) tmem_ld8_nowait(taddr + c + i, r + i);
-        }
+      for (int c = c_begin; c < c_begin + part_cols; c += 16) {
+        const int n = min(16, c_begin + part_cols - c);  // 8 or 16
+        uint32_t r[16];
+        tmem_ld8_nowait(taddr + c, r);
+        if (n == 16) tmem_ld8_nowait(taddr + c + 8, r + 8);
         tmem_wait_ld();
-        if (c + 32 >= c_begin + half_cols) {  // last TMEM read of this tile: hand the accumulator back
+        if (c + 16 >= c_begin + part_cols) {  // last TMEM read of this tile: hand the accumulator back
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&acc_empty[b]);
         }
-        float y[32];
+        float y[16];
 #pragma unroll
-        for (int jj = 0; jj < 32; ++jj) y[jj] = apply_act<ACT>(__uint_as_float(r[jj]) + bias);
+        for (int jj = 0; jj < 16; ++jj) y[jj] = apply_act<ACT>(__uint_as_float(r[jj]) + bias);
 #pragma unroll
-        for (int jj = 0; jj < 32; ++jj) {
+        for (int jj = 0; jj < 16; ++jj) {
           if constexpr (OUT_F32) stage[jj * 32 + lane] = y[jj];
           else stage[jj * 32 + lane] = __float2half_rn(y[jj]);
         }
@@ -449,10 +467,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
       }
     }
+    if (tr && warp == 2 && lane == 0) tr[7] = globaltimer();
   }
 
   tc_fence_before();
   __syncthreads();
+  if (pair) cluster_sync();  // no CTA leaves while its peer may still multicast or signal into it
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem, kPersistTmemCols);
@@ -471,22 +491,32 @@ static void launch_persistent_t(const GemmMaps& maps, const GemmParams& p, int g
   }
   GemmParams q = p;
   q.groups = groups;
-  q.trace = nullptr;
+  static const bool pair_on = [] {
+    const char* v = getenv("SP_PERSIST_PAIR");
+    return v != nullptr && atoi(v) != 0;
+  }();
   const int units = groups * p.m_tiles * p.n_tiles;
+  q.cluster = (pair_on && p.m_tiles % 2 == 0 && units >= 4) ? 2 : 1;
+  int grid = units < n_sm ? units : n_sm;
+  if (q.cluster == 2) grid &= ~1;
+  q.trace = trace_ptr_advance(grid);
   const int row_bytes = 32 * (OUT_F32 ? 4 : 2);
-  const size_t smem = static_cast<size_t>(p.stages) * (kATileBytes + p.bn * 128) + kEpiWarps * 32 * row_bytes +
+  const size_t smem = static_cast<size_t>(p.stages) * (kATileBytes + p.bn * 128) + kPEpiWarps * 16 * row_bytes +
                       1024 + 256;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(units < n_sm ? units : n_sm);
-  cfg.blockDim = dim3(kThreads);
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kPThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = q.cluster;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  if (trace_on()) g_trace_counts_push(static_cast<int>(cfg.gridDim.x));
+  cfg.numAttrs = 2;
   cudaLaunchKernelEx(&cfg, gemm_persistent_kernel<ACT, OUT_F32>, maps.w, maps.x64, maps.x16, q);
 }
 
@@ -498,7 +528,8 @@ void gemm_configure_persistent(int t_rows, bool out_f32, int units_per_tile, int
   int best_tiles = (t_rows + 255) / 256, best_cost = 0x7fffffff;
   for (int tiles = (t_rows + 255) / 256; tiles <= (t_rows + 63) / 64; ++tiles) {
     const int per = (t_rows + tiles - 1) / tiles;
-    const int b = ((per + 15) / 16) * 16;
+    const int b = ((per + 31) / 32) * 32;  // 16 epilogue warps take a quarter each (multiples of 8)
+    if (b > 256) continue;
     const int units = units_per_tile * tiles;
     const int rounds = (units + n_ctas - 1) / n_ctas;
     const int cost = rounds * (64 + b);  // ~64 tokens' worth of per-tile fixed cost (fill, epilogue)
@@ -509,10 +540,10 @@ void gemm_configure_persistent(int t_rows, bool out_f32, int units_per_tile, int
   }
   const int tiles = best_tiles;
   const int per = (t_rows + tiles - 1) / tiles;
-  int b = ((per + 15) / 16) * 16;
+  int b = ((per + 31) / 32) * 32;
   *bn = b;
   *n_tiles = tiles;
-  const int staging = kEpiWarps * 32 * 32 * (out_f32 ? 4 : 2);
+  const int staging = kPEpiWarps * 16 * 32 * (out_f32 ? 4 : 2);
   int st = (224 * 1024 - staging) / (kATileBytes + b * 128);
   if (st > 8) st = 8;
   if (st < 2) st = 2;
@@ -551,8 +582,13 @@ void set_gemm_trace(unsigned long long* buf) {
   g_trace_used = 0;
   g_trace_counts.clear();
 }
-static void g_trace_counts_push(int n) { g_trace_counts.push_back(n); }
-static bool trace_on() { return g_trace != nullptr; }
+static unsigned long long* trace_ptr_advance(int ctas) {
+  if (!g_trace) return nullptr;
+  unsigned long long* p = g_trace + 8 * g_trace_used;
+  g_trace_used += (size_t)ctas;
+  g_trace_counts.push_back(ctas);
+  return p;
+}
 int gemm_trace_counts(int* out, int max) {
   const int n = static_cast<int>(g_trace_counts.size());
   for (int i = 0; i < n && i < max; ++i) out[i] = g_trace_counts[i];

@@ -284,20 +284,23 @@ __device__ __forceinline__ float warp_sum(float v) {
 
 __device__ __forceinline__ float gelu_erf_exact(float x) { return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f)); }
 
-// erf-GELU with erf from Abramowitz & Stegun 7.1.26 (|error| <= 1.5e-7 absolute on erf):
-// one fast reciprocal, one exp2 and 6 FMAs instead of libdevice erff (~4x fewer instructions).
-// The result is stored as fp16 (relative precision 4.9e-4), far above the approximation error.
+// erf-GELU with erf from Abramowitz & Stegun 7.1.28: erf(z) ~ 1 - (1 + a1 z + ... + a6 z^6)^-16,
+// |error| <= 3e-7 (8.7e-7 measured on the GELU in fp32): one MUFU reciprocal and ~11 FMA/FMUL,
+// no exponential. The result is stored as fp16 (relative precision 4.9e-4).
 __device__ __forceinline__ float gelu_erf(float x) {
   const float z = fabsf(x) * 0.70710678118654752f;
-  const float t = __fdividef(1.0f, fmaf(0.3275911f, z, 1.0f));
-  float poly = fmaf(1.061405429f, t, -1.453152027f);
-  poly = fmaf(poly, t, 1.421413741f);
-  poly = fmaf(poly, t, -0.284496736f);
-  poly = fmaf(poly, t, 0.254829592f);
-  poly *= t;
-  const float e = exp2f(-z * z * 1.4426950408889634f);
-  const float erf_abs = fmaf(-poly, e, 1.0f);
-  const float erf_v = copysignf(erf_abs, x);
+  float p = fmaf(4.30638e-5f, z, 2.765672e-4f);
+  p = fmaf(p, z, 1.520143e-4f);
+  p = fmaf(p, z, 9.2705272e-3f);
+  p = fmaf(p, z, 4.22820123e-2f);
+  p = fmaf(p, z, 7.05230784e-2f);
+  p = fmaf(p, z, 1.0f);
+  float r = __fdividef(1.0f, p);
+  r *= r;  // ^2
+  r *= r;  // ^4
+  r *= r;  // ^8
+  r *= r;  // ^16
+  const float erf_v = copysignf(1.0f - r, x);
   return 0.5f * x * (1.0f + erf_v);
 }
 

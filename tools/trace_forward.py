@@ -9,7 +9,7 @@ lib = _lib.load()
 fw = torch.empty(256 << 18, device="cuda"); fr = torch.ones(256 << 18, device="cuda")
 logits = torch.empty(1, 2, device="cuda")
 tr = torch.zeros(8 * 20000, dtype=torch.int64, device="cuda")
-names = ["qkv", "o", "ffn1", "ffn2"] * 2 + ["pool"]
+names = ["qkv", "o", "ffn1", "ffn2"] * 2 + ["pool"]  # (per-L order of GEMM launches)
 for L in [int(x) for x in sys.argv[1].split(",")]:
     ids = torch.randint(1000, 30000, (L,), dtype=torch.int32, device="cuda")
     cu = torch.tensor([0, L], dtype=torch.int32, device="cuda")
@@ -34,7 +34,10 @@ for L in [int(x) for x in sys.argv[1].split(",")]:
     base = t[:, 0].min()
     off = 0
     print(f"L={L}: event {e0.elapsed_time(e1)*1e3:.1f} us")
-    for nm, n in zip(names, sizes):
+    for li, n in enumerate(sizes):
+        nm = names[li] if li < len(names) else f"g{li}"
         seg = (t[off:off + n] - base) / 1e3; off += n
+        if len(seg) == 0:
+            continue
         print(f"  {nm:5s} ctas={n:4d} entry[{seg[:,0].min():6.1f},{seg[:,0].max():6.1f}] wpre={np.median(seg[:,2]):6.1f} mma0={np.median(seg[:,4]):6.1f} "
               f"last_commit={seg[:,5].max():6.1f} epi0_max={seg[:,6].max():6.1f} end={seg[:,7].max():6.1f}")
