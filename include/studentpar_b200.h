@@ -13,6 +13,8 @@
  *   sp_group_forward_dense <- the same for the reference's dense StudentModel      nnkernel.py:289-301
  *   sp_group_forward_host  <- the same call with HOST buffers (ids in, logits out), the serving seam
  *                             Simulation._dispatch -> service_time                 servesim.py:486, :287-307
+ *   sp_group_forward_eval  <- the forward half of accumulate_prefix_gradients (every student's
+ *   (+ _dense_eval)           final representation, logits of every prefix k) distill.py:483-494
  *   sp_last_error          <- the ValueError / RuntimeError message the reference would raise
  *
  * Conventions: plain pointers and sizes only. "device" pointers are CUDA device addresses on the
@@ -119,6 +121,18 @@ int sp_group_forward(sp_group* group, const int32_t* ids, const int32_t* cu_seql
 /* Dense kind: x fp16 [n_rows][d_in] device (one row per sample, shared by every student). */
 int sp_group_forward_dense(sp_group* group, const void* x, int32_t n_rows, int32_t k_active, float* rep_out,
                            float* logits_out, int32_t add_bias, void* stream);
+
+/* Training-side evaluation (offline distillation / pruning, not the serving path):
+ *   finals_out        fp32 [k_active][n_seqs][hidden]     student m's final representation S_m(x)
+ *                     (the `finals` list of accumulate_prefix_gradients, distill.py:483-486)
+ *   prefix_logits_out fp32 [k_active][n_seqs][n_classes]  classifier(sum_{m<=j} alpha_m S_m(x)) + b_c
+ *                     for every prefix j = 1..k_active (distill.py:489-492), accumulated left to right
+ * Either output may be NULL (not both). Device buffers; k_active >= 1. Not re-entrant per group. */
+int sp_group_forward_eval(sp_group* group, const int32_t* ids, const int32_t* cu_seqlens, int32_t n_seqs,
+                          int32_t n_tokens, int32_t max_seq_len, int32_t k_active, float* finals_out,
+                          float* prefix_logits_out, void* stream);
+int sp_group_forward_dense_eval(sp_group* group, const void* x, int32_t n_rows, int32_t k_active, float* finals_out,
+                                float* prefix_logits_out, void* stream);
 
 /* BERT kind end to end with HOST buffers: validates ids/cu_seqlens like the reference validates its
  * inputs, copies them to the device, runs the group, copies logits back and synchronizes `stream`. */

@@ -176,7 +176,7 @@ __global__ void __launch_bounds__(1024)
     head_kernel(const float* __restrict__ final_rep, long long final_gs, long long split_stride, int splits,
                 const float* __restrict__ b_pool, int groups, const float* __restrict__ alpha,
                 const float* __restrict__ w_cls, const float* __restrict__ b_cls, int n_classes, int hidden,
-                int add_bias, float* __restrict__ rep, float* __restrict__ logits) {
+                int add_bias, float* __restrict__ rep, float* __restrict__ logits, float* __restrict__ finals) {
   pdl_wait();
   pdl_launch_dependents();
   __shared__ float red[32][4];
@@ -209,6 +209,7 @@ __global__ void __launch_bounds__(1024)
           } else {
             v = vals[i][0];
           }
+          if (finals) finals[((long long)(m0 + i) * gridDim.x + b) * hidden + j] = v;
           r += al[i] * v;
         }
       }
@@ -298,11 +299,61 @@ void launch_reduce_ln(const float* part, int splits, long long part_split_stride
 void launch_head(const float* final_rep, long long final_gs, long long split_stride, int splits,
                  const float* b_pool, int groups, const float* alpha, const float* w_cls, const float* b_cls,
                  int n_classes, int hidden, int n_rows, int add_bias, float* rep, float* logits,
-                 cudaStream_t stream) {
+                 cudaStream_t stream, float* finals) {
   if (n_rows <= 0) return;
   const int threads = ((hidden + 31) / 32) * 32;
   launch_pdl(head_kernel, dim3(n_rows), dim3(threads), 0, stream, final_rep, final_gs, split_stride, splits, b_pool,
-             groups, alpha, w_cls, b_cls, n_classes, hidden, add_bias, rep, logits);
+             groups, alpha, w_cls, b_cls, n_classes, hidden, add_bias, rep, logits, finals);
+}
+
+// Logits of every prefix k = 1..groups from the students' final representations — the forward half
+// of accumulate_prefix_gradients (distill.py:483-494): rep_k = rep_{k-1} + alpha[k-1] * finals[k-1]
+// accumulated left to right (:490, as EnsembleState.rep :177), z_k = W_c rep_k (+ b_c).
+// One CTA per row; finals [groups][n_rows][hidden], out [groups][n_rows][n_classes].
+__global__ void __launch_bounds__(1024)
+    prefix_logits_kernel(const float* __restrict__ finals, int groups, const float* __restrict__ alpha,
+                         const float* __restrict__ w_cls, const float* __restrict__ b_cls, int n_classes,
+                         int hidden, int add_bias, float* __restrict__ out) {
+  pdl_wait();
+  pdl_launch_dependents();
+  __shared__ float red[32][4];
+  const int b = blockIdx.x;
+  const int j = threadIdx.x;
+  const int n_rows = gridDim.x;
+  const int warps = (blockDim.x + 31) >> 5;
+  float r = 0.f;
+  for (int m = 0; m < groups; ++m) {
+    if (j < hidden) r += __ldg(alpha + m) * finals[((long long)m * n_rows + b) * hidden + j];
+    for (int c0 = 0; c0 < n_classes; c0 += 4) {
+      float acc[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        acc[c] = (j < hidden && c0 + c < n_classes) ? __ldg(w_cls + (long long)(c0 + c) * hidden + j) * r : 0.f;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc[c] = warp_sum(acc[c]);
+      if (lane_id() == 0)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) red[warp_id()][c] = acc[c];
+      __syncthreads();
+      if (threadIdx.x < 4 && c0 + threadIdx.x < n_classes) {
+        const int c = threadIdx.x;
+        float z = 0.f;
+        for (int w = 0; w < warps; ++w) z += red[w][c];
+        if (add_bias) z += b_cls[c0 + c];
+        out[((long long)m * n_rows + b) * n_classes + c0 + c] = z;
+      }
+      __syncthreads();
+    }
+  }
+}
+
+void launch_prefix_logits(const float* finals, int groups, const float* alpha, const float* w_cls,
+                          const float* b_cls, int n_classes, int hidden, int n_rows, int add_bias, float* out,
+                          cudaStream_t stream) {
+  if (n_rows <= 0 || groups <= 0) return;
+  const int threads = ((hidden + 31) / 32) * 32;
+  launch_pdl(prefix_logits_kernel, dim3(n_rows), dim3(threads), 0, stream, finals, groups, alpha, w_cls, b_cls,
+             n_classes, hidden, add_bias, out);
 }
 
 }  // namespace sp

@@ -117,6 +117,10 @@ struct sp_group {
   cudaStream_t cap_stream = nullptr;
   int graph_launches = 0;  // kernels per graph replay
   double sum_len_sq = 0.0;  // sum_b L_b^2 of the current request (attention flops)
+  // training-side evaluation outputs of the current sp_group_forward*_eval call (else null)
+  float* eval_finals = nullptr;  // [k][rows][H]
+  float* eval_prefix = nullptr;  // [k][rows][C]
+  float* eval_scratch = nullptr;  // finals when the caller only asks for prefix logits
   // per-launch profiling (CUDA events around every kernel of the last forward)
   bool profiling = false;
   struct Rec {
@@ -580,9 +584,14 @@ int bert_forward(sp_group* g, const int32_t* ids, const int32_t* cu, int n_seqs,
                                    (double)c.n_classes * H * 4.0 + n_seqs * H * 4.0, 0.0);
   sp::launch_head(g->final32, (long long)g->rows_cap * H, (long long)S * g->rows_cap * H,
                   pool_splits > 1 ? pool_splits : 0, w.b_pool, k, w.alpha, w.w_cls, w.b_cls, c.n_classes, H, n_seqs,
-                  add_bias, rep, logits, st);
+                  add_bias, rep, logits, st, g->eval_finals);
   g->rec_end();
   ++launches;
+  if (g->eval_prefix) {
+    sp::launch_prefix_logits(g->eval_finals, k, w.alpha, w.w_cls, w.b_cls, c.n_classes, H, n_seqs, add_bias,
+                             g->eval_prefix, st);
+    ++launches;
+  }
   g->last_launches = launches;
   return SP_OK;
 }
@@ -649,9 +658,14 @@ int dense_forward(sp_group* g, const half* x, int n_rows, int k, float* rep, flo
   }
   g->rec_begin(SP_LAUNCH_HEAD, (double)k * n_rows * H * 4.0 + (double)c.n_classes * H * 4.0, 0.0);
   sp::launch_head(g->final32, fgs, 0, 0, nullptr, k, w.alpha, w.w_cls, w.b_cls, c.n_classes, H, n_rows, add_bias, rep,
-                  logits, st);
+                  logits, st, g->eval_finals);
   g->rec_end();
   ++launches;
+  if (g->eval_prefix) {
+    sp::launch_prefix_logits(g->eval_finals, k, w.alpha, w.w_cls, w.b_cls, c.n_classes, H, n_rows, add_bias,
+                             g->eval_prefix, st);
+    ++launches;
+  }
   g->last_launches = launches;
   (void)x;
   return SP_OK;
@@ -708,6 +722,49 @@ int sp_group_forward_dense(sp_group* g, const void* x, int32_t n_rows, int32_t k
   if (rc) return rc;
   SP_CUDA(cudaGetLastError());
   return SP_OK;
+}
+
+// Training-side evaluation: route the per-student finals / prefix logits of one forward call.
+static int eval_begin(sp_group* g, float* finals_out, float* prefix_out) {
+  if (!finals_out && !prefix_out) return fail(SP_EINVAL, "finals_out and prefix_logits_out are both null");
+  if (!finals_out && g->eval_scratch == nullptr) {
+    int rc = dev_alloc(g, &g->eval_scratch, (size_t)g->cfg.n_students * g->rows_cap * g->cfg.hidden);
+    if (rc) return rc;
+  }
+  g->eval_finals = finals_out ? finals_out : g->eval_scratch;
+  g->eval_prefix = prefix_out;
+  return SP_OK;
+}
+static void eval_end(sp_group* g) {
+  g->eval_finals = nullptr;
+  g->eval_prefix = nullptr;
+}
+
+int sp_group_forward_eval(sp_group* g, const int32_t* ids, const int32_t* cu_seqlens, int32_t n_seqs,
+                          int32_t n_tokens, int32_t max_seq_len, int32_t k_active, float* finals_out,
+                          float* prefix_logits_out, void* stream) {
+  if (g == nullptr) return fail(SP_EINVAL, "null group");
+  if (k_active < 1 || k_active > g->cfg.n_students)
+    return fail(SP_EINVAL, "k=%d out of range 1..%d", k_active, g->cfg.n_students);
+  cudaSetDevice(g->device);
+  int rc = eval_begin(g, finals_out, prefix_logits_out);
+  if (rc) return rc;
+  rc = sp_group_forward(g, ids, cu_seqlens, n_seqs, n_tokens, max_seq_len, k_active, nullptr, g->d_logits, 1, stream);
+  eval_end(g);
+  return rc;
+}
+
+int sp_group_forward_dense_eval(sp_group* g, const void* x, int32_t n_rows, int32_t k_active, float* finals_out,
+                                float* prefix_logits_out, void* stream) {
+  if (g == nullptr) return fail(SP_EINVAL, "null group");
+  if (k_active < 1 || k_active > g->cfg.n_students)
+    return fail(SP_EINVAL, "k=%d out of range 1..%d", k_active, g->cfg.n_students);
+  cudaSetDevice(g->device);
+  int rc = eval_begin(g, finals_out, prefix_logits_out);
+  if (rc) return rc;
+  rc = sp_group_forward_dense(g, x, n_rows, k_active, nullptr, g->d_logits, 1, stream);
+  eval_end(g);
+  return rc;
 }
 
 int sp_group_forward_host(sp_group* g, const int32_t* ids, const int32_t* cu, int32_t n_seqs, int32_t n_tokens,

@@ -216,7 +216,7 @@ class StudentGroup:
                                                     _stream_handle(stream, self.device)))
 
     # ------------------------------------------------------------------ reference-facing API
-    def _run(self, x, k, add_bias=True, want_rep=True, k_local=None):
+    def _run(self, x, k, add_bias=True, want_rep=True, k_local=None, evaluate=False):
         dev = self.device
         if self.kind == "dense":
             w: DenseGroupWeights = self.weights
@@ -235,6 +235,12 @@ class StudentGroup:
             with torch.cuda.device(dev):
                 x16 = _dev_tensor(xp, dev)
                 rep = torch.empty((n, self.hidden), dtype=torch.float32, device=dev) if want_rep else None
+                if evaluate:
+                    finals, prefix = self._eval_buffers(kl, n)
+                    _lib.check(self._lib.sp_group_forward_dense_eval(self._handle, x16.data_ptr(), n, kl,
+                                                                     finals.data_ptr(), prefix.data_ptr(),
+                                                                     _stream_handle(None, dev)))
+                    return finals[:, :, : w.rep_dim], prefix, squeeze, w.rep_dim
                 logits = torch.empty((n, self.n_classes), dtype=torch.float32, device=dev)
                 self.forward_dense_device(x16, n, kl, rep, logits, add_bias)
             width = w.rep_dim
@@ -250,10 +256,34 @@ class StudentGroup:
                 ids_d = _dev_tensor(ids, dev)
                 cu_d = _dev_tensor(cu, dev)
                 rep = torch.empty((n, self.hidden), dtype=torch.float32, device=dev) if want_rep else None
+                if evaluate:
+                    finals, prefix = self._eval_buffers(kl, n)
+                    _lib.check(self._lib.sp_group_forward_eval(self._handle, ids_d.data_ptr(), cu_d.data_ptr(), n,
+                                                               len(ids), max_len, kl, finals.data_ptr(),
+                                                               prefix.data_ptr(), _stream_handle(None, dev)))
+                    return finals, prefix, squeeze, self.hidden
                 logits = torch.empty((n, self.n_classes), dtype=torch.float32, device=dev)
                 self.forward_packed_device(ids_d, cu_d, n, len(ids), max_len, kl, rep, logits, add_bias)
             width = self.hidden
         return rep, logits, squeeze, width
+
+    def _eval_buffers(self, kl: int, n: int):
+        if not np.array_equal(self.global_index, np.arange(self.n_students)):
+            raise ValueError("training-side evaluation needs the whole group on one device (not a shard)")
+        finals = torch.empty((kl, n, self.hidden), dtype=torch.float32, device=self.device)
+        prefix = torch.empty((kl, n, self.n_classes), dtype=torch.float32, device=self.device)
+        return finals, prefix
+
+    def finals_and_prefix_logits(self, x, k: int | None = None) -> tuple[np.ndarray, np.ndarray]:
+        """One GPU forward for training-side evaluation — the forward half of
+        accumulate_prefix_gradients (distill.py:483-494): every student's final representation
+        ``finals[m]`` = S_m(x) ([k, n, width], distill.py:483-486) and the logits of every prefix
+        ``prefix[j-1]`` = classifier(sum_{m<j} alpha_m S_m(x)) ([k, n, C], :489-492), float64 copies.
+        A 1-D (single-sample) input drops the sample axis, as rep() does (nnkernel.py:67-70)."""
+        finals, prefix, squeeze, _ = self._run(x, k, evaluate=True)
+        f = finals.double().cpu().numpy()
+        z = prefix.double().cpu().numpy()
+        return (f[:, 0], z[:, 0]) if squeeze else (f, z)
 
     def rep(self, x, k: int | None = None) -> np.ndarray:
         """Prefix-ensemble representation of the first k students (distill.py:169-178), float64."""

@@ -13,6 +13,10 @@ Outputs (small, committed; they travel to the GPU box where the reference does n
                           (ensemble-checkpoint-v1, binary mode, bit exact)
   ensemble_trained_task.npz  its validation/test inputs + labels and the reference's
                           prefix_accuracy for every k (real-data argmax parity)
+  training_eval_ref.npz   training-side evaluation of that checkpoint by the reference: a trained
+                          teacher's reps/logits/head on the validation split, residual_mse for every
+                          k (distill.py:297-302), the accumulate_prefix_gradients total (:471-494)
+                          and ensemble_accuracy_via_teacher_head (:676-683)
   servesim_ref.npz        generate_workload / allocate_students / nearest_rank_percentile /
                           decide_controller_action reference outputs (serving-side restatements)
 """
@@ -99,6 +103,23 @@ def trained_case():
                         acc_val=np.asarray(acc_val), acc_test=np.asarray(acc_test), best_k=best_k, **logits)
 
 
+def training_eval_case():
+    splits = dst.make_gaussian_task(n_classes=2, d_in=8, n_train=160, n_val=96, n_test=96, class_sep=2.5, seed=3)
+    teacher = nn.TeacherModel.build(8, 16, 24, 3, 2, make_rng(3))
+    dst.train_teacher(teacher, splits, epochs=40, learning_rate=3e-3, seed=3)
+    state = dst.load_ensemble(OUT / "ensemble_trained.json")
+    val = splits.validation
+    t_rep, t_logits = teacher.forward(val.inputs)
+    out = {"x_val": val.inputs, "y_val": val.labels, "teacher_rep": t_rep, "teacher_logits": t_logits,
+           "head_w": teacher.head.weight, "head_b": teacher.head.bias}
+    out["residual_mse"] = np.asarray([dst.residual_mse(teacher, state, val, k) for k in range(1, len(state) + 1)])
+    for temp in (1.0, 2.0):
+        _, total = dst.accumulate_prefix_gradients(state, val.inputs, t_logits, temp)
+        out[f"prefix_total_T{temp:g}"] = np.asarray(total)
+    out["acc_teacher_head"] = np.asarray(dst.ensemble_accuracy_via_teacher_head(teacher, state, val))
+    np.savez_compressed(OUT / "training_eval_ref.npz", **out)
+
+
 def servesim_case():
     out = {}
     reqs = ss.generate_workload(ss.PoissonSpec(rps=2000.0, duration_ms=50.0), seed=7)
@@ -142,8 +163,11 @@ def main():
                engine_precision=True)
     dense_case("wide", d_in=64, rep_dim=256, depth=2, k_students=3, n_classes=2, n_rows=32, seed=3,
                engine_precision=True)
-    trained_case()
-    servesim_case()
+    if "--training-eval-only" not in sys.argv:
+        trained_case()
+    training_eval_case()
+    if "--training-eval-only" not in sys.argv:
+        servesim_case()
     meta = {"generator": "tests/golden/make_golden.py", "reference": "/root/reference/pkg/src/studentpar",
             "numpy": np.__version__}
     (OUT / "golden_meta.json").write_text(json.dumps(meta, indent=1) + "\n")
