@@ -174,6 +174,10 @@ int sp_group_set_profiling(sp_group* group, int enable);
  * launches recorded (or a negative sp_status). */
 int sp_group_profile_read(sp_group* group, sp_launch_record* out, int max_records);
 
+/* Debug: when buf (device, >= 64 x n_SMs uint64) is non-null, the whole-request persistent kernel
+ * records globaltimer stamps per CTA (entry, end of every stage, weight-producer phase ends). */
+int sp_debug_set_request_trace(void* buf);
+
 /* Op-level entry points (single kernels, used by the per-kernel parity tests). */
 int sp_op_gemm(const void* w, const void* x, int32_t groups, int32_t n_out, int32_t k_dim, int32_t t_rows,
                int32_t x_group_rows, int32_t x_rows_total, const float* bias, int32_t act, void* out,

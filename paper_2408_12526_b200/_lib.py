@@ -71,6 +71,7 @@ SIGNATURES: dict[str, tuple] = {
     "sp_group_forward_dense": (
         C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p]
     ),
+    "sp_debug_set_request_trace": (C.c_int, [C.c_void_p]),
     "sp_group_forward_eval": (
         C.c_int,
         [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,

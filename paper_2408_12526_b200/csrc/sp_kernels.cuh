@@ -142,4 +142,54 @@ void launch_prefix_logits(const float* finals, int groups, const float* alpha, c
                           const float* b_cls, int n_classes, int hidden, int n_rows, int add_bias, float* out,
                           cudaStream_t stream);
 
+
+// ---------------------------------------------------------------------------------------------
+// Whole-request persistent kernel (sp_request.cu): every stage of a short request (<= 128 tokens)
+// in one launch, one CTA per SM. See the file header for the design.
+constexpr int kReqMaxLayers = 4;
+constexpr int kReqMaxTokens = 128;
+constexpr int kReqMaxPhases = 4 * kReqMaxLayers + 1;
+constexpr int kReqMaxTiles = 1024;   // students x feature tiles of one projection
+constexpr int kReqMaxStudents = 32;
+constexpr int kReqMaxSplit = 4;      // split-K chunks per tile (partials reduced by the consumer)
+// dataflow counter bank (ints); two banks alternate between consecutive requests
+constexpr int kReqOffDone = 64;                                               // [phase][student]
+constexpr int kReqOffRows = kReqOffDone + kReqMaxPhases * kReqMaxStudents;    // [row stage][student]
+constexpr int kReqOffAtt = kReqOffRows + (2 * kReqMaxLayers + 1) * kReqMaxStudents;  // [layer][student]
+constexpr int kReqOffPoolTotal = kReqOffAtt + kReqMaxLayers * kReqMaxStudents;
+constexpr int kReqBankInts = kReqOffPoolTotal + 64;
+
+struct ReqMaps {
+  CUtensorMap w[kReqMaxLayers][4];  // per layer: QKV, O, FFN1, FFN2 weights (box {64, 128})
+  CUtensorMap w_pool;
+  CUtensorMap x16_64, x16_16;  // LN outputs (QKV / FFN1 operand)
+  CUtensorMap ctx_64, ctx_16;  // attention output (O operand)
+  CUtensorMap ffn_64, ffn_16;  // GELU output (FFN2 operand)
+  CUtensorMap cls_64, cls_16;  // CLS rows (pooler operand)
+};
+
+struct ReqParams {
+  const int* ids;
+  const int* cu;
+  int n_seqs, k, s_total, hidden, ffn, n_heads, n_layers, t_cap, b_cap, rows_cap, n_classes, add_bias;
+  int ring_bytes;
+  long long part_ss, pool_ss;  // split strides of the O/FFN2 partials (pre) and pooler partials
+  float eps, scale_log2;
+  const half *word, *pos, *type;
+  long long word_gs, pos_gs;
+  const float *emb_g, *emb_b, *b_qkv, *b_o, *ln1_g, *ln1_b, *b_f1, *b_f2, *ln2_g, *ln2_b, *b_pool;
+  const float *alpha, *w_cls, *b_cls;
+  float* x32;
+  half *x16, *qkv, *ctx, *ffn_act, *cls16;
+  float *pre, *pool_part, *logits, *rep;
+  int* banks;
+  int* epoch;
+  unsigned long long* trace;  // optional per-CTA timeline (64 stamps per CTA), else null
+};
+
+// Dynamic shared memory of the per-request kernel for head_dim d (ring + attention K/V + barriers).
+int request_smem_bytes(int head_dim, int* ring_bytes);
+// Returns false if (hidden, head_dim) has no instantiation.
+bool launch_request(const ReqMaps& m, const ReqParams& p, int grid, cudaStream_t stream);
+
 }  // namespace sp

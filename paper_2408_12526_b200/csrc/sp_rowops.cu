@@ -4,70 +4,11 @@
 // is PDL-launched: griddepcontrol.wait first, then it lets the next projection start prefetching.
 #include "sp_kernels.cuh"
 #include "sp_ptx.cuh"
+#include "sp_device.cuh"
 
 namespace sp {
 
 static constexpr int kMaxSplitsRow = 4;
-
-// Largest b with cu[b] <= t (cu is nondecreasing, cu[0] = 0).
-__device__ __forceinline__ int seq_of(const int* cu, int n_seqs, int t) {
-  int lo = 0, hi = n_seqs - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (__ldg(cu + mid) <= t) lo = mid;
-    else hi = mid - 1;
-  }
-  return lo;
-}
-
-// Each lane owns NC chunks of 4 consecutive features: feature = c*128 + lane*4 + j.
-template <int NC>
-__device__ __forceinline__ void layer_norm_store(float (&v)[NC][4], const float* gamma, const float* beta, float eps,
-                                                 int hidden, float* x32, half* x16, half* cls16) {
-  const int lane = lane_id();
-  float4 gm[NC], bt[NC];
-#pragma unroll
-  for (int c = 0; c < NC; ++c) {
-    gm[c] = __ldg(reinterpret_cast<const float4*>(gamma + c * 128 + lane * 4));
-    bt[c] = __ldg(reinterpret_cast<const float4*>(beta + c * 128 + lane * 4));
-  }
-  float s = 0.f;
-#pragma unroll
-  for (int c = 0; c < NC; ++c) s += (v[c][0] + v[c][1]) + (v[c][2] + v[c][3]);
-  const float mean = warp_sum(s) / hidden;
-  float q = 0.f;
-#pragma unroll
-  for (int c = 0; c < NC; ++c)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const float d = v[c][j] - mean;
-      q += d * d;
-    }
-  const float rstd = rsqrtf(warp_sum(q) / hidden + eps);
-#pragma unroll
-  for (int c = 0; c < NC; ++c) {
-    const int f = c * 128 + lane * 4;
-    float4 y;
-    y.x = (v[c][0] - mean) * rstd * gm[c].x + bt[c].x;
-    y.y = (v[c][1] - mean) * rstd * gm[c].y + bt[c].y;
-    y.z = (v[c][2] - mean) * rstd * gm[c].z + bt[c].z;
-    y.w = (v[c][3] - mean) * rstd * gm[c].w + bt[c].w;
-    *reinterpret_cast<float4*>(x32 + f) = y;
-    __half2 h01 = __floats2half2_rn(y.x, y.y), h23 = __floats2half2_rn(y.z, y.w);
-    uint2 packed = make_uint2(*reinterpret_cast<uint32_t*>(&h01), *reinterpret_cast<uint32_t*>(&h23));
-    *reinterpret_cast<uint2*>(x16 + f) = packed;
-    if (cls16) *reinterpret_cast<uint2*>(cls16 + f) = packed;
-  }
-}
-
-__device__ __forceinline__ void h4_to_f4(const uint2 u, float (&o)[4]) {
-  const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&u.x));
-  const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&u.y));
-  o[0] = a.x;
-  o[1] = a.y;
-  o[2] = b.x;
-  o[3] = b.y;
-}
 
 template <int NC>
 __global__ void __launch_bounds__(128)

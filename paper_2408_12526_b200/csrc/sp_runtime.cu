@@ -84,6 +84,7 @@ int choose_splits(int units, int nkb, int smax) {
 }
 
 constexpr int kMaxSplits = 4;
+static_assert(sp::kReqMaxSplit <= kMaxSplits, "request-kernel partials live in the split-K buffers");
 
 }  // namespace
 
@@ -121,6 +122,11 @@ struct sp_group {
   float* eval_finals = nullptr;  // [k][rows][H]
   float* eval_prefix = nullptr;  // [k][rows][C]
   float* eval_scratch = nullptr;  // finals when the caller only asks for prefix logits
+  // whole-request persistent kernel (sp_request.cu), allocated on first use
+  bool req_ready = false;
+  int* req_banks = nullptr;    // [2][kReqBankInts] dataflow counters
+  int* req_epoch = nullptr;
+  sp::ReqMaps req_maps;
   // per-launch profiling (CUDA events around every kernel of the last forward)
   bool profiling = false;
   struct Rec {
@@ -486,6 +492,124 @@ bool use_ln_fused(int m_tiles, int n_tiles, int groups, int k_dim, int hidden) {
   return m_tiles * n_tiles * groups >= min_ctas_long_k;
 }
 
+unsigned long long* g_req_trace = nullptr;  // sp_debug_set_request_trace
+
+bool fused_enabled() {  // measured slower than the PDL-chained kernels: opt-in
+  static const bool on = [] {
+    const char* v = getenv("SP_FUSED");
+    return v != nullptr && atoi(v) != 0;
+  }();
+  return on;
+}
+
+// Can this request run as ONE persistent kernel (sp_request.cu)? Short requests only: the
+// activations of all tokens must fit one TMEM accumulator column block (<= 128 tokens).
+bool fused_ok(const sp_group* g, int n_seqs, int n_tokens_bound, int k) {
+  const sp_config& c = g->cfg;
+  if (!fused_enabled() || c.kind != SP_KIND_BERT || g->profiling || g->eval_finals || g->eval_prefix) return false;
+  if (k < 1 || k > sp::kReqMaxStudents || c.n_layers > sp::kReqMaxLayers) return false;
+  if (n_tokens_bound > sp::kReqMaxTokens || n_seqs > n_tokens_bound) return false;
+  const int H = c.hidden, F = c.ffn;
+  if (F % 128 || k * std::max(3 * H, F) / 128 > sp::kReqMaxTiles) return false;
+  const int nc = H / 128, d = H / c.n_heads;
+  return (nc == 6 && d == 64) || (nc == 8 && d == 64) || (nc == 1 && d == 32) || (nc == 2 && d == 64);
+}
+
+int fused_prepare(sp_group* g) {
+  if (g->req_ready) return SP_OK;
+  const sp_config& c = g->cfg;
+  const int G = sp::sm_count();
+  (void)G;
+  int rc;
+  if ((rc = dev_alloc(g, &g->req_banks, 2 * (size_t)sp::kReqBankInts))) return rc;
+  if ((rc = dev_alloc(g, &g->req_epoch, 1))) return rc;
+  SP_CUDA(cudaMemset(g->req_banks, 0, 2 * sizeof(int) * sp::kReqBankInts));
+  SP_CUDA(cudaMemset(g->req_epoch, 0, sizeof(int)));
+  sp::ReqMaps& m = g->req_maps;
+  memset(&m, 0, sizeof(m));
+  for (int l = 0; l < c.n_layers; ++l) {
+    m.w[l][0] = g->m_qkv[l];
+    m.w[l][1] = g->m_o[l];
+    m.w[l][2] = g->m_f1[l];
+    m.w[l][3] = g->m_f2[l];
+  }
+  m.w_pool = g->m_pool;
+  m.x16_64 = g->xm_x16.x64;
+  m.x16_16 = g->xm_x16.x16;
+  m.ctx_64 = g->xm_ctx.x64;
+  m.ctx_16 = g->xm_ctx.x16;
+  m.ffn_64 = g->xm_ffn.x64;
+  m.ffn_16 = g->xm_ffn.x16;
+  m.cls_64 = g->xm_cls.x64;
+  m.cls_16 = g->xm_cls.x16;
+  g->req_ready = true;
+  return SP_OK;
+}
+
+int fused_forward(sp_group* g, const int32_t* ids, const int32_t* cu, int n_seqs, int k, float* rep, float* logits,
+                  int add_bias, cudaStream_t st) {
+  int rc = fused_prepare(g);
+  if (rc) return rc;
+  const sp_config& c = g->cfg;
+  const sp_weights& w = g->w;
+  sp::ReqParams p;
+  memset(&p, 0, sizeof(p));
+  p.ids = ids;
+  p.cu = cu;
+  p.n_seqs = n_seqs;
+  p.k = k;
+  p.s_total = c.n_students;
+  p.hidden = c.hidden;
+  p.ffn = c.ffn;
+  p.n_heads = c.n_heads;
+  p.n_layers = c.n_layers;
+  p.t_cap = c.max_tokens;
+  p.b_cap = c.max_seqs;
+  p.rows_cap = g->rows_cap;
+  p.n_classes = c.n_classes;
+  p.add_bias = add_bias;
+  p.part_ss = (long long)c.n_students * c.max_tokens * c.hidden;  // g->part: [split][S][T][H]
+  p.pool_ss = (long long)c.n_students * g->rows_cap * c.hidden;   // g->final32: [split][S][R][H]
+  p.eps = c.ln_eps;
+  p.scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(c.hidden / c.n_heads));
+  p.word = static_cast<const half*>(w.word_emb);
+  p.pos = static_cast<const half*>(w.pos_emb);
+  p.type = static_cast<const half*>(w.type_emb);
+  p.word_gs = (long long)c.vocab * c.hidden;
+  p.pos_gs = (long long)c.max_pos * c.hidden;
+  p.emb_g = w.emb_ln_gamma;
+  p.emb_b = w.emb_ln_beta;
+  p.b_qkv = w.b_qkv;
+  p.b_o = w.b_o;
+  p.ln1_g = w.ln1_gamma;
+  p.ln1_b = w.ln1_beta;
+  p.b_f1 = w.b_ffn1;
+  p.b_f2 = w.b_ffn2;
+  p.ln2_g = w.ln2_gamma;
+  p.ln2_b = w.ln2_beta;
+  p.b_pool = w.b_pool;
+  p.alpha = w.alpha;
+  p.w_cls = w.w_cls;
+  p.b_cls = w.b_cls;
+  p.x32 = g->x32;
+  p.x16 = g->x16;
+  p.qkv = g->qkv;
+  p.ctx = g->ctx;
+  p.ffn_act = g->ffn;
+  p.pre = g->part;
+  p.cls16 = g->cls16;
+  p.pool_part = g->final32;
+  p.logits = logits;
+  p.rep = rep;
+  p.banks = g->req_banks;
+  p.epoch = g->req_epoch;
+  p.trace = g_req_trace;
+  if (!sp::launch_request(g->req_maps, p, sp::sm_count(), st))
+    return fail(SP_ECUDA, "request kernel launch: %s", cudaGetErrorString(cudaGetLastError()));
+  g->last_launches = 1;
+  return SP_OK;
+}
+
 // dyn = true (graph capture): n_tokens / max_len are bucket bounds used for grids and tiles; every
 // kernel reads the live token count from cu_seqlens[n_seqs] on the device.
 int bert_forward(sp_group* g, const int32_t* ids, const int32_t* cu, int n_seqs, int n_tokens, int max_len, int k,
@@ -511,6 +635,10 @@ int bert_forward(sp_group* g, const int32_t* ids, const int32_t* cu, int n_seqs,
     unsigned long long n;
   };
   auto pf = [&](const void* p, size_t elems) { return pf_on ? Pf{p, (unsigned long long)elems * 2} : Pf{nullptr, 0}; };
+  if (k > 0 && fused_ok(g, n_seqs, n_tokens, k)) {  // short request: one persistent kernel
+    g->rec_reset(st);
+    return fused_forward(g, ids, cu, n_seqs, k, rep, logits, add_bias, st);
+  }
   g->rec_reset(st);
   const double GTH = (double)k * n_tokens * H;
   if (k > 0) {
@@ -790,7 +918,8 @@ int sp_group_forward_host(sp_group* g, const int32_t* ids, const int32_t* cu, in
     if (ids[t] < 0 || ids[t] >= c.vocab) return fail(SP_EINVAL, "token id %d at %d outside vocab", ids[t], t);
   cudaSetDevice(g->device);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const bool use_graph = graphs_enabled() && n_seqs == 1 && !g->profiling;
+  // short requests run as one persistent kernel (no graph needed); longer ones replay a graph
+  const bool use_graph = graphs_enabled() && n_seqs == 1 && !g->profiling && !fused_ok(g, n_seqs, n_tokens, k_active);
   cudaGraphExec_t exec = nullptr;
   if (use_graph) {
     int rc = get_graph(g, n_tokens, k_active, add_bias, &exec);
@@ -861,6 +990,11 @@ int sp_op_attention(const void* qkv, void* ctx, const int32_t* cu_seqlens, int32
 
 }  // extern "C"
 
+extern "C" int sp_debug_set_request_trace(void* buf) {
+  g_req_trace = static_cast<unsigned long long*>(buf);
+  return SP_OK;
+}
+
 extern "C" int sp_group_prepare_graphs(sp_group* g, int32_t max_tokens, int32_t k_active, int32_t add_bias) {
   if (g == nullptr) return fail(SP_EINVAL, "null group");
   if (g->cfg.kind != SP_KIND_BERT) return fail(SP_EINVAL, "graphs serve BERT-kind groups");
@@ -869,6 +1003,11 @@ extern "C" int sp_group_prepare_graphs(sp_group* g, int32_t max_tokens, int32_t 
   cudaSetDevice(g->device);
   const int top = std::min(max_tokens, g->cfg.max_tokens);
   for (int t = 16; t - 15 <= top; t += 16) {
+    if (k_active > 0 && fused_ok(g, 1, t, k_active)) {  // served by the persistent kernel
+      int rc = fused_prepare(g);
+      if (rc) return rc;
+      continue;
+    }
     cudaGraphExec_t exec;
     int rc = get_graph(g, t, k_active, add_bias, &exec);
     if (rc) return rc;

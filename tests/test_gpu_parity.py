@@ -223,10 +223,10 @@ def test_host_graph_path_bit_identical_to_device_path():
             np.testing.assert_array_equal(z_host, z_dev)
 
 
-@pytest.mark.parametrize("env", ["SP_LN_FUSE=1", "SP_ATTN_TC=1", "SP_GEMM_CLUSTER=1", "SP_PERSIST_PAIR=1"])
+@pytest.mark.parametrize("env", ["SP_LN_FUSE=1", "SP_ATTN_TC=1", "SP_GEMM_CLUSTER=1", "SP_PERSIST_PAIR=1", "SP_FUSED=1"])
 def test_opt_in_kernel_variants_match_oracle(env):
     """The opt-in kernel variants (fused projection+LayerNorm, tcgen05 attention, cluster-multicast
-    GEMM, paired persistent GEMM) stay correct: run a fresh process with the knob set (knobs are read once per process)."""
+    GEMM, paired persistent GEMM, whole-request persistent kernel) stay correct: run a fresh process with the knob set (knobs are read once per process)."""
     import subprocess
     import sys
 
@@ -237,10 +237,11 @@ def test_opt_in_kernel_variants_match_oracle(env):
         "cfg, K = PRESETS['base']; w = random_bert_group(cfg, 3, seed=5)\n"
         "g = StudentGroup(w, max_tokens=1024, max_seqs=4); o = OracleBertGroup(w)\n"
         "rng = np.random.default_rng(0)\n"
-        "for L in (16, 200, 512):\n"
-        "    ids = np.r_[101, rng.integers(1000, 30522, size=L - 1)].astype(np.int32)\n"
-        "    z = g.logits([ids]); _, zr = o.forward([ids])\n"
-        "    err = float(np.abs(z - zr).max() / np.abs(zr).max()); assert err <= 1e-3, (L, err)\n"
+        "cases = [[L] for L in (1, 16, 77, 128, 200, 512)] + [[5, 40, 60]]\n"
+        "for lens in cases:\n"
+        "    seqs = [np.r_[101, rng.integers(1000, 30522, size=L - 1)].astype(np.int32) for L in lens]\n"
+        "    z = g.logits(seqs); _, zr = o.forward(seqs)\n"
+        "    err = float(np.abs(z - zr).max() / np.abs(zr).max()); assert err <= 1e-3, (lens, err)\n"
         "print('ok')\n")
     key, val = env.split("=")
     import os
