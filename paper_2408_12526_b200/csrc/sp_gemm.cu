@@ -22,6 +22,8 @@
 #include <type_traits>
 #include <vector>
 
+#include <algorithm>
+
 #include "sp_kernels.cuh"
 #include "sp_ptx.cuh"
 
@@ -260,7 +262,7 @@ static constexpr int kPersistTmemCols = 512;  // 2 accumulators x 256 columns
 static constexpr int kPEpiWarps = 16;          // 4 warps per TMEM lane quadrant, a quarter of the columns each
 static constexpr int kPThreads = 64 + 32 * kPEpiWarps;
 
-template <int ACT, bool OUT_F32>
+template <int ACT, bool OUT_F32, bool PAIR>
 __global__ void __launch_bounds__(kPThreads, 1)
     gemm_persistent_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_x64,
                            const __grid_constant__ CUtensorMap map_x16, const GemmParams p) {
@@ -270,7 +272,17 @@ __global__ void __launch_bounds__(kPThreads, 1)
   constexpr int kRowsPerPass = 32 / kLanesPerRow;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const int stage_bytes = kATileBytes + p.bn * 128;
+  // pair mode (cluster of 2, cta_group::2): the pair computes a 256-feature x bn-token tile with one
+  // MMA stream issued by the leader; each CTA stages its own 128 weight rows and HALF of the token
+  // tile, so per-CTA operand traffic per flop drops by a third (bn = 256) and the leader's TMEM-
+  // resident accumulator rows 0-127 / the peer's rows 128-255 are drained by each CTA's epilogue.
+  // (a kernel containing cta_group::2 instructions only launches in clusters: PAIR is a template
+  // parameter so the single-CTA instantiation has none)
+  constexpr bool pair = PAIR;
+  const uint32_t crank = pair ? cluster_ctarank() : 0u;
+  const bool leader = crank == 0;
+  const int x_rows = pair ? (p.bn >> 1) : p.bn;  // token rows staged by this CTA
+  const int stage_bytes = kATileBytes + x_rows * 128;
   uint8_t* staging = smem + p.stages * stage_bytes;  // 16 warps x 16 rows x kRowBytes
   uint64_t* full = reinterpret_cast<uint64_t*>(staging + kPEpiWarps * 16 * kRowBytes);
   uint64_t* empty = full + p.stages;
@@ -282,25 +294,23 @@ __global__ void __launch_bounds__(kPThreads, 1)
   const int lane = lane_id();
   unsigned long long* tr = p.trace ? p.trace + 8ull * blockIdx.x : nullptr;
   if (tr && threadIdx.x == 0) tr[0] = globaltimer();
-  // pair mode (cluster of 2): the CTAs of a pair take neighbouring feature tiles of the same token
-  // tile in lockstep and TMA-multicast half of the token tile each (a third less L2->SM traffic)
-  const bool pair = p.cluster == 2;
-  const uint32_t crank = pair ? cluster_ctarank() : 0u;
   const int m_per = pair ? (p.m_tiles >> 1) : p.m_tiles;
   const int units_per_group = m_per * p.n_tiles;
   const int units = units_per_group * p.groups;
   const int u_first = pair ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
   const int u_stride = pair ? (int)(gridDim.x >> 1) : (int)gridDim.x;
   const int nkb = p.k_dim / kBlockK;
+  // the leader's barrier collects both CTAs' bytes; the pair's epilogues both release its accumulator
+  const uint32_t full_bytes = pair ? 2u * (uint32_t)stage_bytes : (uint32_t)stage_bytes;
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < p.stages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], pair ? 2 : 1);
+      mbar_init(&empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&acc_full[b], 1);
-      mbar_init(&acc_empty[b], kPEpiWarps);
+      mbar_init(&acc_empty[b], pair ? 2 * kPEpiWarps : kPEpiWarps);
     }
     fence_barrier_init();
     tma_prefetch_desc(&map_w);
@@ -308,12 +318,17 @@ __global__ void __launch_bounds__(kPThreads, 1)
     tma_prefetch_desc(&map_x16);
   }
   if (warp == 1) {
-    tmem_alloc(tmem_slot, kPersistTmemCols);
-    tmem_relinquish();
+    if constexpr (PAIR) {
+      tmem_alloc_2sm(tmem_slot, kPersistTmemCols);
+      tmem_relinquish_2sm();
+    } else {
+      tmem_alloc(tmem_slot, kPersistTmemCols);
+      tmem_relinquish();
+    }
   }
   tc_fence_before();
   __syncthreads();
-  if (pair) cluster_sync();  // peer barriers initialised before any multicast
+  if constexpr (PAIR) cluster_sync();  // peer barriers initialised before any remote complete_tx / arrive
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   pdl_launch_dependents();
@@ -329,17 +344,19 @@ __global__ void __launch_bounds__(kPThreads, 1)
     if (elect_one()) {
       const uint64_t pol_w = policy_evict_last();  // re-read by the other token tiles
       const uint64_t pol_x = policy_evict_last();
-      const int r_begin = pair ? static_cast<int>(crank) * (p.bn >> 1) : 0;
-      const int r_end = pair ? r_begin + (p.bn >> 1) : p.bn;
+      auto load_w = [&](int s, int kb, int wrow) {
+        if constexpr (PAIR) tma_load_2d_2sm(&map_w, &full[s], smem + s * stage_bytes, kb * kBlockK, wrow, pol_w);
+        else tma_load_2d(&map_w, &full[s], smem + s * stage_bytes, kb * kBlockK, wrow, pol_w);
+      };
       auto load_x = [&](int s, int kb, int xrow) {
         uint8_t* sb = smem + s * stage_bytes + kATileBytes;
-        int r = r_begin;
-        if (pair) {
-          for (; r + 64 <= r_end; r += 64) tma_load_2d_mc(&map_x64, &full[s], sb + r * 128, kb * kBlockK, xrow + r, 0x3, pol_x);
-          for (; r < r_end; r += 16) tma_load_2d_mc(&map_x16, &full[s], sb + r * 128, kb * kBlockK, xrow + r, 0x3, pol_x);
+        int r = 0;
+        if constexpr (PAIR) {
+          for (; r + 64 <= x_rows; r += 64) tma_load_2d_2sm(&map_x64, &full[s], sb + r * 128, kb * kBlockK, xrow + r, pol_x);
+          for (; r < x_rows; r += 16) tma_load_2d_2sm(&map_x16, &full[s], sb + r * 128, kb * kBlockK, xrow + r, pol_x);
         } else {
-          for (; r + 64 <= r_end; r += 64) tma_load_2d(&map_x64, &full[s], sb + r * 128, kb * kBlockK, xrow + r, pol_x);
-          for (; r < r_end; r += 16) tma_load_2d(&map_x16, &full[s], sb + r * 128, kb * kBlockK, xrow + r, pol_x);
+          for (; r + 64 <= x_rows; r += 64) tma_load_2d(&map_x64, &full[s], sb + r * 128, kb * kBlockK, xrow + r, pol_x);
+          for (; r < x_rows; r += 16) tma_load_2d(&map_x16, &full[s], sb + r * 128, kb * kBlockK, xrow + r, pol_x);
         }
       };
       int s = 0;
@@ -349,13 +366,13 @@ __global__ void __launch_bounds__(kPThreads, 1)
         int g, mt, nt;
         decode(u, g, mt, nt);
         const int wrow = g * p.n_out + mt * kBlockM;
-        const int xrow = g * p.x_group_rows + nt * p.bn;
+        const int xrow = g * p.x_group_rows + nt * p.bn + (int)crank * x_rows;
         int kb = 0;
         if (first) {  // weight prefetch of the first stages before the dependency wait
           const int n_pre = min(p.stages, nkb);
           for (int i = 0; i < n_pre; ++i) {
-            mbar_arrive_expect_tx(&full[i], stage_bytes);
-            tma_load_2d(&map_w, &full[i], smem + i * stage_bytes, i * kBlockK, wrow, pol_w);
+            if (leader) mbar_arrive_expect_tx(&full[i], full_bytes);
+            load_w(i, i, wrow);
           }
           if (p.l2_prefetch)
             for (int i = n_pre; i < nkb; ++i) tma_prefetch_l2_2d(&map_w, i * kBlockK, wrow);
@@ -369,9 +386,8 @@ __global__ void __launch_bounds__(kPThreads, 1)
         }
         for (; kb < nkb; ++kb) {
           mbar_wait(&empty[s], ph ^ 1);
-          mbar_arrive_expect_tx(&full[s], stage_bytes);
-          uint8_t* sa = smem + s * stage_bytes;
-          tma_load_2d(&map_w, &full[s], sa, kb * kBlockK, wrow, pol_w);
+          if (leader) mbar_arrive_expect_tx(&full[s], full_bytes);
+          load_w(s, kb, wrow);
           load_x(s, kb, xrow);
           if (++s == p.stages) {
             s = 0;
@@ -382,36 +398,52 @@ __global__ void __launch_bounds__(kPThreads, 1)
       if (first) pdl_wait();  // no work: still honour the dependency
     }
   } else if (warp == 1) {
-    if (elect_one()) {
-      const uint32_t idesc = umma_idesc_f16(kBlockM, p.bn);
+    if (leader && elect_one()) {
+      const uint32_t idesc = umma_idesc_f16(pair ? 2 * kBlockM : kBlockM, p.bn);
       int s = 0;
       uint32_t ph = 0;
       int j = 0;
+      unsigned long long w_acc = 0, w_full = 0;  // trace: ns the MMA thread waited on each barrier kind
       for (int u = u_first; u < units; u += u_stride, ++j) {
         const int b = j & 1;
-        mbar_wait(&acc_empty[b], ((j >> 1) & 1) ^ 1);  // epilogue drained this accumulator
+        unsigned long long t0 = tr ? globaltimer() : 0ull;
+        mbar_wait(&acc_empty[b], ((j >> 1) & 1) ^ 1);  // epilogue(s) drained this accumulator
+        if (tr) w_acc += globaltimer() - t0;
         tc_fence_after();
         const uint32_t acc = tmem + static_cast<uint32_t>(b * 256);
         for (int kb = 0; kb < nkb; ++kb) {
+          if (tr) t0 = globaltimer();
           mbar_wait(&full[s], ph);
+          if (tr) w_full += globaltimer() - t0;
           tc_fence_after();
           if (tr && j == 0 && kb == 0) tr[4] = globaltimer();
           const uint32_t sa = smem_u32(smem + s * stage_bytes);
           const uint64_t adesc = umma_sdesc_sw128(sa);
           const uint64_t bdesc = umma_sdesc_sw128(sa + kATileBytes);
+          if constexpr (PAIR) {
 #pragma unroll
-          for (int k = 0; k < kBlockK / 16; ++k)
-            umma_f16_ss(acc, adesc + 2 * k, bdesc + 2 * k, idesc, (kb > 0 || k > 0) ? 1u : 0u);
-          if (pair) umma_commit_mc(&empty[s], 0x3);
-          else umma_commit(&empty[s]);
+            for (int k = 0; k < kBlockK / 16; ++k)
+              umma_f16_ss_2sm(acc, adesc + 2 * k, bdesc + 2 * k, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+            umma_commit_2sm_mc(&empty[s], 0x3);
+          } else {
+#pragma unroll
+            for (int k = 0; k < kBlockK / 16; ++k)
+              umma_f16_ss(acc, adesc + 2 * k, bdesc + 2 * k, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+            umma_commit(&empty[s]);
+          }
           if (++s == p.stages) {
             s = 0;
             ph ^= 1;
           }
         }
-        umma_commit(&acc_full[b]);
+        if constexpr (PAIR) umma_commit_2sm_mc(&acc_full[b], 0x3);
+        else umma_commit(&acc_full[b]);
       }
-      if (tr) tr[5] = globaltimer();
+      if (tr) {
+        tr[5] = globaltimer();
+        tr[1] = w_full;
+        tr[3] = w_acc;
+      }
     }
     __syncwarp();
   } else {
@@ -421,6 +453,9 @@ __global__ void __launch_bounds__(kPThreads, 1)
     const int c_begin = (e >> 2) * part_cols;
     OutT* stage = reinterpret_cast<OutT*>(staging + e * 16 * kRowBytes);
     const int t_rows = p.t_dev ? __ldg(p.t_dev) : p.t_rows;
+    // accumulator release: local barrier, or the leader's through the cluster window
+    uint32_t acc_empty_leader0 = 0u;
+    if constexpr (PAIR) acc_empty_leader0 = mapa_shared(smem_u32(&acc_empty[0]), 0);
     int j = 0;
     for (int u = u_first; u < units; u += u_stride, ++j) {
       int g, mt, nt;
@@ -443,7 +478,10 @@ __global__ void __launch_bounds__(kPThreads, 1)
         if (c + 16 >= c_begin + part_cols) {  // last TMEM read of this tile: hand the accumulator back
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&acc_empty[b]);
+          if (lane == 0) {
+            if constexpr (PAIR) mbar_arrive_cluster(acc_empty_leader0 + (uint32_t)(b * sizeof(uint64_t)));
+            else mbar_arrive(&acc_empty[b]);
+          }
         }
         float y[16];
 #pragma unroll
@@ -472,10 +510,11 @@ __global__ void __launch_bounds__(kPThreads, 1)
 
   tc_fence_before();
   __syncthreads();
-  if (pair) cluster_sync();  // no CTA leaves while its peer may still multicast or signal into it
+  if constexpr (PAIR) cluster_sync();  // no CTA leaves while its peer may still signal into it
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem, kPersistTmemCols);
+    if constexpr (PAIR) tmem_dealloc_2sm(tmem, kPersistTmemCols);
+    else tmem_dealloc(tmem, kPersistTmemCols);
   }
 }
 
@@ -486,22 +525,21 @@ static void launch_persistent_t(const GemmMaps& maps, const GemmParams& p, int g
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncSetAttribute(gemm_persistent_kernel<ACT, OUT_F32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(gemm_persistent_kernel<ACT, OUT_F32, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         227 * 1024);
+    cudaFuncSetAttribute(gemm_persistent_kernel<ACT, OUT_F32, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          227 * 1024);
   }
   GemmParams q = p;
   q.groups = groups;
-  static const bool pair_on = [] {
-    const char* v = getenv("SP_PERSIST_PAIR");
-    return v != nullptr && atoi(v) != 0;
-  }();
-  const int units = groups * p.m_tiles * p.n_tiles;
-  q.cluster = (pair_on && p.m_tiles % 2 == 0 && units >= 4) ? 2 : 1;
+  q.cluster = gemm_persistent_pair(p.t_rows, p.m_tiles, groups) ? 2 : 1;
+  const int units = groups * p.m_tiles * p.n_tiles;  // per-CTA tiles (a pair takes two at once)
   int grid = units < n_sm ? units : n_sm;
   if (q.cluster == 2) grid &= ~1;
   q.trace = trace_ptr_advance(grid);
   const int row_bytes = 32 * (OUT_F32 ? 4 : 2);
-  const size_t smem = static_cast<size_t>(p.stages) * (kATileBytes + p.bn * 128) + kPEpiWarps * 16 * row_bytes +
+  const int x_rows = q.cluster == 2 ? p.bn / 2 : p.bn;
+  const size_t smem = static_cast<size_t>(q.stages) * (kATileBytes + x_rows * 128) + kPEpiWarps * 16 * row_bytes +
                       1024 + 256;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
@@ -517,22 +555,47 @@ static void launch_persistent_t(const GemmMaps& maps, const GemmParams& p, int g
   attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-  cudaLaunchKernelEx(&cfg, gemm_persistent_kernel<ACT, OUT_F32>, maps.w, maps.x64, maps.x16, q);
+  if (q.cluster == 2) cudaLaunchKernelEx(&cfg, gemm_persistent_kernel<ACT, OUT_F32, true>, maps.w, maps.x64, maps.x16, q);
+  else cudaLaunchKernelEx(&cfg, gemm_persistent_kernel<ACT, OUT_F32, false>, maps.w, maps.x64, maps.x16, q);
+}
+
+// CTA pairs (cta_group::2) halve each CTA's token-tile traffic; SP_PERSIST_PAIR=0/1 forces them
+// off/on, default: from SP_PERSIST_PAIR_MIN_ROWS tokens (see DESIGN.md for the measured crossover).
+bool gemm_persistent_pair(int t_rows, int m_tiles, int groups) {
+  static const int pair_mode = [] {
+    const char* v = getenv("SP_PERSIST_PAIR");
+    return v == nullptr ? -1 : atoi(v);
+  }();
+  static const int min_rows = [] {
+    const char* v = getenv("SP_PERSIST_PAIR_MIN_ROWS");
+    return v ? atoi(v) : 1024;
+  }();
+  const bool on = pair_mode < 0 ? t_rows >= min_rows : pair_mode != 0;
+  return on && m_tiles % 2 == 0 && groups * m_tiles >= 4;
 }
 
 // Tile policy of the persistent path: pick the token-tile count that minimises the makespan
 // ceil(units / CTAs) x (fixed + bn) (bn <= 256), so projections with few feature tiles (O, FFN2:
 // 6 per student) still fill every SM; ring as deep as the smem left after staging.
-void gemm_configure_persistent(int t_rows, bool out_f32, int units_per_tile, int n_ctas, int* bn, int* n_tiles,
-                               int* stages) {
-  int best_tiles = (t_rows + 255) / 256, best_cost = 0x7fffffff;
+void gemm_configure_persistent(int t_rows, bool out_f32, int units_per_tile, int n_ctas, bool pair, int* bn,
+                               int* n_tiles, int* stages) {
+  // Cost of a tiling = rounds x per-unit time, in cycles per 64-wide k-block of one CTA:
+  //   MMA      2 * bn                          (128 x bn x 64 at 8192 flop/clk)
+  //   operands 3 * (128 + token rows staged)   (L2 -> SM at ~42 B/clk per SM, 12.4 TB/s / 148)
+  // plus ~200 cycles of per-unit fill / drain. Pairs stage half the token tile per CTA and run
+  // units_per_tile / 2 units on n_ctas / 2 pairs.
+  const int ctas = pair ? n_ctas / 2 : n_ctas;
+  const int upt = pair ? units_per_tile / 2 : units_per_tile;
+  int best_tiles = (t_rows + 255) / 256;
+  long long best_cost = 0x7fffffffffffll;
   for (int tiles = (t_rows + 255) / 256; tiles <= (t_rows + 63) / 64; ++tiles) {
     const int per = (t_rows + tiles - 1) / tiles;
     const int b = ((per + 31) / 32) * 32;  // 16 epilogue warps take a quarter each (multiples of 8)
     if (b > 256) continue;
-    const int units = units_per_tile * tiles;
-    const int rounds = (units + n_ctas - 1) / n_ctas;
-    const int cost = rounds * (64 + b);  // ~64 tokens' worth of per-tile fixed cost (fill, epilogue)
+    const int x = pair ? b / 2 : b;
+    const long long rounds = (upt * (long long)tiles + ctas - 1) / ctas;
+    const long long unit = std::max(2LL * b, 3LL * (128 + x)) + 200;
+    const long long cost = rounds * unit;
     if (cost < best_cost) {
       best_cost = cost;
       best_tiles = tiles;
@@ -544,7 +607,7 @@ void gemm_configure_persistent(int t_rows, bool out_f32, int units_per_tile, int
   *bn = b;
   *n_tiles = tiles;
   const int staging = kPEpiWarps * 16 * 32 * (out_f32 ? 4 : 2);
-  int st = (224 * 1024 - staging) / (kATileBytes + b * 128);
+  int st = (224 * 1024 - staging) / (kATileBytes + (pair ? b / 2 : b) * 128);
   if (st > 8) st = 8;
   if (st < 2) st = 2;
   *stages = st;

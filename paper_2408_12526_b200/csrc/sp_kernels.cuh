@@ -94,8 +94,9 @@ void launch_gemm_ln(const GemmMaps& maps, const GemmParams& p, const LnParams& l
 size_t gemm_ln_smem_bytes(int bn, int stages);
 // Persistent variant for large token counts (splits must be 1).
 void launch_gemm_persistent(const GemmMaps& maps, const GemmParams& p, int groups, cudaStream_t stream);
-void gemm_configure_persistent(int t_rows, bool out_f32, int units_per_tile, int n_ctas, int* bn, int* n_tiles,
-                               int* stages);
+bool gemm_persistent_pair(int t_rows, int m_tiles, int groups);
+void gemm_configure_persistent(int t_rows, bool out_f32, int units_per_tile, int n_ctas, bool pair, int* bn,
+                               int* n_tiles, int* stages);
 int sm_count();
 size_t gemm_smem_bytes(int bn, int stages);
 void gemm_configure_tiles(int t_rows, bool cluster2, int* bn, int* n_tiles, int* stages);

@@ -379,8 +379,8 @@ int run_gemm(sp_group* grp, int kind, const CUtensorMap& wmap, const XMaps& xm, 
     p.splits = 1;
     p.kb_per_split = k_dim / 64;
     p.cluster = 1;
-    sp::gemm_configure_persistent(t_rows, out_f32 != 0, groups * p.m_tiles, sp::sm_count(), &p.bn, &p.n_tiles,
-                                  &p.stages);
+    sp::gemm_configure_persistent(t_rows, out_f32 != 0, groups * p.m_tiles, sp::sm_count(),
+                                  sp::gemm_persistent_pair(t_rows, p.m_tiles, groups), &p.bn, &p.n_tiles, &p.stages);
     p.out = out;
     p.out_group_stride = out_gs;
     p.out_ld = n_out;

@@ -1,0 +1,34 @@
+"""Persistent GEMM at a batched shape: where does the MMA thread wait (operands vs accumulators)?"""
+import sys, os, ctypes, numpy as np, torch
+sys.path.insert(0, ".")
+from paper_2408_12526_b200 import _lib
+lib = _lib.load()
+G, T = 12, int(sys.argv[1]) if len(sys.argv) > 1 else 4224
+shapes = {"qkv": (3072, 1024, 0), "o": (1024, 1024, 0), "ffn1_gelu": (4096, 1024, 2), "ffn1_id": (4096, 1024, 0),
+          "ffn2": (1024, 4096, 0)}
+flush = torch.empty(256 << 18, device="cuda"); flush_r = torch.ones(256 << 18, device="cuda")
+for name, (N, K, act) in shapes.items():
+    w = (torch.randn(G, N, K, device="cuda") * 0.02).half()
+    x = torch.randn(G * T, K, device="cuda").half()
+    out = torch.empty(G, T, N, device="cuda", dtype=torch.float16)
+    bias = torch.zeros(G, N, device="cuda")
+    tr = torch.zeros(8 * 4096, dtype=torch.int64, device="cuda")
+    run = lambda: _lib.check(lib.sp_op_gemm(w.data_ptr(), x.data_ptr(), G, N, K, T, T, G * T, bias.data_ptr(), act,
+                                            out.data_ptr(), 0, 1, None))
+    for _ in range(3): run()
+    ts = []
+    for _ in range(5):
+        flush.zero_(); flush_r.sum(); torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(); run(); e1.record(); torch.cuda.synchronize(); ts.append(e0.elapsed_time(e1) * 1e3)
+    flush.zero_(); flush_r.sum(); torch.cuda.synchronize()
+    lib.sp_debug_set_gemm_trace(tr.data_ptr()); run(); torch.cuda.synchronize()
+    cnt = (ctypes.c_int32 * 4)(); lib.sp_debug_gemm_trace_launches(cnt, 4); n_cta = cnt[0]
+    lib.sp_debug_set_gemm_trace(None)
+    t = tr.view(-1, 8)[:n_cta].cpu().numpy().astype(np.float64)
+    fl = 2.0 * G * N * K * T
+    us = np.median(ts)
+    lead = t[t[:, 5] > 0]  # CTAs that issued MMAs
+    span = (lead[:, 5] - lead[:, 4]) / 1e3
+    print(f"{name}: N={N} K={K} act={act} ctas={n_cta} {us:.1f} us = {fl / us / 1e6:.0f} TFLOP/s; MMA span med {np.median(span):.1f} us; "
+          f"MMA waits (med over issuing CTAs): operands {np.median(lead[:, 1]) / 1e3:.1f} us, accumulator {np.median(lead[:, 3]) / 1e3:.1f} us")
