@@ -342,7 +342,8 @@ __global__ void __launch_bounds__(kPThreads, 1)
 
   if (warp == 0) {
     if (elect_one()) {
-      const uint64_t pol_w = policy_evict_last();  // re-read by the other token tiles
+      const uint64_t pol_w = p.w_keep == 2 ? policy_evict_last() : (p.w_keep == 1 ? policy_evict_normal()
+                                                                                     : policy_evict_first());
       const uint64_t pol_x = policy_evict_last();
       auto load_w = [&](int s, int kb, int wrow) {
         if constexpr (PAIR) tma_load_2d_2sm(&map_w, &full[s], smem + s * stage_bytes, kb * kBlockK, wrow, pol_w);

@@ -379,8 +379,15 @@ int run_gemm(sp_group* grp, int kind, const CUtensorMap& wmap, const XMaps& xm, 
     p.splits = 1;
     p.kb_per_split = k_dim / 64;
     p.cluster = 1;
+    static const int w_pol = [] {  // persistent path weight L2 policy: 0 evict_first, 1 normal, 2 evict_last
+      const char* v = getenv("SP_PERSIST_WPOL");
+      return v ? atoi(v) : -1;
+    }();
     sp::gemm_configure_persistent(t_rows, out_f32 != 0, groups * p.m_tiles, sp::sm_count(),
                                   sp::gemm_persistent_pair(t_rows, p.m_tiles, groups), &p.bn, &p.n_tiles, &p.stages);
+    // weights re-read by many token tiles stay in L2 (evict_last); streamed once or twice (batch-1)
+    // they must not push the residual stream out (evict_first: -2% at L=512)
+    p.w_keep = w_pol >= 0 ? w_pol : (p.n_tiles > 2 ? 2 : 0);
     p.out = out;
     p.out_group_stride = out_gs;
     p.out_ld = n_out;

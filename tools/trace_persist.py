@@ -3,9 +3,10 @@ import sys, os, ctypes, numpy as np, torch
 sys.path.insert(0, ".")
 from paper_2408_12526_b200 import _lib
 lib = _lib.load()
-G, T = 12, int(sys.argv[1]) if len(sys.argv) > 1 else 4224
-shapes = {"qkv": (3072, 1024, 0), "o": (1024, 1024, 0), "ffn1_gelu": (4096, 1024, 2), "ffn1_id": (4096, 1024, 0),
-          "ffn2": (1024, 4096, 0)}
+G = int(os.environ.get("TP_G", 12)); T = int(sys.argv[1]) if len(sys.argv) > 1 else 4224
+H = int(os.environ.get("TP_H", 1024))
+shapes = {"qkv": (3 * H, H, 0), "o": (H, H, 0), "ffn1_gelu": (4 * H, H, 2), "ffn1_id": (4 * H, H, 0),
+          "ffn2": (H, 4 * H, 0)}
 flush = torch.empty(256 << 18, device="cuda"); flush_r = torch.ones(256 << 18, device="cuda")
 for name, (N, K, act) in shapes.items():
     w = (torch.randn(G, N, K, device="cuda") * 0.02).half()
