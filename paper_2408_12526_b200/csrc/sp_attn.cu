@@ -16,8 +16,8 @@
 
 namespace sp {
 
-template <int D, int NW>
-__global__ void __launch_bounds__(32 * NW, NW == 4 ? 4 : 2)
+template <int D, int NW, int MINB>
+__global__ void __launch_bounds__(32 * NW, MINB)
     attn_kernel(const half* __restrict__ qkv, half* __restrict__ ctx, const int* __restrict__ cu, int n_heads,
                 int hidden, long long group_rows, float scale_log2, const void* pf_ptr, unsigned long long pf_bytes) {
   constexpr int BQ = 16 * NW, BK = 64, LD = D + 8;  // +8 halfs: conflict-free ldmatrix rows
@@ -108,44 +108,49 @@ __global__ void __launch_bounds__(32 * NW, NW == 4 ? 4 : 2)
         if (kk + 1 < D / 16) mma_16816(s[nt], qa[kk + 1], kf[2], kf[3]);
       }
     }
-    // scale (log2 domain) + key mask, row max
+    // row max of the raw scores (key mask only in the block that crosses the sequence end), then
+    // p = 2^(s * scale_log2 - m) as one FFMA + MUFU.EX2 per score; m kept in the scaled domain
+    if (k0 + BK > L) {
+#pragma unroll
+      for (int nt = 0; nt < BK / 8; ++nt)
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (k0 + nt * 8 + 2 * tq + (e & 1) >= L) s[nt][e] = -INFINITY;
+    }
     float mx[2] = {-INFINITY, -INFINITY};
 #pragma unroll
     for (int nt = 0; nt < BK / 8; ++nt) {
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int key = k0 + nt * 8 + 2 * tq + (e & 1);
-        float x = s[nt][e] * scale_log2;
-        if (key >= L) x = -INFINITY;
-        s[nt][e] = x;
-        mx[e >> 1] = fmaxf(mx[e >> 1], x);
-      }
+      mx[0] = fmaxf(mx[0], fmaxf(s[nt][0], s[nt][1]));
+      mx[1] = fmaxf(mx[1], fmaxf(s[nt][2], s[nt][3]));
     }
-    float corr[2];
+    float corr[2], neg_m[2];
 #pragma unroll
     for (int r = 0; r < 2; ++r) {
       mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 1));
       mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 2));
-      const float m_new = fmaxf(m_run[r], mx[r]);
-      corr[r] = exp2f(m_run[r] - m_new);
+      const float m_new = fmaxf(m_run[r], mx[r] * scale_log2);
+      corr[r] = fast_exp2(m_run[r] - m_new);
       m_run[r] = m_new;
+      neg_m[r] = -m_new;
       l_run[r] *= corr[r];
     }
 #pragma unroll
     for (int nt = 0; nt < BK / 8; ++nt) {
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        const float pv = exp2f(s[nt][e] - m_run[e >> 1]);
+        const float pv = fast_exp2(fmaf(s[nt][e], scale_log2, neg_m[e >> 1]));
         s[nt][e] = pv;
         l_run[e >> 1] += pv;
       }
     }
+    if (__any_sync(0xffffffffu, corr[0] != 1.f || corr[1] != 1.f)) {  // running max moved: rescale O
 #pragma unroll
-    for (int dt = 0; dt < D / 8; ++dt) {
-      o[dt][0] *= corr[0];
-      o[dt][1] *= corr[0];
-      o[dt][2] *= corr[1];
-      o[dt][3] *= corr[1];
+      for (int dt = 0; dt < D / 8; ++dt) {
+        o[dt][0] *= corr[0];
+        o[dt][1] *= corr[0];
+        o[dt][2] *= corr[1];
+        o[dt][3] *= corr[1];
+      }
     }
     // O += P V
 #pragma unroll
@@ -188,7 +193,7 @@ __global__ void __launch_bounds__(32 * NW, NW == 4 ? 4 : 2)
   }
 }
 
-template <int D, int NW>
+template <int D, int NW, int MINB>
 static void launch_attn_t(const half* qkv, half* ctx, const int* cu, int n_seqs, int max_len, int groups,
                           int n_heads, int hidden, long long group_rows, float scale_log2, const void* pf_ptr,
                           unsigned long long pf_bytes, cudaStream_t stream) {
@@ -196,11 +201,11 @@ static void launch_attn_t(const half* qkv, half* ctx, const int* cu, int n_seqs,
   const size_t smem = (size_t)(BQ + 4 * 64) * LD * sizeof(half);
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(attn_kernel<D, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(attn_kernel<D, NW, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr_set = true;
   }
   dim3 grid((max_len + BQ - 1) / BQ, n_seqs, groups * n_heads);
-  launch_pdl(attn_kernel<D, NW>, grid, dim3(32 * NW), smem, stream, qkv, ctx, cu, n_heads, hidden, group_rows,
+  launch_pdl(attn_kernel<D, NW, MINB>, grid, dim3(32 * NW), smem, stream, qkv, ctx, cu, n_heads, hidden, group_rows,
              scale_log2, pf_ptr, pf_bytes);
 }
 
@@ -214,9 +219,23 @@ void launch_attention(const half* qkv, half* ctx, const int* cu_seqlens, int n_s
     const char* v = getenv("SP_ATTN_NW");
     return v ? atoi(v) : 0;
   }();
-  const int nw = nw_env ? nw_env : (max_len <= 64 ? 4 : (max_len <= 384 ? 6 : 8));  // measured sweep
-#define SP_ATTN(D_, NW_) \
-  launch_attn_t<D_, NW_>(qkv, ctx, cu_seqlens, n_seqs, max_len, groups, n_heads, hidden, group_rows, scale_log2, pf_ptr, pf_bytes, stream)
+  const int nw = nw_env ? nw_env : (max_len <= 128 ? 4 : (max_len <= 288 ? 6 : 8));  // measured sweep
+  // resident CTAs per SM (register cap): SP_ATTN_MINB overrides the default (4 for 4 warps, else 2)
+  static const int minb_env = [] {
+    const char* v = getenv("SP_ATTN_MINB");
+    return v ? atoi(v) : 0;
+  }();
+  const int minb = minb_env ? minb_env : (nw == 4 ? 4 : 2);
+#define SP_ATTN_B(D_, NW_, B_) \
+  launch_attn_t<D_, NW_, B_>(qkv, ctx, cu_seqlens, n_seqs, max_len, groups, n_heads, hidden, group_rows, scale_log2, pf_ptr, pf_bytes, stream)
+#define SP_ATTN(D_, NW_)                                     \
+  do {                                                      \
+    if (minb >= 6) SP_ATTN_B(D_, NW_, 6);                   \
+    else if (minb == 5) SP_ATTN_B(D_, NW_, 5);              \
+    else if (minb == 4) SP_ATTN_B(D_, NW_, 4);              \
+    else if (minb == 3) SP_ATTN_B(D_, NW_, 3);              \
+    else SP_ATTN_B(D_, NW_, 2);                             \
+  } while (0)
   if (head_dim == 64) {
     if (nw == 8) SP_ATTN(64, 8);
     else if (nw == 6) SP_ATTN(64, 6);
@@ -227,6 +246,7 @@ void launch_attention(const half* qkv, half* ctx, const int* cu_seqlens, int n_s
     else SP_ATTN(32, 4);
   }
 #undef SP_ATTN
+#undef SP_ATTN_B
 }
 
 }  // namespace sp
