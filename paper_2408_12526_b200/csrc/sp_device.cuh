@@ -66,16 +66,18 @@ template <int NC>
 __device__ __forceinline__ void layer_norm_store(float (&v)[NC][4], const float* gamma, const float* beta, float eps,
                                                  int hidden, float* x32, half* x16, half* cls16) {
   const int lane = lane_id();
+  float s = 0.f;
+#pragma unroll
+  for (int c = 0; c < NC; ++c) s += (v[c][0] + v[c][1]) + (v[c][2] + v[c][3]);
+  const float mean = warp_sum(s) / hidden;
+  // gamma / beta issued here (not with the row loads): the row's inputs are dead by now, so they
+  // do not add to the peak register count, and the loads overlap the variance reduction
   float4 gm[NC], bt[NC];
 #pragma unroll
   for (int c = 0; c < NC; ++c) {
     gm[c] = __ldg(reinterpret_cast<const float4*>(gamma + c * 128 + lane * 4));
     bt[c] = __ldg(reinterpret_cast<const float4*>(beta + c * 128 + lane * 4));
   }
-  float s = 0.f;
-#pragma unroll
-  for (int c = 0; c < NC; ++c) s += (v[c][0] + v[c][1]) + (v[c][2] + v[c][3]);
-  const float mean = warp_sum(s) / hidden;
   float q = 0.f;
 #pragma unroll
   for (int c = 0; c < NC; ++c)

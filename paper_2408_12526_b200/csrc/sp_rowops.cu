@@ -54,7 +54,9 @@ __global__ void __launch_bounds__(128)
                        x16 + row, nullptr);
 }
 
-template <int NC>
+// SPLITS: number of split-K partials, a template parameter so only the live ones hold registers
+// (4 x NC float4 partials capped occupancy at 4 blocks/SM when the persistent path writes one).
+template <int NC, int SPLITS>
 __global__ void __launch_bounds__(128)
     reduce_ln_kernel(const float* __restrict__ part, int splits, long long part_split_stride,
                      const float* __restrict__ bias, const float* __restrict__ gamma, const float* __restrict__ beta,
@@ -71,15 +73,14 @@ __global__ void __launch_bounds__(128)
   const int lane = lane_id();
   const long long row = (long long)g * x_gs + (long long)t * hidden;
   // issue every load of the row up front: residual, bias and up to kMaxSplitsRow partial sums
-  float4 r[NC], bs[NC], pv[kMaxSplitsRow][NC];
+  float4 r[NC], bs[NC], pv[SPLITS][NC];
 #pragma unroll
   for (int c = 0; c < NC; ++c) {
     const int f = c * 128 + lane * 4;
     r[c] = *reinterpret_cast<const float4*>(x32 + row + f);
     bs[c] = __ldg(reinterpret_cast<const float4*>(bias + (long long)g * hidden + f));
 #pragma unroll
-    for (int s = 0; s < kMaxSplitsRow; ++s)
-      if (s < splits) pv[s][c] = *reinterpret_cast<const float4*>(part + s * part_split_stride + row + f);
+    for (int s = 0; s < SPLITS; ++s) pv[s][c] = *reinterpret_cast<const float4*>(part + s * part_split_stride + row + f);
   }
   float v[NC][4];
 #pragma unroll
@@ -89,13 +90,11 @@ __global__ void __launch_bounds__(128)
     v[c][2] = r[c].z + bs[c].z;
     v[c][3] = r[c].w + bs[c].w;
 #pragma unroll
-    for (int s = 0; s < kMaxSplitsRow; ++s) {  // fixed order: deterministic
-      if (s < splits) {
-        v[c][0] += pv[s][c].x;
-        v[c][1] += pv[s][c].y;
-        v[c][2] += pv[s][c].z;
-        v[c][3] += pv[s][c].w;
-      }
+    for (int s = 0; s < SPLITS; ++s) {  // fixed order: deterministic
+      v[c][0] += pv[s][c].x;
+      v[c][1] += pv[s][c].y;
+      v[c][2] += pv[s][c].z;
+      v[c][3] += pv[s][c].w;
     }
   }
   half* cls_row = nullptr;
@@ -223,9 +222,16 @@ void launch_reduce_ln(const float* part, int splits, long long part_split_stride
   if (n_tokens == 0 || groups <= 0) return;
   dim3 grid(((n_tokens < 0 ? -n_tokens : n_tokens) + 3) / 4, groups);
   if (n_tokens < 0) n_tokens = -1;
-#define SP_REDUCE(NC_)                                                                                          \
-  launch_pdl(reduce_ln_kernel<NC_>, grid, dim3(128), 0, stream, part, splits, part_split_stride, bias, gamma, \
+#define SP_REDUCE_S(NC_, S_)                                                                                     \
+  launch_pdl(reduce_ln_kernel<NC_, S_>, grid, dim3(128), 0, stream, part, splits, part_split_stride, bias, gamma, \
              beta, hidden, eps, x32, x16, x_gs, n_tokens, cu_seqlens, n_seqs, cls16, cls_gs, pf_ptr, pf_bytes)
+#define SP_REDUCE(NC_)                     \
+  do {                                     \
+    if (splits <= 1) SP_REDUCE_S(NC_, 1);  \
+    else if (splits == 2) SP_REDUCE_S(NC_, 2); \
+    else if (splits == 3) SP_REDUCE_S(NC_, 3); \
+    else SP_REDUCE_S(NC_, 4);              \
+  } while (0)
   switch (hidden / 128) {
     case 1: SP_REDUCE(1); break;
     case 2: SP_REDUCE(2); break;
@@ -235,6 +241,7 @@ void launch_reduce_ln(const float* part, int splits, long long part_split_stride
     default: break;
   }
 #undef SP_REDUCE
+#undef SP_REDUCE_S
 }
 
 void launch_head(const float* final_rep, long long final_gs, long long split_stride, int splits,
