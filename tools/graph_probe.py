@@ -1,6 +1,11 @@
 """How much of a batch-1 request is host launch overhead? Eager vs CUDA-graph replay."""
 import sys, numpy as np, torch
 sys.path.insert(0, ".")
+import os
+if os.environ.get("SP_LIB_OVERRIDE"):  # A/B another build of the engine library
+    from pathlib import Path
+    import paper_2408_12526_b200._lib as _L
+    _L.LIB_PATH = Path(os.environ["SP_LIB_OVERRIDE"])
 from paper_2408_12526_b200 import PRESETS, StudentGroup, random_bert_group
 cfg, K = PRESETS["base"]
 w = random_bert_group(cfg, K, seed=0)
