@@ -103,8 +103,11 @@ struct sp_group {
   half* cls16 = nullptr;   // [S][max_seqs][H] CLS rows
   float* final32 = nullptr;  // [S][rows_cap][H] per-student final representation
   half* xin = nullptr;     // dense: [max_tokens][d_in] staged input (host API)
-  int32_t* d_ids = nullptr;
+  int32_t* d_ids = nullptr;   // staging block [cu_pad | ids]: d_cu = block, d_ids = block + cu_pad
   int32_t* d_cu = nullptr;
+  int cu_pad = 0;             // max_seqs + 1 rounded up to 32 ints (128 B)
+  int32_t* h_stage = nullptr;  // pinned mirror of the staging block: one H2D copy per request
+  float* h_logits = nullptr;   // pinned logits landing buffer
   float* d_logits = nullptr;
   std::vector<void*> allocs;
   // tensor maps
@@ -182,6 +185,10 @@ void free_all(sp_group* g) {
   g->cap_stream = nullptr;
   for (void* p : g->allocs) cudaFree(p);
   g->allocs.clear();
+  if (g->h_stage) cudaFreeHost(g->h_stage);
+  if (g->h_logits) cudaFreeHost(g->h_logits);
+  g->h_stage = nullptr;
+  g->h_logits = nullptr;
   for (auto& r : g->recs) {
     cudaEventDestroy(r.e0);
     cudaEventDestroy(r.e1);
@@ -242,8 +249,14 @@ int sp_group_create(const sp_config* cfg, const sp_weights* weights, int device,
     return code;
   };
   if ((rc = dev_alloc(g, &g->final32, (size_t)kMaxSplits * S * R * H))) return bail(rc);  // pooler split-K partials
-  if ((rc = dev_alloc(g, &g->d_ids, T))) return bail(rc);
-  if ((rc = dev_alloc(g, &g->d_cu, B + 1))) return bail(rc);
+  g->cu_pad = ((B + 1 + 31) / 32) * 32;
+  if ((rc = dev_alloc(g, &g->d_cu, (size_t)g->cu_pad + T))) return bail(rc);
+  g->d_ids = g->d_cu + g->cu_pad;
+  if (cudaHostAlloc(reinterpret_cast<void**>(&g->h_stage), sizeof(int32_t) * ((size_t)g->cu_pad + T),
+                    cudaHostAllocDefault) != cudaSuccess ||
+      cudaHostAlloc(reinterpret_cast<void**>(&g->h_logits), sizeof(float) * (size_t)R * c.n_classes,
+                    cudaHostAllocDefault) != cudaSuccess)
+    return bail(fail(SP_ENOMEM, "pinned staging buffers"));
   if ((rc = dev_alloc(g, &g->d_logits, R * c.n_classes))) return bail(rc);
 
   if (c.kind == SP_KIND_BERT) {
@@ -752,7 +765,12 @@ int get_graph(sp_group* g, int n_tokens, int k, int add_bias, cudaGraphExec_t* o
   if (g->cap_stream == nullptr) SP_CUDA(cudaStreamCreateWithFlags(&g->cap_stream, cudaStreamNonBlocking));
   SP_CUDA(cudaStreamBeginCapture(g->cap_stream, cudaStreamCaptureModeThreadLocal));
   const int max_len = std::min(bucket, g->cfg.max_pos);
+  // the request's copies are graph nodes too: pinned [cu | ids] staging -> device (bucket size; the
+  // kernels read the live length from cu), forward, logits -> pinned
+  cudaMemcpyAsync(g->d_cu, g->h_stage, sizeof(int32_t) * ((size_t)g->cu_pad + std::min(bucket, g->cfg.max_tokens)),
+                  cudaMemcpyHostToDevice, g->cap_stream);
   int rc = bert_forward(g, g->d_ids, g->d_cu, 1, bucket, max_len, k, nullptr, g->d_logits, add_bias, g->cap_stream, true);
+  cudaMemcpyAsync(g->h_logits, g->d_logits, sizeof(float) * g->cfg.n_classes, cudaMemcpyDeviceToHost, g->cap_stream);
   cudaGraph_t graph = nullptr;
   cudaError_t e = cudaStreamEndCapture(g->cap_stream, &graph);
   if (rc) return rc;
@@ -932,18 +950,28 @@ int sp_group_forward_host(sp_group* g, const int32_t* ids, const int32_t* cu, in
     int rc = get_graph(g, n_tokens, k_active, add_bias, &exec);
     if (rc) return rc;
   }
-  SP_CUDA(cudaMemcpyAsync(g->d_ids, ids, sizeof(int32_t) * n_tokens, cudaMemcpyHostToDevice, st));
-  SP_CUDA(cudaMemcpyAsync(g->d_cu, cu, sizeof(int32_t) * (n_seqs + 1), cudaMemcpyHostToDevice, st));
-  if (use_graph) {
+  // pinned staging ([cu | ids] block; the caller's buffers may be pageable). Every call ends with a
+  // stream sync, so the previous request no longer reads h_stage.
+  memcpy(g->h_stage, cu, sizeof(int32_t) * (n_seqs + 1));
+  memcpy(g->h_stage + g->cu_pad, ids, sizeof(int32_t) * n_tokens);
+  if (use_graph) {  // H2D copy, forward and D2H copy are all nodes of the bucket's graph
     SP_CUDA(cudaGraphLaunch(exec, st));
     g->last_launches = g->graph_launches;
-  } else {
+    SP_CUDA(cudaStreamSynchronize(st));
+    memcpy(logits_out, g->h_logits, sizeof(float) * c.n_classes);
+    return SP_OK;
+  }
+  SP_CUDA(cudaMemcpyAsync(g->d_cu, g->h_stage, sizeof(int32_t) * ((size_t)g->cu_pad + n_tokens),
+                          cudaMemcpyHostToDevice, st));
+  {
     int rc = bert_forward(g, g->d_ids, g->d_cu, n_seqs, n_tokens, max_len, k_active, nullptr, g->d_logits, add_bias, st);
     if (rc) return rc;
   }
   SP_CUDA(cudaGetLastError());
-  SP_CUDA(cudaMemcpyAsync(logits_out, g->d_logits, sizeof(float) * n_seqs * c.n_classes, cudaMemcpyDeviceToHost, st));
+  SP_CUDA(cudaMemcpyAsync(g->h_logits, g->d_logits, sizeof(float) * n_seqs * c.n_classes, cudaMemcpyDeviceToHost,
+                          st));
   SP_CUDA(cudaStreamSynchronize(st));
+  memcpy(logits_out, g->h_logits, sizeof(float) * n_seqs * c.n_classes);
   return SP_OK;
 }
 

@@ -37,9 +37,16 @@ def _ptr(t: torch.Tensor | None) -> int | None:
     return None if t is None else t.data_ptr()
 
 
+_raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+
+
 def _stream_handle(stream: torch.cuda.Stream | None, device: torch.device) -> int:
-    s = stream if stream is not None else torch.cuda.current_stream(device)
-    return s.cuda_stream
+    if stream is not None:
+        return stream.cuda_stream
+    if _raw_stream is not None:  # ~10x cheaper than building a torch.cuda.Stream object
+        return _raw_stream(device.index if isinstance(device, torch.device) and device.index is not None
+                           else torch.cuda.current_device())
+    return torch.cuda.current_stream(device).cuda_stream
 
 
 def pack_sequences(x) -> tuple[np.ndarray, np.ndarray, bool]:
@@ -190,6 +197,14 @@ class StudentGroup:
     # ------------------------------------------------------------------ k handling
     def local_k(self, k: int | None, total: int | None = None) -> int:
         """Map the reference's global prefix k (distill.py:171-173) to the number of local students."""
+        key = (k, total)
+        cache = self.__dict__.setdefault("_local_k_cache", {})
+        if key in cache:
+            return cache[key]
+        cache[key] = n = self._local_k(k, total)
+        return n
+
+    def _local_k(self, k: int | None, total: int | None) -> int:
         total = self.n_students if total is None else total
         k = total if k is None else int(k)
         if not 1 <= k <= total:
