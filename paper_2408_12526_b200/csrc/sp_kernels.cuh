@@ -188,6 +188,29 @@ struct ReqParams {
   unsigned long long* trace;  // optional per-CTA timeline (64 stamps per CTA), else null
 };
 
+// FFN1 + FFN2 of one layer in one persistent kernel (sp_mlp.cu).
+struct MlpMaps {
+  CUtensorMap w_a, xa64, xa16;  // FFN1 weights [S*F, H]; LayerNorm output x16
+  CUtensorMap w_b, xb64, xb16;  // FFN2 weights [S*H, F]; GELU activations
+};
+struct MlpParams {
+  int n_a, k_a, bn_a, n_tiles_a;  // FFN1: n_out = F, k = H
+  int n_b, k_b, bn_b, n_tiles_b;  // FFN2: n_out = H, k = F
+  int groups, t_rows, x_group_rows, stages;
+  const int* t_dev;
+  half* out_a;  // GELU activations [S][x_group_rows][F]
+  long long out_a_gs;
+  int out_a_ld;
+  const float* bias_a;
+  int bias_a_gs;
+  float* out_b;  // raw FFN2 projection [S][x_group_rows][H]
+  long long out_b_gs;
+  int out_b_ld;
+  int* done;  // [kReqMaxStudents + 1] FFN1 tiles finished per student + exit counter (zero between launches)
+};
+int mlp_smem_bytes(int bn_max, int* stages);
+void launch_mlp(const MlpMaps& m, const MlpParams& p, cudaStream_t stream);
+
 // Dynamic shared memory of the per-request kernel for head_dim d (ring + attention K/V + barriers).
 int request_smem_bytes(int head_dim, int* ring_bytes);
 // Returns false if (hidden, head_dim) has no instantiation.

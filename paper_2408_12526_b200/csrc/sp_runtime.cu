@@ -109,6 +109,7 @@ struct sp_group {
   int32_t* h_stage = nullptr;  // pinned mirror of the staging block: one H2D copy per request
   float* h_logits = nullptr;   // pinned logits landing buffer
   float* d_logits = nullptr;
+  int* mlp_done = nullptr;  // fused FFN kernel: FFN1 tiles finished per student + exit counter
   std::vector<void*> allocs;
   // tensor maps
   std::vector<CUtensorMap> m_qkv, m_o, m_f1, m_f2, m_layers;
@@ -258,6 +259,9 @@ int sp_group_create(const sp_config* cfg, const sp_weights* weights, int device,
                     cudaHostAllocDefault) != cudaSuccess)
     return bail(fail(SP_ENOMEM, "pinned staging buffers"));
   if ((rc = dev_alloc(g, &g->d_logits, R * c.n_classes))) return bail(rc);
+  if ((rc = dev_alloc(g, &g->mlp_done, sp::kReqMaxStudents + 1))) return bail(rc);
+  if (cudaMemset(g->mlp_done, 0, sizeof(int) * (sp::kReqMaxStudents + 1)) != cudaSuccess)
+    return bail(fail(SP_ECUDA, "memset"));
 
   if (c.kind == SP_KIND_BERT) {
     if (!w.word_emb || !w.pos_emb || !w.type_emb || !w.emb_ln_gamma || !w.emb_ln_beta || !w.w_qkv || !w.b_qkv ||
@@ -630,6 +634,58 @@ int fused_forward(sp_group* g, const int32_t* ids, const int32_t* cu, int n_seqs
   return SP_OK;
 }
 
+bool mlp_fusion_enabled() {  // SP_MLP_FUSE=0 falls back to two launches
+  static const bool on = [] {
+    const char* v = getenv("SP_MLP_FUSE");
+    return v == nullptr || atoi(v) != 0;
+  }();
+  return on;
+}
+
+// FFN1 (+GELU) and FFN2 of layer l as one persistent kernel (sp_mlp.cu); FFN2's raw projection
+// lands in g->part (one split) for the LayerNorm kernel.
+int run_mlp(sp_group* g, int l, int k, int n_tokens, const int* t_dev, cudaStream_t st) {
+  const sp_config& c = g->cfg;
+  const sp_weights& w = g->w;
+  const int H = c.hidden, F = c.ffn, T = c.max_tokens;
+  const size_t lS = (size_t)l * c.n_students;
+  sp::MlpParams p{};
+  p.n_a = F;
+  p.k_a = H;
+  p.n_b = H;
+  p.k_b = F;
+  int stages = 0;
+  sp::gemm_configure_persistent(n_tokens, false, k * (F / 128), sp::sm_count(), false, &p.bn_a, &p.n_tiles_a, &stages);
+  sp::gemm_configure_persistent(n_tokens, true, k * (H / 128), sp::sm_count(), false, &p.bn_b, &p.n_tiles_b, &stages);
+  sp::mlp_smem_bytes(std::max(p.bn_a, p.bn_b), &p.stages);
+  p.groups = k;
+  p.t_rows = n_tokens;
+  p.x_group_rows = T;
+  p.t_dev = t_dev;
+  p.out_a = g->ffn;
+  p.out_a_gs = (long long)T * F;
+  p.out_a_ld = F;
+  p.bias_a = w.b_ffn1 + lS * F;
+  p.bias_a_gs = F;
+  p.out_b = g->part;
+  p.out_b_gs = (long long)T * H;
+  p.out_b_ld = H;
+  p.done = g->mlp_done;
+  sp::MlpMaps m;
+  m.w_a = g->m_f1[l];
+  m.xa64 = g->xm_x16.x64;
+  m.xa16 = g->xm_x16.x16;
+  m.w_b = g->m_f2[l];
+  m.xb64 = g->xm_ffn.x64;
+  m.xb16 = g->xm_ffn.x16;
+  const double G = k, Tt = n_tokens;
+  g->rec_begin(SP_LAUNCH_GEMM_FFN1, G * 2.0 * F * H * 2.0 + G * Tt * (H * 2.0 + F * 2.0 * 2.0 + H * 4.0),
+               2.0 * 2.0 * G * F * H * Tt);
+  sp::launch_mlp(m, p, st);
+  g->rec_end();
+  return 1;
+}
+
 // dyn = true (graph capture): n_tokens / max_len are bucket bounds used for grids and tiles; every
 // kernel reads the live token count from cu_seqlens[n_seqs] on the device.
 int bert_forward(sp_group* g, const int32_t* ids, const int32_t* cu, int n_seqs, int n_tokens, int max_len, int k,
@@ -701,18 +757,30 @@ int bert_forward(sp_group* g, const int32_t* ids, const int32_t* cu, int n_seqs,
         g->rec_end();
         ++launches;
       }
-      launches += run_gemm(g, SP_LAUNCH_GEMM_FFN1, g->m_f1[l], g->xm_x16, k, F, H, n_tokens, T, w.b_ffn1 + lS * F, F, sp::ACT_GELU, g->ffn,
-                           (long long)T * F, 0, 1, 0, st, t_dev);
+      // FFN1 + FFN2 as one persistent kernel where both would take the (single-CTA) persistent path
+      // (only where FFN2 itself would be a one-split persistent GEMM: measured -2% at L=512, but
+      // +3% at L=256 where FFN2's split-K tiles beat the fused kernel's 96-token phase-B tiles)
+      const bool mlp = mlp_fusion_enabled() && s_f == 1 && n_tokens >= 129 &&
+                       !sp::gemm_persistent_pair(n_tokens, F / 128, k) && !sp::gemm_persistent_pair(n_tokens, H / 128, k) &&
+                       !use_ln_fused(H / 128, n_tiles, k, F, H);
+      if (mlp) {
+        launches += run_mlp(g, l, k, n_tokens, t_dev, st);
+      } else {
+        launches += run_gemm(g, SP_LAUNCH_GEMM_FFN1, g->m_f1[l], g->xm_x16, k, F, H, n_tokens, T, w.b_ffn1 + lS * F, F,
+                             sp::ACT_GELU, g->ffn, (long long)T * F, 0, 1, 0, st, t_dev);
+      }
       const bool last = (l == c.n_layers - 1);
-      if (use_ln_fused(H / 128, n_tiles, k, F, H)) {
+      if (!mlp && use_ln_fused(H / 128, n_tiles, k, F, H)) {
         sp::LnParams ln{w.b_ffn2 + lS * H, w.ln2_gamma + lS * H, w.ln2_beta + lS * H, c.ln_eps, g->x32, g->x16, xgs,
                         last ? g->cls16 : nullptr, (long long)B * H, cu, n_seqs, H};
         launches += run_gemm_ln(g, SP_LAUNCH_GEMM_FFN2, g->m_f2[l], g->xm_ffn, k, H, F, n_tokens, T, ln, t_dev, st);
       } else {
-        launches += run_gemm(g, SP_LAUNCH_GEMM_FFN2, g->m_f2[l], g->xm_ffn, k, H, F, n_tokens, T, nullptr, H,
-                             sp::ACT_NONE, g->part, xgs, 1, s_f, part_ss, st, t_dev);
-        g->rec_begin(SP_LAUNCH_REDUCE_LN, GTH * (4.0 * s_f + 10.0), 0.0);
-        sp::launch_reduce_ln(g->part, s_f, part_ss, w.b_ffn2 + lS * H, w.ln2_gamma + lS * H, w.ln2_beta + lS * H, H,
+        if (!mlp)
+          launches += run_gemm(g, SP_LAUNCH_GEMM_FFN2, g->m_f2[l], g->xm_ffn, k, H, F, n_tokens, T, nullptr, H,
+                               sp::ACT_NONE, g->part, xgs, 1, s_f, part_ss, st, t_dev);
+        const int s_ln2 = mlp ? 1 : s_f;  // the fused MLP kernel writes one (complete) projection
+        g->rec_begin(SP_LAUNCH_REDUCE_LN, GTH * (4.0 * s_ln2 + 10.0), 0.0);
+        sp::launch_reduce_ln(g->part, s_ln2, part_ss, w.b_ffn2 + lS * H, w.ln2_gamma + lS * H, w.ln2_beta + lS * H, H,
                              c.ln_eps, g->x32, g->x16, xgs, n_rows_arg, k, cu, n_seqs, last ? g->cls16 : nullptr,
                              (long long)B * H, st,
                              PF(last ? pf(w.w_pool, (size_t)k * H * H) : pf(wq + (lS + S) * 3 * H * H, (size_t)k * 3 * H * H)));
