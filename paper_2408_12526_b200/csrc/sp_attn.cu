@@ -16,7 +16,8 @@
 
 namespace sp {
 
-template <int D, int NW, int MINB>
+// NBUF: K/V blocks in the cp.async ring (NBUF-1 in flight ahead of the one being consumed).
+template <int D, int NW, int MINB, int NBUF>
 __global__ void __launch_bounds__(32 * NW, MINB)
     attn_kernel(const half* __restrict__ qkv, half* __restrict__ ctx, const int* __restrict__ cu, int n_heads,
                 int hidden, long long group_rows, float scale_log2, const void* pf_ptr, unsigned long long pf_bytes) {
@@ -25,8 +26,8 @@ __global__ void __launch_bounds__(32 * NW, MINB)
   constexpr int VPR = D / 8;  // 16-byte vectors per row
   extern __shared__ __align__(16) uint8_t attn_smem[];
   half* sQ = reinterpret_cast<half*>(attn_smem);
-  half* sK = sQ + BQ * LD;        // [2][BK][LD]
-  half* sV = sK + 2 * BK * LD;    // [2][BK][LD]
+  half* sK = sQ + BQ * LD;         // [NBUF][BK][LD]
+  half* sV = sK + NBUF * BK * LD;  // [NBUF][BK][LD]
 
   prefetch_share_l2(pf_ptr, pf_bytes);  // next projection's weights, while attention runs
   pdl_wait();
@@ -56,14 +57,18 @@ __global__ void __launch_bounds__(32 * NW, MINB)
     }
   };
 
-  // Q tile + first K/V block
+  // Q tile + the first NBUF-1 K/V blocks (one commit group each, empty groups past the end)
   for (int i = tid; i < BQ * VPR; i += NT) {
     const int r = i / VPR, c = (i % VPR) * 8;
     const bool ok = q0 + r < L;
     cp_async16(sQ + r * LD + c, base + (long long)(ok ? q0 + r : 0) * row_stride + c, ok ? 16u : 0u);
   }
-  load_kv(0, 0);
-  cp_async_commit();
+  const int n_blk = (L + BK - 1) / BK;
+#pragma unroll
+  for (int i = 0; i < NBUF - 1; ++i) {
+    if (i < n_blk) load_kv(i, i * BK);
+    cp_async_commit();
+  }
 
   uint32_t qa[D / 16][4];
   float o[D / 8][4];
@@ -74,10 +79,11 @@ __global__ void __launch_bounds__(32 * NW, MINB)
   const int n_blocks = (L + BK - 1) / BK;
 
   for (int kb = 0; kb < n_blocks; ++kb) {
-    const int buf = kb & 1;
-    if (kb + 1 < n_blocks) load_kv(buf ^ 1, (kb + 1) * BK);  // prefetch the next block
+    const int buf = kb % NBUF;
+    // refill the buffer freed by block kb-1 with block kb+NBUF-1, then wait for block kb
+    if (kb + NBUF - 1 < n_blocks) load_kv((kb + NBUF - 1) % NBUF, (kb + NBUF - 1) * BK);
     cp_async_commit();
-    cp_async_wait<1>();  // everything but the just-issued prefetch has landed
+    cp_async_wait<NBUF - 1>();  // all but the NBUF-1 newest groups have landed: block kb is in
     __syncthreads();
     if (kb == 0) {
       // Q fragments (A operand, row-major 16 x 16 per k-step) via ldmatrix
@@ -193,19 +199,19 @@ __global__ void __launch_bounds__(32 * NW, MINB)
   }
 }
 
-template <int D, int NW, int MINB>
+template <int D, int NW, int MINB, int NBUF>
 static void launch_attn_t(const half* qkv, half* ctx, const int* cu, int n_seqs, int max_len, int groups,
                           int n_heads, int hidden, long long group_rows, float scale_log2, const void* pf_ptr,
                           unsigned long long pf_bytes, cudaStream_t stream) {
   constexpr int BQ = 16 * NW, LD = D + 8;
-  const size_t smem = (size_t)(BQ + 4 * 64) * LD * sizeof(half);
+  const size_t smem = (size_t)(BQ + 2 * NBUF * 64) * LD * sizeof(half);
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(attn_kernel<D, NW, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(attn_kernel<D, NW, MINB, NBUF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr_set = true;
   }
   dim3 grid((max_len + BQ - 1) / BQ, n_seqs, groups * n_heads);
-  launch_pdl(attn_kernel<D, NW, MINB>, grid, dim3(32 * NW), smem, stream, qkv, ctx, cu, n_heads, hidden, group_rows,
+  launch_pdl(attn_kernel<D, NW, MINB, NBUF>, grid, dim3(32 * NW), smem, stream, qkv, ctx, cu, n_heads, hidden, group_rows,
              scale_log2, pf_ptr, pf_bytes);
 }
 
@@ -226,8 +232,21 @@ void launch_attention(const half* qkv, half* ctx, const int* cu_seqlens, int n_s
     return v ? atoi(v) : 0;
   }();
   const int minb = minb_env ? minb_env : (nw == 4 ? 4 : 2);
-#define SP_ATTN_B(D_, NW_, B_) \
-  launch_attn_t<D_, NW_, B_>(qkv, ctx, cu_seqlens, n_seqs, max_len, groups, n_heads, hidden, group_rows, scale_log2, pf_ptr, pf_bytes, stream)
+  // K/V ring depth: SP_ATTN_NBUF overrides (2 or 4)
+  static const int nbuf_env = [] {
+    const char* v = getenv("SP_ATTN_NBUF");
+    return v ? atoi(v) : 0;
+  }();
+  const int nbuf = nbuf_env ? nbuf_env : 2;  // 4 measured no faster: attention is compute-bound per CTA
+#define SP_ATTN_B(D_, NW_, B_)                                                                                      \
+  do {                                                                                                             \
+    if (nbuf >= 4)                                                                                                 \
+      launch_attn_t<D_, NW_, B_, 4>(qkv, ctx, cu_seqlens, n_seqs, max_len, groups, n_heads, hidden, group_rows,    \
+                                    scale_log2, pf_ptr, pf_bytes, stream);                                         \
+    else                                                                                                           \
+      launch_attn_t<D_, NW_, B_, 2>(qkv, ctx, cu_seqlens, n_seqs, max_len, groups, n_heads, hidden, group_rows,    \
+                                    scale_log2, pf_ptr, pf_bytes, stream);                                         \
+  } while (0)
 #define SP_ATTN(D_, NW_)                                     \
   do {                                                      \
     if (minb >= 6) SP_ATTN_B(D_, NW_, 6);                   \
