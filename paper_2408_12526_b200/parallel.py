@@ -80,13 +80,25 @@ class ShardedStudentGroup:
         from .group import validate_packed
 
         cfg = self.local.weights.cfg
+        ids = np.ascontiguousarray(ids, dtype=np.int32)
+        cu = np.ascontiguousarray(cu, dtype=np.int32)
         max_len = validate_packed(ids, cu, cfg.vocab, cfg.max_pos)
-        n = len(cu) - 1
-        dev = self.device
-        ids_h = torch.from_numpy(np.ascontiguousarray(ids, dtype=np.int32)).pin_memory()
-        cu_h = torch.from_numpy(np.ascontiguousarray(cu, dtype=np.int32)).pin_memory()
-        ids_d = ids_h.to(dev, non_blocking=True)
-        cu_d = cu_h.to(dev, non_blocking=True)
-        logits = torch.empty((n, self.n_classes), dtype=torch.float32, device=dev)
-        self.forward_packed_device(ids_d, cu_d, n, len(ids), max_len, k, logits)
-        return logits.cpu().numpy()
+        n, t = len(cu) - 1, len(ids)
+        if n > self.local.max_seqs or t > self.local.max_tokens:
+            raise ValueError(f"request ({n} seqs, {t} tokens) exceeds the group's capacity")
+        if self._pinned_logits is None:  # staging allocated once (pinned: async copies, no per-call alloc)
+            dev = self.device
+            self._h_ids = torch.empty(self.local.max_tokens, dtype=torch.int32).pin_memory()
+            self._h_cu = torch.empty(self.local.max_seqs + 1, dtype=torch.int32).pin_memory()
+            self._d_ids = torch.empty(self.local.max_tokens, dtype=torch.int32, device=dev)
+            self._d_cu = torch.empty(self.local.max_seqs + 1, dtype=torch.int32, device=dev)
+            self._d_logits = torch.empty((self.local.max_seqs, self.n_classes), dtype=torch.float32, device=dev)
+            self._pinned_logits = torch.empty((self.local.max_seqs, self.n_classes), dtype=torch.float32).pin_memory()
+        self._h_ids.numpy()[:t] = ids
+        self._h_cu.numpy()[: n + 1] = cu
+        self._d_ids[:t].copy_(self._h_ids[:t], non_blocking=True)
+        self._d_cu[: n + 1].copy_(self._h_cu[: n + 1], non_blocking=True)
+        self.forward_packed_device(self._d_ids, self._d_cu, n, t, max_len, k, self._d_logits)
+        self._pinned_logits[:n].copy_(self._d_logits[:n], non_blocking=True)
+        torch.cuda.current_stream(self.device).synchronize()
+        return self._pinned_logits[:n].numpy().copy()

@@ -91,3 +91,23 @@ def test_adaptive_server_runs_on_engine():
     assert len(seen_k) == len(trace)
     assert min(seen_k) >= 2 and max(seen_k) <= 4
     assert metrics.completed == len(trace)
+
+
+def test_sharded_host_path_matches_group_host_path():
+    """ShardedStudentGroup.forward_host (the N-GPU bench's e2e path: pinned staging, forward,
+    logit reduce, D2H) at world size 1 equals StudentGroup.forward_host on the same weights."""
+    from paper_2408_12526_b200 import PRESETS, StudentGroup, random_bert_group
+    from paper_2408_12526_b200.parallel import ShardedStudentGroup
+
+    cfg, K = PRESETS["tiny"]
+    sh = ShardedStudentGroup(cfg, K, seed=4, rank=0, world=1, max_tokens=256, max_seqs=4)
+    ref = StudentGroup(random_bert_group(cfg, K, seed=4), max_tokens=256, max_seqs=4)
+    rng = np.random.default_rng(2)
+    for lens in ([17], [5, 60, 33], [128, 1]):
+        seqs = _seqs(rng, lens)
+        ids = np.concatenate(seqs)
+        cu = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+        for k in (1, K):
+            z = sh.forward_host(ids, cu, k)
+            assert z.shape == (len(lens), 2)
+            np.testing.assert_allclose(z, ref.forward_host(ids, cu, k), rtol=0, atol=1e-5)
