@@ -587,6 +587,10 @@ void gemm_configure_persistent(int t_rows, bool out_f32, int units_per_tile, int
   // units_per_tile / 2 units on n_ctas / 2 pairs.
   const int ctas = pair ? n_ctas / 2 : n_ctas;
   const int upt = pair ? units_per_tile / 2 : units_per_tile;
+  static const int force_bn = [] {  // experiment knob: fixed token-tile width
+    const char* v = getenv("SP_PERSIST_BN");
+    return v ? atoi(v) : 0;
+  }();
   int best_tiles = (t_rows + 255) / 256;
   long long best_cost = 0x7fffffffffffll;
   for (int tiles = (t_rows + 255) / 256; tiles <= (t_rows + 63) / 64; ++tiles) {
@@ -596,7 +600,8 @@ void gemm_configure_persistent(int t_rows, bool out_f32, int units_per_tile, int
     const int x = pair ? b / 2 : b;
     const long long rounds = (upt * (long long)tiles + ctas - 1) / ctas;
     const long long unit = std::max(2LL * b, 3LL * (128 + x)) + 200;
-    const long long cost = rounds * unit;
+    long long cost = rounds * unit;
+    if (force_bn) cost = std::abs(b - force_bn);
     if (cost < best_cost) {
       best_cost = cost;
       best_tiles = tiles;
