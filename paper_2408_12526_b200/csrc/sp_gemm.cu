@@ -487,6 +487,18 @@ __global__ void __launch_bounds__(kPThreads, 1)
         float y[16];
 #pragma unroll
         for (int jj = 0; jj < 16; ++jj) y[jj] = apply_act<ACT>(__uint_as_float(r[jj]) + bias);
+        if (p.direct_store) {
+          // one warp store per token column: 32 consecutive features (64 B fp16 / 128 B fp32)
+          OutT* col = out + (long long)(n0 + c) * p.out_ld + lane;
+#pragma unroll
+          for (int jj = 0; jj < 16; ++jj) {
+            if (jj < n && n0 + c + jj < t_rows) {
+              if constexpr (OUT_F32) col[(long long)jj * p.out_ld] = y[jj];
+              else col[(long long)jj * p.out_ld] = __float2half_rn(y[jj]);
+            }
+          }
+          continue;
+        }
 #pragma unroll
         for (int jj = 0; jj < 16; ++jj) {
           if constexpr (OUT_F32) stage[jj * 32 + lane] = y[jj];

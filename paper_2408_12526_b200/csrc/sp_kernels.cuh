@@ -61,6 +61,7 @@ struct GemmParams {
   int groups;                 // students in the launch (persistent path)
   int l2_prefetch;            // pull the rest of the weight slab into L2 before griddepcontrol.wait
   const int* t_dev;           // if set: live token count (device), t_rows is only the tile bound
+  int direct_store;           // persistent epilogue: warp-wide stores from registers (no smem staging)
 };
 
 // Debug hook: when set, every GEMM launch records a per-CTA timeline into this device buffer.

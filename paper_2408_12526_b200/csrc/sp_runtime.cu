@@ -405,6 +405,11 @@ int run_gemm(sp_group* grp, int kind, const CUtensorMap& wmap, const XMaps& xm, 
     // weights re-read by many token tiles stay in L2 (evict_last); streamed once or twice (batch-1)
     // they must not push the residual stream out (evict_first: -2% at L=512)
     p.w_keep = w_pol >= 0 ? w_pol : (p.n_tiles > 2 ? 2 : 0);
+    static const int direct = [] {
+      const char* v = getenv("SP_PERSIST_DIRECT_STORE");  // measured 2-4% slower than smem staging
+      return v ? atoi(v) : 0;
+    }();
+    p.direct_store = direct;
     p.out = out;
     p.out_group_stride = out_gs;
     p.out_ld = n_out;
