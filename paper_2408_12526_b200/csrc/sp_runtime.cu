@@ -364,12 +364,16 @@ namespace {
 
 // Tensor-core attention (head_dim 64, L <= 512) is opt-in (SP_ATTN_TC=1): it is correct but measured
 // slower than the pipelined mma.sync kernel at every batch-1 length.
+// tcgen05 attention (sp_attn_tc.cu) vs mma.sync attention (sp_attn.cu), by the measured crossover
+// (tools/len_probe.py): tcgen05 wins up to 128 keys and beyond 384 (one CTA per SM: at 160-384 the
+// mma.sync kernel's two CTAs per SM win). SP_ATTN_TC=0 / 1 forces either kernel.
 bool use_attn_tc(int head_dim, int max_len) {
-  static const bool on = [] {
+  static const int mode = [] {
     const char* v = getenv("SP_ATTN_TC");
-    return v != nullptr && atoi(v) != 0;
+    return v == nullptr ? -1 : atoi(v);
   }();
-  return on && head_dim == 64 && max_len <= 512;
+  if (head_dim != 64 || max_len > 512 || mode == 0) return false;
+  return mode > 0 || max_len <= 128 || max_len > 384;
 }
 
 // Launch one grouped projection. Returns the number of kernels launched (1).
