@@ -94,7 +94,8 @@ def _attn_ref(qkv, cu, G, nh, hd):
 
 
 @pytest.mark.parametrize("hd,nh,lens", [(64, 12, [1, 17, 64, 65, 200]), (32, 4, [8, 33, 64, 3]),
-                                         (64, 16, [512, 1, 130])])
+                                         (64, 16, [512, 1, 130]), (64, 8, [100, 1, 128, 37]),
+                                         (64, 12, [416, 385, 3])])
 def test_attention_varlen_matches_torch(cuda_lib, hd, nh, lens):
     from paper_2408_12526_b200 import _lib
 
