@@ -73,6 +73,27 @@ bool make_xmaps(XMaps* m, const void* ptr, uint64_t rows, uint64_t cols) {
 }
 
 int choose_splits(int units, int nkb, int smax) {
+  static const int policy = [] {  // 0: first split with >= 128 CTAs; 1 (default, -2 us at L=128-256): balance the SMs
+    const char* v = getenv("SP_SPLIT_POLICY");
+    return v ? atoi(v) : 1;
+  }();
+  if (policy == 1) {
+    // makespan in k-blocks of the busiest CTA slot: ceil(units * s / slots) waves of nkb / s each
+    int best = 1;
+    long long best_cost = 0x7fffffffffffll;
+    for (int s = 1; s <= smax; ++s) {
+      if (nkb % s || (s > 1 && nkb / s < 2)) continue;
+      const long long ctas = (long long)units * s;
+      // per-SM load: CTAs per SM (ceil over the 148 SMs) x k-blocks each, + partial-sum traffic
+      const long long per_sm = (ctas + 147) / 148;
+      const long long cost = per_sm * (nkb / s) * 4 + s;
+      if (cost < best_cost) {
+        best_cost = cost;
+        best = s;
+      }
+    }
+    return best;
+  }
   int best = 1;
   for (int s = 1; s <= smax; ++s) {
     if (nkb % s) continue;
