@@ -77,7 +77,7 @@ int choose_splits(int units, int nkb, int smax) {
     const char* v = getenv("SP_SPLIT_POLICY");
     return v ? atoi(v) : 1;
   }();
-  if (policy == 1) {
+  if (policy == 1 && units < 148) {  // with >= 1 tile per SM the one-split persistent path wins
     // makespan in k-blocks of the busiest CTA slot: ceil(units * s / slots) waves of nkb / s each
     int best = 1;
     long long best_cost = 0x7fffffffffffll;
@@ -402,8 +402,8 @@ int run_gemm(sp_group* grp, int kind, const CUtensorMap& wmap, const XMaps& xm, 
              int t_rows, int x_group_rows, const float* bias, int bias_gs, int act, void* out, long long out_gs,
              int out_f32, int splits, long long split_stride, cudaStream_t st, const int* t_dev = nullptr) {
   static const int persist_min_rows = [] {
-    const char* v = getenv("SP_GEMM_PERSIST_MIN_ROWS");  // tuning knob; default: beyond one 128-token tile
-    return v ? atoi(v) : 129;
+    const char* v = getenv("SP_GEMM_PERSIST_MIN_ROWS");  // one-split projections from 17 tokens on: measured
+    return v ? atoi(v) : 17;                                 // equal or 2-4 us faster than the small-T kernel
   }();
   static const int l2_prefetch = [] {
     const char* v = getenv("SP_GEMM_L2PREFETCH");  // measured neutral-to-slower: opt-in
