@@ -30,8 +30,7 @@ __global__ void __launch_bounds__(32 * NW, MINB)
   half* sV = sK + NBUF * BK * LD;  // [NBUF][BK][LD]
 
   prefetch_share_l2(pf_ptr, pf_bytes);  // next projection's weights, while attention runs
-  pdl_wait();
-  pdl_launch_dependents();
+  pdl_enter();
   const int b = blockIdx.y;
   const int s0 = __ldg(cu + b);
   const int L = __ldg(cu + b + 1) - s0;
@@ -267,5 +266,7 @@ void launch_attention(const half* qkv, half* ctx, const int* cu_seqlens, int n_s
 #undef SP_ATTN
 #undef SP_ATTN_B
 }
+
+void attn_set_early_trigger(int v) { set_early_trigger_tu(v); }
 
 }  // namespace sp

@@ -32,7 +32,13 @@ namespace sp {
 static constexpr int kBlockM = 128;
 static constexpr int kBlockK = 64;                         // one 128-byte swizzle row of fp16
 static constexpr int kATileBytes = kBlockM * kBlockK * 2;  // 16 KiB
-static constexpr int kTmemCols = 256;                      // bn <= 256 fp32 columns
+// TMEM columns of the small-T kernel: the next power of two >= bn (>= 32), so that CTAs of the next
+// projection, launched early (PDL), can allocate theirs while this one still runs (512 per SM)
+__device__ __forceinline__ uint32_t tmem_cols_for(int bn) {
+  uint32_t c = 32;
+  while (c < static_cast<uint32_t>(bn)) c <<= 1;
+  return c;
+}
 static constexpr int kEpiWarps = 8;
 static constexpr int kThreads = 64 + 32 * kEpiWarps;
 static constexpr int kMaxBn = 256;
@@ -75,7 +81,14 @@ __global__ void __launch_bounds__(kThreads, 2)
   const int lane = lane_id();
   unsigned long long* tr = p.trace ? p.trace + 8ull * (blockIdx.y * gridDim.x + blockIdx.x) : nullptr;
   if (tr && threadIdx.x == 0) tr[0] = globaltimer();
+  // Release the next kernel at once: its CTAs become resident (as resources allow) and start their
+  // own weight prefetch while this one runs; they griddepcontrol.wait before reading our output.
+  pdl_launch_dependents();
 
+  // weights: streamed once per request -> evict_first, unless several token tiles re-read them
+  const uint64_t pol_w = (p.n_tiles > 1 && p.w_keep) ? policy_evict_last() : policy_evict_first();
+  const int wrow = g * p.n_out + m0;
+  const int n_pre = min(p.stages, kb1 - kb0);
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < p.stages; ++s) {
       mbar_init(&full[s], 1);
@@ -86,9 +99,20 @@ __global__ void __launch_bounds__(kThreads, 2)
     tma_prefetch_desc(&map_w);
     tma_prefetch_desc(&map_x64);
     tma_prefetch_desc(&map_x16);
+    if (!pair) {
+      // 1) weight prefetch: independent of the previous kernel and of the TMEM allocation below
+      //    (which waits while an earlier kernel on this SM still holds the columns). The first
+      //    stages go straight to smem; the rest of this CTA's slab optionally into L2.
+      for (int i = 0; i < n_pre; ++i) {
+        mbar_arrive_expect_tx(&full[i], stage_bytes);
+        tma_load_2d(&map_w, &full[i], smem + i * stage_bytes, (kb0 + i) * kBlockK, wrow, pol_w);
+      }
+      if (p.l2_prefetch)
+        for (int kb = kb0 + n_pre; kb < kb1; ++kb) tma_prefetch_l2_2d(&map_w, kb * kBlockK, wrow);
+    }
   }
   if (warp == 1) {
-    tmem_alloc(tmem_slot, kTmemCols);
+    tmem_alloc(tmem_slot, tmem_cols_for(p.bn));
     tmem_relinquish();
   }
   tc_fence_before();
@@ -96,15 +120,11 @@ __global__ void __launch_bounds__(kThreads, 2)
   if (pair) cluster_sync();  // peer barriers initialised before any multicast lands in them
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  pdl_launch_dependents();
   if (tr && threadIdx.x == 0) tr[1] = globaltimer();
 
   if (warp == 0) {
     if (elect_one()) {
-      // weights: streamed once per request -> evict_first, unless several token tiles re-read them
-      const uint64_t pol_w = (p.n_tiles > 1 && p.w_keep) ? policy_evict_last() : policy_evict_first();
       const uint64_t pol_x = policy_evict_last();   // activations: re-read by every M tile
-      const int wrow = g * p.n_out + m0;
       const int xrow = g * p.x_group_rows + n0;
       // token tile: alone, or (pair) this CTA's half multicast into both CTAs of the cluster
       const int r_begin = pair ? static_cast<int>(crank) * (p.bn >> 1) : 0;
@@ -122,16 +142,12 @@ __global__ void __launch_bounds__(kThreads, 2)
           for (; r < r_end; r += 16) tma_load_2d(&map_x16, &full[s], sb + r * 128, kc, xrow + r, pol_x);
         }
       };
-      // 1) weight prefetch: independent of the previous kernel. The first stages go straight to
-      //    smem; the rest of this CTA's weight slab is pulled into L2 so the HBM stream continues
-      //    across the kernel boundary while the previous kernel finishes.
-      const int n_pre = min(p.stages, kb1 - kb0);
-      for (int i = 0; i < n_pre; ++i) {
-        mbar_arrive_expect_tx(&full[i], stage_bytes);
-        tma_load_2d(&map_w, &full[i], smem + i * stage_bytes, (kb0 + i) * kBlockK, wrow, pol_w);
+      if (pair) {  // (pair: the peer's barriers are initialised only after cluster_sync)
+        for (int i = 0; i < n_pre; ++i) {
+          mbar_arrive_expect_tx(&full[i], stage_bytes);
+          tma_load_2d(&map_w, &full[i], smem + i * stage_bytes, (kb0 + i) * kBlockK, wrow, pol_w);
+        }
       }
-      if (p.l2_prefetch)
-        for (int kb = kb0 + n_pre; kb < kb1; ++kb) tma_prefetch_l2_2d(&map_w, kb * kBlockK, wrow);
       if (tr) tr[2] = globaltimer();
       // 2) activations are produced by the previous kernel
       pdl_wait();
@@ -148,6 +164,7 @@ __global__ void __launch_bounds__(kThreads, 2)
           ph ^= 1;
         }
       }
+      if (p.progress && nt == 0) atomicAdd(p.progress, (unsigned long long)(kb1 - kb0) * kATileBytes);
       if (tr) tr[3] = globaltimer();
     }
   } else if (warp == 1) {
@@ -180,9 +197,9 @@ __global__ void __launch_bounds__(kThreads, 2)
     __syncwarp();
   } else {
     // ---------------------------------------------------------------- epilogue
-    const int e = warp - 2;  // 0..7
+    const int e = warp - 2;  // 0..epi_warps-1
     const int q = warp & 3;  // TMEM lane quadrant (hardware: warp w accesses lanes 32*(w%4)..)
-    const int half_cols = p.bn >> 1;
+    const int half_cols = p.epi_warps == 8 ? (p.bn >> 1) : p.bn;  // 4 warps: every column
     const int c_begin = (e >> 2) * half_cols;
     const int feat = m0 + q * 32 + lane;
     const bool partial = p.splits > 1;
@@ -244,7 +261,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   if (pair) cluster_sync();  // no CTA leaves while its peer may still signal its barriers
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem, kTmemCols);
+    tmem_dealloc(tmem, tmem_cols_for(p.bn));
   }
 }
 
@@ -395,6 +412,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
             ph ^= 1;
           }
         }
+        if (p.progress && nt == 0) atomicAdd(p.progress, (unsigned long long)nkb * kATileBytes);  // one count per slab
       }
       if (first) pdl_wait();  // no work: still honour the dependency
     }
@@ -716,7 +734,7 @@ static void launch_gemm_t(const GemmMaps& maps, const GemmParams& p, int groups,
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(p.m_tiles * p.n_tiles * p.splits, groups);
-  cfg.blockDim = dim3(kThreads);
+  cfg.blockDim = dim3(64 + 32 * p.epi_warps);
   cfg.dynamicSmemBytes = gemm_smem_bytes(p.bn, p.stages);
   cfg.stream = stream;
   cudaLaunchAttribute attr[2];
@@ -735,6 +753,13 @@ static void launch_gemm_t(const GemmMaps& maps, const GemmParams& p, int groups,
     g_trace_counts.push_back(static_cast<int>(cfg.gridDim.x * cfg.gridDim.y));
   }
   cudaLaunchKernelEx(&cfg, gemm_kernel<ACT, OUT_F32>, maps.w, maps.x64, maps.x16, q);
+}
+
+// Epilogue warps of the small-T kernel: 4 for narrow token tiles (192 threads: with 32-column TMEM
+// and fewer stages, CTAs of the next projection fit beside this one's), else 8.
+int gemm_epi_warps(int bn) {
+  static const int max_bn4 = env_int("SP_GEMM_EPI4_MAXBN", 32, 0, 256);
+  return bn <= max_bn4 ? 4 : 8;
 }
 
 void launch_gemm(const GemmMaps& maps, const GemmParams& p, int groups, cudaStream_t stream) {

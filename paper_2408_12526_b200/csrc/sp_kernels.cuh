@@ -62,7 +62,28 @@ struct GemmParams {
   int l2_prefetch;            // pull the rest of the weight slab into L2 before griddepcontrol.wait
   const int* t_dev;           // if set: live token count (device), t_rows is only the tile bound
   int direct_store;           // persistent epilogue: warp-wide stores from registers (no smem staging)
+  int epi_warps;              // small-T kernel: 4 or 8 epilogue warps (gemm_epi_warps)
+  unsigned long long* progress;  // weight streamer pacing (sp_stream.cu): += weight bytes requested, or null
 };
+
+// Weight streamer (sp_stream.cu): L2 prefetch of a request's projection weights in consumption
+// order on a side branch, paced against GemmParams.progress.
+constexpr int kStreamMaxSegs = 24;
+struct StreamPlan {
+  const void* ptr[kStreamMaxSegs];
+  unsigned long long bytes[kStreamMaxSegs];
+  int n;
+  unsigned long long skip;    // leading bytes the chain loads itself (first projection)
+  unsigned long long window;  // max bytes prefetched ahead of the projections' progress
+  unsigned long long total;   // progress the request's projections add (sum of bytes)
+  unsigned long long chunk;   // bytes per bulk prefetch
+  unsigned long long max_wait_ns;
+};
+void launch_weight_stream(const StreamPlan& plan, unsigned long long* state, int ctas, cudaStream_t stream);
+
+// SP_EARLY_TRIGGER: row / attention kernels release their dependents before the dependency wait.
+void rowops_set_early_trigger(int v);
+void attn_set_early_trigger(int v);
 
 // Debug hook: when set, every GEMM launch records a per-CTA timeline into this device buffer.
 void set_gemm_trace(unsigned long long* buf);
@@ -101,6 +122,7 @@ void gemm_configure_persistent(int t_rows, bool out_f32, int units_per_tile, int
 int sm_count();
 size_t gemm_smem_bytes(int bn, int stages);
 void gemm_configure_tiles(int t_rows, bool cluster2, int* bn, int* n_tiles, int* stages);
+int gemm_epi_warps(int bn);
 
 // Unpadded multi-head attention over cu_seqlens-packed sequences.
 //   qkv: fp16 [groups][x_group_rows][3H] (Q | K | V, head h at columns h*D within each third)

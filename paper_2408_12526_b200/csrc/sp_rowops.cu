@@ -18,8 +18,7 @@ __global__ void __launch_bounds__(128)
                     const float* __restrict__ beta, int hidden, float eps, float* x32, half* x16, long long x_gs,
                     const void* pf_ptr, unsigned long long pf_bytes) {
   prefetch_share_l2(pf_ptr, pf_bytes);
-  pdl_wait();
-  pdl_launch_dependents();
+  pdl_enter();
   const int t = blockIdx.x * 4 + warp_id();
   if (n_tokens < 0) n_tokens = __ldg(cu + n_seqs);  // graph replay: live count = cu_seqlens[n_seqs]
   if (t >= n_tokens) return;
@@ -64,8 +63,7 @@ __global__ void __launch_bounds__(128)
                      const int* __restrict__ cu, int n_seqs, half* cls16, long long cls_gs, const void* pf_ptr,
                      unsigned long long pf_bytes) {
   prefetch_share_l2(pf_ptr, pf_bytes);
-  pdl_wait();
-  pdl_launch_dependents();
+  pdl_enter();
   const int t = blockIdx.x * 4 + warp_id();
   if (n_tokens < 0) n_tokens = __ldg(cu + n_seqs);
   if (t >= n_tokens) return;
@@ -117,8 +115,7 @@ __global__ void __launch_bounds__(1024)
                 const float* __restrict__ b_pool, int groups, const float* __restrict__ alpha,
                 const float* __restrict__ w_cls, const float* __restrict__ b_cls, int n_classes, int hidden,
                 int add_bias, float* __restrict__ rep, float* __restrict__ logits, float* __restrict__ finals) {
-  pdl_wait();
-  pdl_launch_dependents();
+  pdl_enter();
   __shared__ float red[32][4];
   const int b = blockIdx.x;
   const int j = threadIdx.x;
@@ -262,8 +259,7 @@ __global__ void __launch_bounds__(1024)
     prefix_logits_kernel(const float* __restrict__ finals, int groups, const float* __restrict__ alpha,
                          const float* __restrict__ w_cls, const float* __restrict__ b_cls, int n_classes,
                          int hidden, int add_bias, float* __restrict__ out) {
-  pdl_wait();
-  pdl_launch_dependents();
+  pdl_enter();
   __shared__ float red[32][4];
   const int b = blockIdx.x;
   const int j = threadIdx.x;
@@ -303,5 +299,7 @@ void launch_prefix_logits(const float* finals, int groups, const float* alpha, c
   launch_pdl(prefix_logits_kernel, dim3(n_rows), dim3(threads), 0, stream, finals, groups, alpha, w_cls, b_cls,
              n_classes, hidden, add_bias, out);
 }
+
+void rowops_set_early_trigger(int v) { set_early_trigger_tu(v); }
 
 }  // namespace sp

@@ -51,6 +51,11 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 // fp16 row-major [rows, cols] viewed as a 2-D tensor map with a {64, box_rows} box, 128-B swizzle.
+int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v ? atoi(v) : dflt;
+}
+
 bool make_map(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols, uint32_t box_rows) {
   auto fn = encode_fn();
   if (fn == nullptr || ptr == nullptr || rows == 0) return false;
@@ -131,6 +136,11 @@ struct sp_group {
   float* h_logits = nullptr;   // pinned logits landing buffer
   float* d_logits = nullptr;
   int* mlp_done = nullptr;  // fused FFN kernel: FFN1 tiles finished per student + exit counter
+  // weight streamer (sp_stream.cu): [progress, base, finished CTAs], side stream + fork/join events
+  unsigned long long* ws_state = nullptr;
+  unsigned long long* ws_active = nullptr;  // = ws_state while a streamed forward is being launched
+  cudaStream_t ws_stream = nullptr;
+  cudaEvent_t ws_fork = nullptr, ws_join = nullptr;
   std::vector<void*> allocs;
   // tensor maps
   std::vector<CUtensorMap> m_qkv, m_o, m_f1, m_f2, m_layers;
@@ -202,6 +212,9 @@ int dev_alloc(sp_group* g, T** p, size_t count) {
 
 void free_all(sp_group* g) {
   for (auto& kv : g->graphs) cudaGraphExecDestroy(kv.second);
+  if (g->ws_stream) cudaStreamDestroy(g->ws_stream);
+  if (g->ws_fork) cudaEventDestroy(g->ws_fork);
+  if (g->ws_join) cudaEventDestroy(g->ws_join);
   g->graphs.clear();
   if (g->cap_stream) cudaStreamDestroy(g->cap_stream);
   g->cap_stream = nullptr;
@@ -283,6 +296,17 @@ int sp_group_create(const sp_config* cfg, const sp_weights* weights, int device,
   if ((rc = dev_alloc(g, &g->mlp_done, sp::kReqMaxStudents + 1))) return bail(rc);
   if (cudaMemset(g->mlp_done, 0, sizeof(int) * (sp::kReqMaxStudents + 1)) != cudaSuccess)
     return bail(fail(SP_ECUDA, "memset"));
+  {
+    static const int early = env_int("SP_EARLY_TRIGGER", 0);
+    sp::rowops_set_early_trigger(early);
+    sp::attn_set_early_trigger(early);
+  }
+  if ((rc = dev_alloc(g, &g->ws_state, 4))) return bail(rc);
+  if (cudaMemset(g->ws_state, 0, 4 * sizeof(unsigned long long)) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&g->ws_stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&g->ws_fork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&g->ws_join, cudaEventDisableTiming) != cudaSuccess)
+    return bail(fail(SP_ECUDA, "weight streamer state"));
 
   if (c.kind == SP_KIND_BERT) {
     if (!w.word_emb || !w.pos_emb || !w.type_emb || !w.emb_ln_gamma || !w.emb_ln_beta || !w.w_qkv || !w.b_qkv ||
@@ -411,6 +435,7 @@ int run_gemm(sp_group* grp, int kind, const CUtensorMap& wmap, const XMaps& xm, 
   }();
   if (splits == 1 && t_rows >= persist_min_rows) {
     sp::GemmParams p{};
+    p.progress = grp ? grp->ws_active : nullptr;
     p.l2_prefetch = l2_prefetch;
     p.t_dev = t_dev;
     p.n_out = n_out;
@@ -457,6 +482,7 @@ int run_gemm(sp_group* grp, int kind, const CUtensorMap& wmap, const XMaps& xm, 
     return 1;
   }
   sp::GemmParams p{};
+  p.progress = grp ? grp->ws_active : nullptr;
   p.l2_prefetch = l2_prefetch;
   p.t_dev = t_dev;
   p.n_out = n_out;
@@ -475,6 +501,7 @@ int run_gemm(sp_group* grp, int kind, const CUtensorMap& wmap, const XMaps& xm, 
   }();
   p.w_keep = w_keep;
   sp::gemm_configure_tiles(t_rows, p.cluster == 2, &p.bn, &p.n_tiles, &p.stages);
+  p.epi_warps = sp::gemm_epi_warps(p.bn);
   p.splits = splits;
   p.kb_per_split = (k_dim / 64) / splits;
   p.out = out;
@@ -718,6 +745,55 @@ int run_mlp(sp_group* g, int l, int k, int n_tokens, const int* t_dev, cudaStrea
 
 // dyn = true (graph capture): n_tokens / max_len are bucket bounds used for grids and tiles; every
 // kernel reads the live token count from cu_seqlens[n_seqs] on the device.
+// Weight streamer for short requests (see sp_stream.cu). Only where every projection of the request
+// reports its progress: the small-T and persistent GEMMs (not the fused MLP / LN / request kernels).
+bool weight_stream_on(const sp_group* g, int n_tokens, int k) {
+  static const int max_tokens = env_int("SP_WS_MAX_TOKENS", 0);
+  static const bool ln_fused = env_int("SP_LN_FUSE", 0) != 0;
+  return k > 0 && n_tokens <= max_tokens && n_tokens <= 128 && !ln_fused && !fused_enabled() &&
+         4 * g->cfg.n_layers + 1 <= sp::kStreamMaxSegs;
+}
+
+int weight_stream_begin(sp_group* g, int k, cudaStream_t st) {
+  static const unsigned long long window = (unsigned long long)env_int("SP_WS_WINDOW_MB", 64) << 20;
+  static const unsigned long long chunk = (unsigned long long)env_int("SP_WS_CHUNK_KB", 64) << 10;
+  static const int ctas = env_int("SP_WS_CTAS", 16);
+  static const bool skip_first = env_int("SP_WS_SKIP_FIRST", 1) != 0;
+  const sp_config& c = g->cfg;
+  const sp_weights& w = g->w;
+  const size_t S = c.n_students, H = c.hidden, F = c.ffn;
+  sp::StreamPlan plan{};
+  auto seg = [&](const void* base, size_t layer_elems, size_t l, size_t per_student) {
+    plan.ptr[plan.n] = static_cast<const half*>(base) + l * layer_elems;
+    plan.bytes[plan.n] = (unsigned long long)k * per_student * 2;
+    plan.total += plan.bytes[plan.n];
+    ++plan.n;
+  };
+  for (int l = 0; l < c.n_layers; ++l) {
+    seg(w.w_qkv, S * 3 * H * H, l, 3 * H * H);
+    seg(w.w_o, S * H * H, l, H * H);
+    seg(w.w_ffn1, S * F * H, l, F * H);
+    seg(w.w_ffn2, S * H * F, l, H * F);
+  }
+  seg(w.w_pool, 0, 0, H * H);
+  plan.skip = skip_first ? plan.bytes[0] : 0;
+  plan.window = window;
+  plan.chunk = chunk;
+  plan.max_wait_ns = 2000000ull;
+  SP_CUDA(cudaEventRecord(g->ws_fork, st));
+  SP_CUDA(cudaStreamWaitEvent(g->ws_stream, g->ws_fork, 0));
+  sp::launch_weight_stream(plan, g->ws_state, ctas, g->ws_stream);
+  SP_CUDA(cudaEventRecord(g->ws_join, g->ws_stream));
+  g->ws_active = g->ws_state;
+  return SP_OK;
+}
+
+int weight_stream_end(sp_group* g, cudaStream_t st) {
+  g->ws_active = nullptr;
+  SP_CUDA(cudaStreamWaitEvent(st, g->ws_join, 0));
+  return SP_OK;
+}
+
 int bert_forward(sp_group* g, const int32_t* ids, const int32_t* cu, int n_seqs, int n_tokens, int max_len, int k,
                  float* rep, float* logits, int add_bias, cudaStream_t st, bool dyn = false) {
   const int n_rows_arg = dyn ? -n_tokens : n_tokens;  // row kernels: negative = live count on device
@@ -747,6 +823,11 @@ int bert_forward(sp_group* g, const int32_t* ids, const int32_t* cu, int n_seqs,
   }
   g->rec_reset(st);
   const double GTH = (double)k * n_tokens * H;
+  const bool ws = weight_stream_on(g, n_tokens, k);
+  if (ws) {
+    const int rc = weight_stream_begin(g, k, st);
+    if (rc) return rc;
+  }
   if (k > 0) {
     g->rec_begin(SP_LAUNCH_EMBED_LN, GTH * 10.0, 0.0);
     sp::launch_embed_ln(ids, cu, n_seqs, n_rows_arg, k, static_cast<const half*>(w.word_emb),
@@ -833,6 +914,11 @@ int bert_forward(sp_group* g, const int32_t* ids, const int32_t* cu, int n_seqs,
                   add_bias, rep, logits, st, g->eval_finals);
   g->rec_end();
   ++launches;
+  if (ws) {
+    const int rc = weight_stream_end(g, st);
+    if (rc) return rc;
+    ++launches;
+  }
   if (g->eval_prefix) {
     sp::launch_prefix_logits(g->eval_finals, k, w.alpha, w.w_cls, w.b_cls, c.n_classes, H, n_seqs, add_bias,
                              g->eval_prefix, st);
