@@ -224,7 +224,9 @@ void launch_attention(const half* qkv, half* ctx, const int* cu_seqlens, int n_s
     const char* v = getenv("SP_ATTN_NW");
     return v ? atoi(v) : 0;
   }();
-  const int nw = nw_env ? nw_env : (max_len <= 128 ? 4 : (max_len <= 288 ? 6 : 8));  // measured sweep
+  // measured sweep (tools/attn_bench.py); 385..448: 64-query tiles at 4 CTAs/SM balance the waves
+  // that 128-query tiles quantize (4 tiles per head), 26 vs 29 us
+  const int nw = nw_env ? nw_env : (max_len <= 128 ? 4 : (max_len <= 288 ? 6 : (max_len <= 384 ? 8 : 4)));
   // resident CTAs per SM (register cap): SP_ATTN_MINB overrides the default (4 for 4 warps, else 2)
   static const int minb_env = [] {
     const char* v = getenv("SP_ATTN_MINB");
@@ -266,7 +268,5 @@ void launch_attention(const half* qkv, half* ctx, const int* cu_seqlens, int n_s
 #undef SP_ATTN
 #undef SP_ATTN_B
 }
-
-void attn_set_early_trigger(int v) { set_early_trigger_tu(v); }
 
 }  // namespace sp

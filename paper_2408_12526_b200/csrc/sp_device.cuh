@@ -6,16 +6,13 @@
 
 namespace sp {
 
-// PDL entry of the row / attention kernels. With c_early_trigger (SP_EARLY_TRIGGER, per translation
-// unit, set at group creation) the dependents are released before the dependency wait, so the next
-// projection's CTAs can become resident and prefetch their weights while this kernel still waits.
-static __constant__ int c_early_trigger;
+// PDL entry of the row / attention kernels: wait for the producer, then release the next kernel.
+// (Releasing before the wait, so the next projection's CTAs prefetch earlier, measured no faster;
+// DESIGN.md section 7.)
 __device__ __forceinline__ void pdl_enter() {
-  if (c_early_trigger) pdl_launch_dependents();
   pdl_wait();
   pdl_launch_dependents();
 }
-static inline void set_early_trigger_tu(int v) { cudaMemcpyToSymbol(c_early_trigger, &v, sizeof(int)); }
 
 __device__ __forceinline__ void mma_16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
   asm volatile(

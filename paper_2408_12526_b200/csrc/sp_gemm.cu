@@ -81,14 +81,6 @@ __global__ void __launch_bounds__(kThreads, 2)
   const int lane = lane_id();
   unsigned long long* tr = p.trace ? p.trace + 8ull * (blockIdx.y * gridDim.x + blockIdx.x) : nullptr;
   if (tr && threadIdx.x == 0) tr[0] = globaltimer();
-  // Release the next kernel at once: its CTAs become resident (as resources allow) and start their
-  // own weight prefetch while this one runs; they griddepcontrol.wait before reading our output.
-  pdl_launch_dependents();
-
-  // weights: streamed once per request -> evict_first, unless several token tiles re-read them
-  const uint64_t pol_w = (p.n_tiles > 1 && p.w_keep) ? policy_evict_last() : policy_evict_first();
-  const int wrow = g * p.n_out + m0;
-  const int n_pre = min(p.stages, kb1 - kb0);
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < p.stages; ++s) {
       mbar_init(&full[s], 1);
@@ -99,17 +91,6 @@ __global__ void __launch_bounds__(kThreads, 2)
     tma_prefetch_desc(&map_w);
     tma_prefetch_desc(&map_x64);
     tma_prefetch_desc(&map_x16);
-    if (!pair) {
-      // 1) weight prefetch: independent of the previous kernel and of the TMEM allocation below
-      //    (which waits while an earlier kernel on this SM still holds the columns). The first
-      //    stages go straight to smem; the rest of this CTA's slab optionally into L2.
-      for (int i = 0; i < n_pre; ++i) {
-        mbar_arrive_expect_tx(&full[i], stage_bytes);
-        tma_load_2d(&map_w, &full[i], smem + i * stage_bytes, (kb0 + i) * kBlockK, wrow, pol_w);
-      }
-      if (p.l2_prefetch)
-        for (int kb = kb0 + n_pre; kb < kb1; ++kb) tma_prefetch_l2_2d(&map_w, kb * kBlockK, wrow);
-    }
   }
   if (warp == 1) {
     tmem_alloc(tmem_slot, tmem_cols_for(p.bn));
@@ -120,11 +101,15 @@ __global__ void __launch_bounds__(kThreads, 2)
   if (pair) cluster_sync();  // peer barriers initialised before any multicast lands in them
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_launch_dependents();
   if (tr && threadIdx.x == 0) tr[1] = globaltimer();
 
   if (warp == 0) {
     if (elect_one()) {
+      // weights: streamed once per request -> evict_first, unless several token tiles re-read them
+      const uint64_t pol_w = (p.n_tiles > 1 && p.w_keep) ? policy_evict_last() : policy_evict_first();
       const uint64_t pol_x = policy_evict_last();   // activations: re-read by every M tile
+      const int wrow = g * p.n_out + m0;
       const int xrow = g * p.x_group_rows + n0;
       // token tile: alone, or (pair) this CTA's half multicast into both CTAs of the cluster
       const int r_begin = pair ? static_cast<int>(crank) * (p.bn >> 1) : 0;
@@ -142,12 +127,15 @@ __global__ void __launch_bounds__(kThreads, 2)
           for (; r < r_end; r += 16) tma_load_2d(&map_x16, &full[s], sb + r * 128, kc, xrow + r, pol_x);
         }
       };
-      if (pair) {  // (pair: the peer's barriers are initialised only after cluster_sync)
-        for (int i = 0; i < n_pre; ++i) {
-          mbar_arrive_expect_tx(&full[i], stage_bytes);
-          tma_load_2d(&map_w, &full[i], smem + i * stage_bytes, (kb0 + i) * kBlockK, wrow, pol_w);
-        }
+      // 1) weight prefetch: independent of the previous kernel. The first stages go straight to
+      //    smem; the rest of this CTA's weight slab is optionally pulled into L2.
+      const int n_pre = min(p.stages, kb1 - kb0);
+      for (int i = 0; i < n_pre; ++i) {
+        mbar_arrive_expect_tx(&full[i], stage_bytes);
+        tma_load_2d(&map_w, &full[i], smem + i * stage_bytes, (kb0 + i) * kBlockK, wrow, pol_w);
       }
+      if (p.l2_prefetch)
+        for (int kb = kb0 + n_pre; kb < kb1; ++kb) tma_prefetch_l2_2d(&map_w, kb * kBlockK, wrow);
       if (tr) tr[2] = globaltimer();
       // 2) activations are produced by the previous kernel
       pdl_wait();
@@ -586,6 +574,8 @@ static void launch_persistent_t(const GemmMaps& maps, const GemmParams& p, int g
   attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
+  prefer_max_smem(q.cluster == 2 ? reinterpret_cast<const void*>(gemm_persistent_kernel<ACT, OUT_F32, true>)
+                                  : reinterpret_cast<const void*>(gemm_persistent_kernel<ACT, OUT_F32, false>));
   if (q.cluster == 2) cudaLaunchKernelEx(&cfg, gemm_persistent_kernel<ACT, OUT_F32, true>, maps.w, maps.x64, maps.x16, q);
   else cudaLaunchKernelEx(&cfg, gemm_persistent_kernel<ACT, OUT_F32, false>, maps.w, maps.x64, maps.x16, q);
 }
@@ -752,6 +742,7 @@ static void launch_gemm_t(const GemmMaps& maps, const GemmParams& p, int groups,
     g_trace_used += (size_t)cfg.gridDim.x * cfg.gridDim.y;
     g_trace_counts.push_back(static_cast<int>(cfg.gridDim.x * cfg.gridDim.y));
   }
+  prefer_max_smem(reinterpret_cast<const void*>(gemm_kernel<ACT, OUT_F32>));
   cudaLaunchKernelEx(&cfg, gemm_kernel<ACT, OUT_F32>, maps.w, maps.x64, maps.x16, q);
 }
 

@@ -273,6 +273,7 @@ void launch_gemm_ln(const GemmMaps& maps, const GemmParams& p, const LnParams& l
   attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
+  prefer_max_smem(reinterpret_cast<const void*>(gemm_ln_kernel));
   cudaLaunchKernelEx(&cfg, gemm_ln_kernel, maps.w, maps.x64, maps.x16, p, ln);
 }
 

@@ -9,6 +9,11 @@
 
 namespace sp {
 
+// Every kernel of the library runs with the same (maximum) shared-memory carveout, so the SM's
+// L1/shared split never changes between consecutive kernels of the chain (SP_CARVEOUT=-1: driver
+// default per kernel). Set once per kernel; defined in sp_runtime.cu.
+void prefer_max_smem(const void* fn);
+
 // Launch with programmatic stream serialization: the kernel may start while its predecessor in
 // the stream finishes; every kernel of this library calls griddepcontrol.wait before touching
 // data the predecessor produces (and only prefetches read-only weights before that).
@@ -25,6 +30,7 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  prefer_max_smem(reinterpret_cast<const void*>(kernel));
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
@@ -80,10 +86,6 @@ struct StreamPlan {
   unsigned long long max_wait_ns;
 };
 void launch_weight_stream(const StreamPlan& plan, unsigned long long* state, int ctas, cudaStream_t stream);
-
-// SP_EARLY_TRIGGER: row / attention kernels release their dependents before the dependency wait.
-void rowops_set_early_trigger(int v);
-void attn_set_early_trigger(int v);
 
 // Debug hook: when set, every GEMM launch records a per-CTA timeline into this device buffer.
 void set_gemm_trace(unsigned long long* buf);

@@ -837,6 +837,7 @@ bool launch_request_t(const ReqMaps& m, const ReqParams& p, int grid, cudaStream
   attrs[0].val.cooperative = 1;
   cfg.attrs = attrs;
   cfg.numAttrs = 1;
+  prefer_max_smem(reinterpret_cast<const void*>(request_kernel<NC, D>));
   return cudaLaunchKernelEx(&cfg, request_kernel<NC, D>, m, q) == cudaSuccess;
 }
 

@@ -300,6 +300,4 @@ void launch_prefix_logits(const float* finals, int groups, const float* alpha, c
              n_classes, hidden, add_bias, out);
 }
 
-void rowops_set_early_trigger(int v) { set_early_trigger_tu(v); }
-
 }  // namespace sp

@@ -4,6 +4,8 @@
 
 #include <algorithm>
 #include <map>
+#include <mutex>
+#include <unordered_set>
 #include <tuple>
 #include <cstdarg>
 #include <cstdio>
@@ -113,6 +115,17 @@ constexpr int kMaxSplits = 4;
 static_assert(sp::kReqMaxSplit <= kMaxSplits, "request-kernel partials live in the split-K buffers");
 
 }  // namespace
+
+namespace sp {
+void prefer_max_smem(const void* fn) {
+  static const int carveout = env_int("SP_CARVEOUT", -1);
+  static std::mutex mu;
+  static std::unordered_set<const void*> done;
+  if (carveout < 0) return;
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.insert(fn).second) cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, carveout);
+}
+}  // namespace sp
 
 struct sp_group {
   sp_config cfg;
@@ -296,11 +309,6 @@ int sp_group_create(const sp_config* cfg, const sp_weights* weights, int device,
   if ((rc = dev_alloc(g, &g->mlp_done, sp::kReqMaxStudents + 1))) return bail(rc);
   if (cudaMemset(g->mlp_done, 0, sizeof(int) * (sp::kReqMaxStudents + 1)) != cudaSuccess)
     return bail(fail(SP_ECUDA, "memset"));
-  {
-    static const int early = env_int("SP_EARLY_TRIGGER", 0);
-    sp::rowops_set_early_trigger(early);
-    sp::attn_set_early_trigger(early);
-  }
   if ((rc = dev_alloc(g, &g->ws_state, 4))) return bail(rc);
   if (cudaMemset(g->ws_state, 0, 4 * sizeof(unsigned long long)) != cudaSuccess ||
       cudaStreamCreateWithFlags(&g->ws_stream, cudaStreamNonBlocking) != cudaSuccess ||
@@ -418,7 +426,7 @@ bool use_attn_tc(int head_dim, int max_len) {
     return v == nullptr ? -1 : atoi(v);
   }();
   if (head_dim != 64 || max_len > 512 || mode == 0) return false;
-  return mode > 0 || max_len <= 128 || max_len > 384;
+  return mode > 0 || max_len <= 128 || max_len > 448;  // 385..448: 4-warp mma.sync tiles, 4 CTAs/SM
 }
 
 // Launch one grouped projection. Returns the number of kernels launched (1).

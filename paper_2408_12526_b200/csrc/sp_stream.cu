@@ -67,6 +67,7 @@ __global__ void __launch_bounds__(32) weight_stream_kernel(const __grid_constant
 }
 
 void launch_weight_stream(const StreamPlan& plan, unsigned long long* state, int ctas, cudaStream_t stream) {
+  prefer_max_smem(reinterpret_cast<const void*>(weight_stream_kernel));
   weight_stream_kernel<<<ctas, 32, 0, stream>>>(plan, state);
 }
 

@@ -1,6 +1,10 @@
 """Batch-1 graph-replay latency (L2 flushed) at many lengths: compare engine knobs via env."""
-import sys, numpy as np, torch
+import os, sys, numpy as np, torch
 sys.path.insert(0, ".")
+if os.environ.get("SP_LIB_OVERRIDE"):  # A/B another build of the engine library
+    from pathlib import Path
+    import paper_2408_12526_b200._lib as _L
+    _L.LIB_PATH = Path(os.environ["SP_LIB_OVERRIDE"])
 from paper_2408_12526_b200 import PRESETS, StudentGroup, random_bert_group
 cfg, K = PRESETS["base"]
 g = StudentGroup(random_bert_group(cfg, K, seed=0), max_tokens=512, max_seqs=1)
