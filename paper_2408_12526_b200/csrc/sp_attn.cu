@@ -30,10 +30,13 @@ __global__ void __launch_bounds__(32 * NW, MINB)
   half* sV = sK + NBUF * BK * LD;  // [NBUF][BK][LD]
 
   prefetch_share_l2(pf_ptr, pf_bytes);  // next projection's weights, while attention runs
-  pdl_enter();
   const int b = blockIdx.y;
-  const int s0 = __ldg(cu + b);
-  const int L = __ldg(cu + b + 1) - s0;
+  pdl_launch_dependents();
+  const int c0 = __ldg(cu + b);  // request input: issued before the dependency wait
+  const int c1 = __ldg(cu + b + 1);
+  pdl_wait();
+  const int s0 = c0;
+  const int L = c1 - c0;
   const int q0 = blockIdx.x * BQ;
   if (q0 >= L) return;
   const int g = blockIdx.z / n_heads;

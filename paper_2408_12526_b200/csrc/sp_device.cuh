@@ -13,6 +13,8 @@ __device__ __forceinline__ void pdl_enter() {
   pdl_wait();
   pdl_launch_dependents();
 }
+// Kernels that read request inputs / weights before the wait: release the next kernel first (so
+// those loads never delay its launch), issue the independent loads, then pdl_wait().
 
 __device__ __forceinline__ void mma_16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
   asm volatile(

@@ -18,7 +18,10 @@ __global__ void __launch_bounds__(128)
                     const float* __restrict__ beta, int hidden, float eps, float* x32, half* x16, long long x_gs,
                     const void* pf_ptr, unsigned long long pf_bytes) {
   prefetch_share_l2(pf_ptr, pf_bytes);
-  pdl_enter();
+  // Everything read here is a request input (ids, cu_seqlens: copied before the first kernel) or a
+  // weight, so the gathers are issued before the dependency wait; only the stores follow it (the
+  // previous request's kernels may still read x32 / x16).
+  pdl_launch_dependents();
   const int t = blockIdx.x * 4 + warp_id();
   if (n_tokens < 0) n_tokens = __ldg(cu + n_seqs);  // graph replay: live count = cu_seqlens[n_seqs]
   if (t >= n_tokens) return;
@@ -48,6 +51,7 @@ __global__ void __launch_bounds__(128)
 #pragma unroll
     for (int j = 0; j < 4; ++j) v[c][j] = a[j] + bb[j] + cc[j];
   }
+  pdl_wait();
   const long long row = (long long)g * x_gs + (long long)t * hidden;
   layer_norm_store<NC>(v, gamma + (long long)g * hidden, beta + (long long)g * hidden, eps, hidden, x32 + row,
                        x16 + row, nullptr);
@@ -63,20 +67,29 @@ __global__ void __launch_bounds__(128)
                      const int* __restrict__ cu, int n_seqs, half* cls16, long long cls_gs, const void* pf_ptr,
                      unsigned long long pf_bytes) {
   prefetch_share_l2(pf_ptr, pf_bytes);
-  pdl_enter();
+  // request inputs (cu_seqlens) and weights (bias) are read before the dependency wait
+  pdl_launch_dependents();
   const int t = blockIdx.x * 4 + warp_id();
   if (n_tokens < 0) n_tokens = __ldg(cu + n_seqs);
   if (t >= n_tokens) return;
   const int g = blockIdx.y;
   const int lane = lane_id();
   const long long row = (long long)g * x_gs + (long long)t * hidden;
-  // issue every load of the row up front: residual, bias and up to kMaxSplitsRow partial sums
   float4 r[NC], bs[NC], pv[SPLITS][NC];
+#pragma unroll
+  for (int c = 0; c < NC; ++c)
+    bs[c] = __ldg(reinterpret_cast<const float4*>(bias + (long long)g * hidden + c * 128 + lane * 4));
+  half* cls_row = nullptr;
+  if (cls16 != nullptr) {
+    const int b = seq_of(cu, n_seqs, t);
+    if (__ldg(cu + b) == t) cls_row = cls16 + (long long)g * cls_gs + (long long)b * hidden;
+  }
+  pdl_wait();
+  // then every load of the row at once: residual and up to kMaxSplitsRow partial sums
 #pragma unroll
   for (int c = 0; c < NC; ++c) {
     const int f = c * 128 + lane * 4;
     r[c] = *reinterpret_cast<const float4*>(x32 + row + f);
-    bs[c] = __ldg(reinterpret_cast<const float4*>(bias + (long long)g * hidden + f));
 #pragma unroll
     for (int s = 0; s < SPLITS; ++s) pv[s][c] = *reinterpret_cast<const float4*>(part + s * part_split_stride + row + f);
   }
@@ -94,11 +107,6 @@ __global__ void __launch_bounds__(128)
       v[c][2] += pv[s][c].z;
       v[c][3] += pv[s][c].w;
     }
-  }
-  half* cls_row = nullptr;
-  if (cls16 != nullptr) {
-    const int b = seq_of(cu, n_seqs, t);
-    if (__ldg(cu + b) == t) cls_row = cls16 + (long long)g * cls_gs + (long long)b * hidden;
   }
   layer_norm_store<NC>(v, gamma + (long long)g * hidden, beta + (long long)g * hidden, eps, hidden, x32 + row,
                        x16 + row, cls_row);

@@ -9,6 +9,6 @@ cfg, r = sys.argv[1], sys.argv[2].split()
 pts = sorted((int(a), float(b)) for a, b in (x.split(":") for x in r))
 # trapezoid mean over L in [16, 512] (bench distribution U{16..512})
 area = sum((x1 - x0) * (y0 + y1) / 2 for (x0, y0), (x1, y1) in zip(pts, pts[1:]))
-print(f"{cfg:45s} mean {area / (pts[-1][0] - pts[0][0]):6.1f}  " + " ".join(f"{a}:{b:.0f}" for a, b in pts))
+print(f"{cfg:45s} mean {area / (pts[-1][0] - pts[0][0]):6.1f}  " + " ".join(f"{a}:{b:.1f}" for a, b in pts))
 PY
 done
