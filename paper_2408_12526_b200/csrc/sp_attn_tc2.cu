@@ -1,0 +1,305 @@
+// sp_attn_tc2.cu — single-pass varlen attention on 5th-gen tensor cores, two CTAs per SM
+// (head_dim 64, L <= 512).
+//
+// One CTA per (student, sequence, head, 128-query block), 192 threads and 256 TMEM columns so two
+// CTAs share an SM (one's softmax runs while the other waits on its MMAs or loads):
+//   warps 0-3  softmax: thread = query row = TMEM lane (warp w owns lanes 32w..32w+31); each
+//              thread keeps its row's running max m and sum l (online softmax, log2 domain)
+//   warp 4     TMA producer: Q once, then 128-key K/V chunks through a 2-stage ring
+//   warp 5     TMEM allocation + MMA issue (one elected lane)
+// TMEM: S = Q K^T of the current chunk in columns [0, 128) (fp32), P = exp2(S - m) as packed fp16
+// in [128, 192), O in [192, 256). O += P V reads P straight from TMEM (tcgen05.mma A operand in
+// tensor memory), so P never touches shared memory.
+//   chunk j: MMA S_j -> softmax reads S_j to registers and frees S (the MMA of S_{j+1} overlaps
+//   the exponentials) -> row max -> P_j = exp2(S*c - m) -> waits PV_{j-1} -> writes P_j -> MMA
+//   O += P_j V_j.
+// Lazy rescale: the running max m is only raised when a chunk's max exceeds it by more than
+// 2^8 (P <= 256 stays exact in fp16, l in fp32); then the thread rescales its O row in TMEM
+// (after PV_{j-1} completed) — rare after the first chunk. Keys past the sequence end are masked;
+// query rows past it are not stored.
+// No reference counterpart; semantics = oracle/bert.py:attention.
+#include "sp_kernels.cuh"
+#include "sp_ptx.cuh"
+
+namespace sp {
+
+namespace {
+
+constexpr int kTile = 128 * 64 * 2;  // 128 rows x 64 fp16 = 16 KiB
+constexpr int kSoftWarps = 4;
+constexpr int kThreads2 = 32 * (kSoftWarps + 2);
+constexpr int kProd = 4, kMma = 5;
+constexpr uint32_t kColS = 0, kColP = 128, kColO = 192;
+constexpr float kRescaleLog2 = 8.f;
+
+__device__ __forceinline__ void umma_f16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]),
+      "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]),
+      "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(kThreads2, 2)
+    attn_tc2_kernel(const __grid_constant__ CUtensorMap map_qkv, half* __restrict__ ctx, const int* __restrict__ cu,
+                    int n_heads, int hidden, long long group_rows, float scale_log2) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;
+  uint8_t* sK = sQ + kTile;      // [2] stages
+  uint8_t* sV = sK + 2 * kTile;  // [2] stages
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + 2 * kTile);
+  uint64_t* q_full = bars;
+  uint64_t* kv_full = bars + 1;   // [2]
+  uint64_t* kv_empty = bars + 3;  // [2]
+  uint64_t* s_full = bars + 5;
+  uint64_t* s_free = bars + 6;
+  uint64_t* p_full = bars + 7;
+  uint64_t* pv_done = bars + 8;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 9);
+
+  pdl_launch_dependents();
+  // grid (student x head, sequence, query tile): the query tile is the slowest index, so the CTAs
+  // of the last (partial, mostly dead-warp) tiles of every head are dispatched last and fill the
+  // second wave instead of full tiles (4 tiles per head at L > 384 vs 296 CTA slots)
+  const int b = blockIdx.y;
+  const int s0 = __ldg(cu + b);  // request input: read before the dependency wait
+  const int L = __ldg(cu + b + 1) - s0;
+  const int q0 = blockIdx.z * 128;
+  if (q0 >= L) return;
+  const int g = blockIdx.x / n_heads;
+  const int h = blockIdx.x % n_heads;
+  const int n_chunks = (L + 127) >> 7;
+  const int row_base = static_cast<int>(g * group_rows + s0);
+  const int warp = warp_id();
+  const int lane = lane_id();
+
+  if (warp == kProd && lane == 0) {
+    mbar_init(q_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
+    }
+    mbar_init(s_full, 1);
+    mbar_init(s_free, kSoftWarps);
+    mbar_init(p_full, kSoftWarps);
+    mbar_init(pv_done, 1);
+    fence_barrier_init();
+    tma_prefetch_desc(&map_qkv);
+  }
+  if (warp == kMma) {
+    tmem_alloc(tmem_slot, 256);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == kProd) {
+    if (elect_one()) {
+      const uint64_t pol = policy_evict_last();
+      pdl_wait();  // qkv is the previous kernel's output
+      mbar_arrive_expect_tx(q_full, kTile);
+      tma_load_2d(&map_qkv, q_full, sQ, h * 64, row_base + q0, pol);
+      for (int j = 0; j < n_chunks; ++j) {
+        const int st = j & 1;
+        if (j >= 2) mbar_wait(&kv_empty[st], ((j >> 1) - 1) & 1);
+        mbar_arrive_expect_tx(&kv_full[st], 2 * kTile);
+        tma_load_2d(&map_qkv, &kv_full[st], sK + st * kTile, hidden + h * 64, row_base + j * 128, pol);
+        tma_load_2d(&map_qkv, &kv_full[st], sV + st * kTile, 2 * hidden + h * 64, row_base + j * 128, pol);
+      }
+    }
+    __syncwarp();
+  } else if (warp == kMma) {
+    if (elect_one()) {
+      const uint32_t idesc_s = umma_idesc_f16(128, 128);
+      const uint32_t idesc_o = umma_idesc_f16(128, 64) | (1u << 16);  // B (= V) is MN-major
+      const uint64_t qdesc = umma_sdesc_sw128(smem_u32(sQ));
+      mbar_wait(q_full, 0);
+      auto issue_s = [&](int j) {
+        mbar_wait(&kv_full[j & 1], (j >> 1) & 1);
+        if (j >= 1) mbar_wait(s_free, (j - 1) & 1);  // softmax holds S_{j-1} in registers
+        tc_fence_after();
+        const uint64_t kdesc = umma_sdesc_sw128(smem_u32(sK + (j & 1) * kTile));
+#pragma unroll
+        for (int k = 0; k < 4; ++k) umma_f16_ss(tmem + kColS, qdesc + 2 * k, kdesc + 2 * k, idesc_s, k > 0 ? 1u : 0u);
+        umma_commit(s_full);
+      };
+      issue_s(0);
+      for (int j = 0; j < n_chunks; ++j) {
+        if (j + 1 < n_chunks) issue_s(j + 1);  // next scores while the softmax works on chunk j
+        mbar_wait(p_full, j & 1);
+        tc_fence_after();
+        const uint8_t* vb = sV + (j & 1) * kTile;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)  // 16 keys per step: P columns 8k.. (2 fp16 each), V rows 16k..
+          umma_f16_ts(tmem + kColO, tmem + kColP + 8 * k, umma_sdesc_sw128(smem_u32(vb + k * 2048)), idesc_o,
+                      (j > 0 || k > 0) ? 1u : 0u);
+        umma_commit(pv_done);
+        umma_commit(&kv_empty[j & 1]);
+      }
+    }
+    __syncwarp();
+  } else {
+    // softmax: thread = query row q0 + row = TMEM lane row
+    const int row = warp * 32 + lane;
+    const uint32_t lane_base = static_cast<uint32_t>(warp * 32) << 16;
+    float m = 0.f, l = 0.f;
+    // A warp whose 32 query rows all lie past the sequence end (the tail tile of a head) skips
+    // the TMEM traffic and the exponentials; it still takes part in every barrier phase. Its P
+    // lanes keep stale values: the O rows they feed are never stored.
+    const bool live = q0 + warp * 32 < L;
+    for (int j = 0; j < n_chunks; ++j) {
+      mbar_wait(s_full, j & 1);
+      if (!live) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(s_free);
+        if (j >= 1) mbar_wait(pv_done, (j - 1) & 1);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(p_full);
+        continue;
+      }
+      tc_fence_after();
+      uint32_t r[4][32];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tmem_ld32_nowait(tmem + lane_base + kColS + 32 * c, r[c]);
+      tmem_wait_ld();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(s_free);  // S may be overwritten by the next chunk's MMA
+      const int valid = L - j * 128;       // keys of this chunk inside the sequence (>= 1)
+      if (valid < 128) {  // last chunk only
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (32 * c + i >= valid) r[c][i] = __float_as_uint(-INFINITY);
+      }
+      float mx = -INFINITY;
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+#pragma unroll
+        for (int i = 0; i < 32; ++i) mx = fmaxf(mx, __uint_as_float(r[c][i]));
+      mx *= scale_log2;
+      float alpha = 1.f;
+      if (j == 0) {
+        m = mx;
+      } else if (mx > m + kRescaleLog2) {
+        alpha = ex2(m - mx);
+        m = mx;
+        l *= alpha;
+      }
+      const float neg_m = -m;
+      uint32_t pk[2][32];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        float ps = 0.f;
+#pragma unroll
+        for (int i = 0; i < 32; i += 2) {
+          const float p0 = ex2(fmaf(__uint_as_float(r[c][i]), scale_log2, neg_m));
+          const float p1 = ex2(fmaf(__uint_as_float(r[c][i + 1]), scale_log2, neg_m));
+          ps += p0 + p1;
+          __half2 hp = __floats2half2_rn(p0, p1);
+          pk[c >> 1][(c & 1) * 16 + (i >> 1)] = *reinterpret_cast<uint32_t*>(&hp);
+        }
+        l += ps;
+      }
+      if (j >= 1) {
+        mbar_wait(pv_done, (j - 1) & 1);  // PV_{j-1} has read P and updated O
+        tc_fence_after();
+        if (__any_sync(0xffffffffu, alpha != 1.f)) {  // rare: rescale this warp's O rows
+          uint32_t o[2][32];
+          tmem_ld32_nowait(tmem + lane_base + kColO, o[0]);
+          tmem_ld32_nowait(tmem + lane_base + kColO + 32, o[1]);
+          tmem_wait_ld();
+#pragma unroll
+          for (int c = 0; c < 2; ++c)
+#pragma unroll
+            for (int i = 0; i < 32; ++i) o[c][i] = __float_as_uint(__uint_as_float(o[c][i]) * alpha);
+          tmem_st32(tmem + lane_base + kColO, o[0]);
+          tmem_st32(tmem + lane_base + kColO + 32, o[1]);
+        }
+      }
+      tmem_st32(tmem + lane_base + kColP, pk[0]);
+      tmem_st32(tmem + lane_base + kColP + 32, pk[1]);
+      tmem_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(p_full);
+    }
+    // epilogue: O / l -> fp16 -> ctx (one 128-byte row per thread)
+    mbar_wait(pv_done, (n_chunks - 1) & 1);
+    if (!live) goto done;
+    tc_fence_after();
+    uint32_t o[2][32];
+    tmem_ld32_nowait(tmem + lane_base + kColO, o[0]);
+    tmem_ld32_nowait(tmem + lane_base + kColO + 32, o[1]);
+    tmem_wait_ld();
+    if (q0 + row < L) {
+      const float inv = 1.f / l;
+      uint4* out = reinterpret_cast<uint4*>(ctx + (static_cast<long long>(row_base) + q0 + row) * hidden + h * 64);
+#pragma unroll
+      for (int v = 0; v < 8; ++v) {
+        uint32_t w[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int e = v * 8 + 2 * i;
+          __half2 hv = __floats2half2_rn(__uint_as_float(o[e >> 5][e & 31]) * inv,
+                                         __uint_as_float(o[(e + 1) >> 5][(e + 1) & 31]) * inv);
+          w[i] = *reinterpret_cast<uint32_t*>(&hv);
+        }
+        out[v] = make_uint4(w[0], w[1], w[2], w[3]);
+      }
+    }
+  }
+done:
+  tc_fence_before();
+  __syncthreads();
+  if (warp == kMma) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 256);
+  }
+}
+
+size_t attn_tc2_smem_bytes() { return 1024 + 5 * kTile + 128; }
+
+void launch_attention_tc2(const CUtensorMap& map_qkv, half* ctx, const int* cu_seqlens, int n_seqs, int max_len,
+                          int groups, int n_heads, int hidden, long long group_rows, cudaStream_t stream) {
+  if (n_seqs <= 0 || max_len <= 0 || groups <= 0) return;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(attn_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(attn_tc2_smem_bytes()));
+    attr_set = true;
+  }
+  const float scale_log2 = 1.4426950408889634f / 8.0f;  // log2(e) / sqrt(64)
+  dim3 grid(groups * n_heads, n_seqs, (max_len + 127) / 128);
+  launch_pdl(attn_tc2_kernel, grid, dim3(kThreads2), attn_tc2_smem_bytes(), stream, map_qkv, ctx, cu_seqlens, n_heads,
+             hidden, group_rows, scale_log2);
+}
+
+}  // namespace sp

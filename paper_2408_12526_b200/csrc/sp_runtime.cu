@@ -420,13 +420,27 @@ namespace {
 // tcgen05 attention (sp_attn_tc.cu) vs mma.sync attention (sp_attn.cu), by the measured crossover
 // (tools/len_probe.py): tcgen05 wins up to 128 keys and beyond 384 (one CTA per SM: at 160-384 the
 // mma.sync kernel's two CTAs per SM win). SP_ATTN_TC=0 / 1 forces either kernel.
-bool use_attn_tc(int head_dim, int max_len) {
+// Attention kernel by length: 0 = mma.sync (sp_attn.cu), 1 = two-pass tcgen05 (sp_attn_tc.cu),
+// 2 = single-pass tcgen05, two CTAs per SM (sp_attn_tc2.cu). SP_ATTN_TC forces one.
+int attn_kind(int head_dim, int max_len) {
   static const int mode = [] {
     const char* v = getenv("SP_ATTN_TC");
     return v == nullptr ? -1 : atoi(v);
   }();
-  if (head_dim != 64 || max_len > 512 || mode == 0) return false;
-  return mode > 0 || max_len <= 128 || max_len > 448;  // 385..448: 4-warp mma.sync tiles, 4 CTAs/SM
+  if (head_dim != 64 || max_len > 512) return 0;
+  if (mode >= 0) return mode;
+  return max_len <= 128 ? 1 : 2;  // measured in-graph (tools/len_probe.py): tc2 from 129 tokens
+}
+
+void launch_attention_any(int kind, const CUtensorMap& map_qkv, const half* qkv, half* ctx, const int* cu,
+                          int n_seqs, int max_len, int groups, int n_heads, int head_dim, int hidden,
+                          long long group_rows, cudaStream_t st) {
+  if (kind == 2)
+    sp::launch_attention_tc2(map_qkv, ctx, cu, n_seqs, max_len, groups, n_heads, hidden, group_rows, st);
+  else if (kind == 1)
+    sp::launch_attention_tc(map_qkv, ctx, cu, n_seqs, max_len, groups, n_heads, hidden, group_rows, st);
+  else
+    sp::launch_attention(qkv, ctx, cu, n_seqs, max_len, groups, n_heads, head_dim, hidden, group_rows, st);
 }
 
 // Launch one grouped projection. Returns the number of kernels launched (1).
@@ -854,11 +868,8 @@ int bert_forward(sp_group* g, const int32_t* ids, const int32_t* cu, int n_seqs,
       launches += run_gemm(g, SP_LAUNCH_GEMM_QKV, g->m_qkv[l], g->xm_x16, k, 3 * H, H, n_tokens, T, w.b_qkv + lS * 3 * H, 3 * H,
                            sp::ACT_NONE, g->qkv, (long long)T * 3 * H, 0, 1, 0, st, t_dev);
       g->rec_begin(SP_LAUNCH_ATTENTION, GTH * 8.0, 4.0 * k * H * g->sum_len_sq);
-      if (use_attn_tc(H / c.n_heads, max_len))
-        sp::launch_attention_tc(g->m_qkv_attn, g->ctx, cu, n_seqs, max_len, k, c.n_heads, H, T, st);
-      else
-        sp::launch_attention(g->qkv, g->ctx, cu, n_seqs, max_len, k, c.n_heads, H / c.n_heads, H, T, st,
-                             PF(pf(wo + lS * H * H, (size_t)k * H * H)));
+      launch_attention_any(attn_kind(H / c.n_heads, max_len), g->m_qkv_attn, g->qkv, g->ctx, cu, n_seqs, max_len, k,
+                           c.n_heads, H / c.n_heads, H, T, st);
       g->rec_end();
       ++launches;
       // O and FFN2 write raw partial sums; the reduce+LN kernel owns bias, residual and LayerNorm
@@ -1201,16 +1212,12 @@ int sp_op_attention(const void* qkv, void* ctx, const int32_t* cu_seqlens, int32
   if (head_dim != 32 && head_dim != 64) return fail(SP_EINVAL, "head_dim must be 32 or 64");
   if (n_seqs < 1 || groups < 1 || n_heads < 1 || max_seq_len < 1) return fail(SP_EINVAL, "bad attention shape");
   const int hidden = n_heads * head_dim;
-  if (use_attn_tc(head_dim, max_seq_len)) {
-    CUtensorMap m;
-    if (!make_map(&m, qkv, (uint64_t)groups * group_rows, 3 * hidden, 128))
-      return fail(SP_EINVAL, "attention tensor map failed");
-    sp::launch_attention_tc(m, static_cast<half*>(ctx), cu_seqlens, n_seqs, max_seq_len, groups, n_heads, hidden,
-                            group_rows, static_cast<cudaStream_t>(stream));
-  } else {
-    sp::launch_attention(static_cast<const half*>(qkv), static_cast<half*>(ctx), cu_seqlens, n_seqs, max_seq_len,
-                         groups, n_heads, head_dim, hidden, group_rows, static_cast<cudaStream_t>(stream));
-  }
+  const int kind = attn_kind(head_dim, max_seq_len);
+  CUtensorMap m{};
+  if (kind != 0 && !make_map(&m, qkv, (uint64_t)groups * group_rows, 3 * hidden, 128))
+    return fail(SP_EINVAL, "attention tensor map failed");
+  launch_attention_any(kind, m, static_cast<const half*>(qkv), static_cast<half*>(ctx), cu_seqlens, n_seqs,
+                       max_seq_len, groups, n_heads, head_dim, hidden, group_rows, static_cast<cudaStream_t>(stream));
   SP_CUDA(cudaGetLastError());
   return SP_OK;
 }

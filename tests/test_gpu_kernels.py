@@ -113,3 +113,48 @@ def test_attention_varlen_matches_torch(cuda_lib, hd, nh, lens):
     ref = _attn_ref(qkv, cu, G, nh, hd)
     torch.testing.assert_close(ctx[:, :T].float(), ref[:, :T], rtol=5e-3, atol=5e-3)
     assert torch.all(ctx[:, T:] == 0), "attention wrote past the packed tokens"
+
+
+_FORCED_ATTN = r"""
+import math, sys, numpy as np, torch
+sys.path.insert(0, '.'); sys.path.insert(0, 'tests')
+from paper_2408_12526_b200 import _lib
+from test_gpu_kernels import _attn_ref
+lib = _lib.load()
+cases = [(64, 12, [1, 17, 64, 65, 200]), (64, 16, [512, 1, 130]), (64, 8, [100, 1, 128, 37]),
+         (64, 12, [416, 385, 3]), (64, 4, [256, 255, 129]), (64, 4, [511, 300])]
+for grow in (False, True):
+    for hd, nh, lens in cases:
+        torch.manual_seed(sum(lens) + grow)
+        G, H = 2, nh * hd
+        cu = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+        T = int(cu[-1]); cap = T + 5
+        qkv = torch.randn(G, cap, 3 * H, device='cuda')
+        if grow:  # scores that keep rising along the keys: exercises the running-max rescale
+            qkv[:, :, H:2 * H] *= torch.linspace(0.2, 3.0, cap, device='cuda')[None, :, None]
+        qkv = qkv.half()
+        ctx = torch.zeros(G, cap, H, device='cuda', dtype=torch.float16)
+        cu_d = torch.from_numpy(cu).cuda()
+        _lib.check(lib.sp_op_attention(qkv.data_ptr(), ctx.data_ptr(), cu_d.data_ptr(), len(lens), max(lens), G,
+                                       nh, hd, cap, None))
+        torch.cuda.synchronize()
+        ref = _attn_ref(qkv, cu, G, nh, hd)
+        torch.testing.assert_close(ctx[:, :T].float(), ref[:, :T], rtol=5e-3, atol=5e-3)
+        assert torch.all(ctx[:, T:] == 0)
+print('ok')
+"""
+
+
+@pytest.mark.parametrize("kind", ["0", "1", "2"])
+def test_attention_kernels_forced(kind):
+    """Every attention kernel (mma.sync, two-pass tcgen05, single-pass two-CTA tcgen05) against the
+    fp32 reference at every length class, with and without key scores that rise along the sequence
+    (forces the single-pass kernel's running-max rescale). Fresh process: SP_ATTN_TC is read once."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    r = subprocess.run([sys.executable, "-c", _FORCED_ATTN], capture_output=True, text=True, timeout=600,
+                       env={**os.environ, "SP_ATTN_TC": kind}, cwd=str(Path(__file__).resolve().parents[1]))
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-3000:]
