@@ -11,6 +11,7 @@
  *   sp_group_forward       <- EnsembleState.rep(x, k) + classifier.forward(rep)  distill.py:169-178, :512
  *                             (BERT-kind students: token ids + cu_seqlens, device buffers)
  *   sp_group_forward_dense <- the same for the reference's dense StudentModel      nnkernel.py:289-301
+ *   sp_group_forward_graph <- the same for one sequence on device buffers, as a CUDA-graph replay
  *   sp_group_forward_host  <- the same call with HOST buffers (ids in, logits out), the serving seam
  *                             Simulation._dispatch -> service_time                 servesim.py:486, :287-307
  *   sp_group_forward_eval  <- the forward half of accumulate_prefix_gradients (every student's
@@ -138,6 +139,14 @@ int sp_group_forward_dense_eval(sp_group* group, const void* x, int32_t n_rows, 
  * inputs, copies them to the device, runs the group, copies logits back and synchronizes `stream`. */
 int sp_group_forward_host(sp_group* group, const int32_t* ids, const int32_t* cu_seqlens, int32_t n_seqs,
                           int32_t n_tokens, int32_t k_active, float* logits_out, int32_t add_bias, void* stream);
+
+/* Batch-1 request on DEVICE buffers replayed as the bucket's CUDA graph (one sequence:
+ * ids int32 [n_tokens], cu_seqlens int32 [2] = {0, n_tokens}; logits f32 [C] device). The inputs
+ * are copied device-to-device into the group's staging, then one graph launch runs the forward;
+ * asynchronous on `stream`. The first call per (16-token bucket, k, logits buffer) captures the
+ * graph. Same result as sp_group_forward (graph replay is bit-identical to eager). */
+int sp_group_forward_graph(sp_group* group, const int32_t* ids, const int32_t* cu_seqlens, int32_t n_tokens,
+                           int32_t k_active, float* logits_out, int32_t add_bias, void* stream);
 
 /* Capture (ahead of serving) the CUDA graphs that sp_group_forward_host replays for
  * single-sequence requests: one per 16-token bucket up to max_tokens, for this k_active/add_bias.

@@ -86,6 +86,9 @@ SIGNATURES: dict[str, tuple] = {
     ),
     "sp_group_last_launches": (C.c_int, [C.c_void_p]),
     "sp_group_prepare_graphs": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32]),
+    "sp_group_forward_graph": (
+        C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_int32, C.c_void_p],
+    ),
     "sp_group_set_profiling": (C.c_int, [C.c_void_p, C.c_int]),
     "sp_group_profile_read": (C.c_int, [C.c_void_p, C.POINTER(SpLaunchRecord), C.c_int]),
     "sp_op_gemm": (

@@ -163,6 +163,8 @@ struct sp_group {
   int last_launches = 0;
   // CUDA graphs of the batch-1 host path, keyed by (16-token bucket, k_active, add_bias)
   std::map<std::tuple<int, int, int>, cudaGraphExec_t> graphs;
+  // graphs of the device-buffer batch-1 path (sp_group_forward_graph), keyed also by the logits slot
+  std::map<std::tuple<int, int, int, uintptr_t>, cudaGraphExec_t> dgraphs;
   cudaStream_t cap_stream = nullptr;
   int graph_launches = 0;  // kernels per graph replay
   double sum_len_sq = 0.0;  // sum_b L_b^2 of the current request (attention flops)
@@ -225,6 +227,7 @@ int dev_alloc(sp_group* g, T** p, size_t count) {
 
 void free_all(sp_group* g) {
   for (auto& kv : g->graphs) cudaGraphExecDestroy(kv.second);
+  for (auto& kv : g->dgraphs) cudaGraphExecDestroy(kv.second);
   if (g->ws_stream) cudaStreamDestroy(g->ws_stream);
   if (g->ws_fork) cudaEventDestroy(g->ws_fork);
   if (g->ws_join) cudaEventDestroy(g->ws_join);
@@ -988,6 +991,34 @@ int get_graph(sp_group* g, int n_tokens, int k, int add_bias, cudaGraphExec_t* o
   return SP_OK;
 }
 
+// Device-buffer batch-1 path: the same bucket graphs without the host copies; the forward reads
+// the group's own device staging (filled by two device-to-device copies) and writes `logits`.
+int get_graph_dev(sp_group* g, int n_tokens, int k, int add_bias, float* logits, cudaGraphExec_t* out) {
+  const int bucket = std::min(((n_tokens + 15) / 16) * 16, std::max(16, g->cfg.max_tokens));
+  const auto key = std::make_tuple(bucket, k, add_bias, reinterpret_cast<uintptr_t>(logits));
+  auto it = g->dgraphs.find(key);
+  if (it != g->dgraphs.end()) {
+    *out = it->second;
+    return SP_OK;
+  }
+  if (g->cap_stream == nullptr) SP_CUDA(cudaStreamCreateWithFlags(&g->cap_stream, cudaStreamNonBlocking));
+  SP_CUDA(cudaStreamBeginCapture(g->cap_stream, cudaStreamCaptureModeThreadLocal));
+  const int max_len = std::min(bucket, g->cfg.max_pos);
+  int rc = bert_forward(g, g->d_ids, g->d_cu, 1, bucket, max_len, k, nullptr, logits, add_bias, g->cap_stream, true);
+  cudaGraph_t graph = nullptr;
+  cudaError_t e = cudaStreamEndCapture(g->cap_stream, &graph);
+  if (rc) return rc;
+  if (e != cudaSuccess) return fail(SP_ECUDA, "graph capture: %s", cudaGetErrorString(e));
+  cudaGraphExec_t exec = nullptr;
+  e = cudaGraphInstantiate(&exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (e != cudaSuccess) return fail(SP_ECUDA, "graph instantiate: %s", cudaGetErrorString(e));
+  g->graph_launches = g->last_launches;
+  g->dgraphs[key] = exec;
+  *out = exec;
+  return SP_OK;
+}
+
 int dense_forward(sp_group* g, const half* x, int n_rows, int k, float* rep, float* logits, int add_bias,
                   cudaStream_t st, const XMaps& xin_maps) {
   const sp_config& c = g->cfg;
@@ -1226,6 +1257,29 @@ int sp_op_attention(const void* qkv, void* ctx, const int32_t* cu_seqlens, int32
 
 extern "C" int sp_debug_set_request_trace(void* buf) {
   g_req_trace = static_cast<unsigned long long*>(buf);
+  return SP_OK;
+}
+
+extern "C" int sp_group_forward_graph(sp_group* g, const int32_t* ids, const int32_t* cu_seqlens, int32_t n_tokens,
+                                      int32_t k_active, float* logits_out, int32_t add_bias, void* stream) {
+  if (g == nullptr) return fail(SP_EINVAL, "null group");
+  const sp_config& c = g->cfg;
+  if (c.kind != SP_KIND_BERT) return fail(SP_EINVAL, "sp_group_forward_graph needs a BERT-kind group");
+  if (!ids || !cu_seqlens || !logits_out) return fail(SP_EINVAL, "null buffer");
+  if (k_active < 1 || k_active > c.n_students) return fail(SP_EINVAL, "k=%d out of range 1..%d", k_active, c.n_students);
+  if (n_tokens < 1 || n_tokens > c.max_tokens || n_tokens > c.max_pos)
+    return fail(SP_EINVAL, "n_tokens=%d outside 1..%d", n_tokens, std::min(c.max_tokens, c.max_pos));
+  if (g->profiling || !graphs_enabled() || fused_ok(g, 1, n_tokens, k_active))
+    return sp_group_forward(g, ids, cu_seqlens, 1, n_tokens, n_tokens, k_active, nullptr, logits_out, add_bias, stream);
+  cudaSetDevice(g->device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaGraphExec_t exec = nullptr;
+  int rc = get_graph_dev(g, n_tokens, k_active, add_bias, logits_out, &exec);
+  if (rc) return rc;
+  SP_CUDA(cudaMemcpyAsync(g->d_cu, cu_seqlens, 2 * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+  SP_CUDA(cudaMemcpyAsync(g->d_ids, ids, sizeof(int32_t) * n_tokens, cudaMemcpyDeviceToDevice, st));
+  SP_CUDA(cudaGraphLaunch(exec, st));
+  g->last_launches = g->graph_launches;
   return SP_OK;
 }
 

@@ -223,6 +223,14 @@ class StudentGroup:
                                               k_local, _ptr(rep), logits.data_ptr(), int(add_bias),
                                               _stream_handle(stream, self.device)))
 
+    def forward_graph_device(self, ids: torch.Tensor, cu: torch.Tensor, n_tokens: int, k_local: int,
+                             logits: torch.Tensor, add_bias: bool = True,
+                             stream: torch.cuda.Stream | None = None) -> None:
+        """One sequence on device buffers, replayed as its 16-token bucket's CUDA graph (no host sync)."""
+        _lib.check(self._lib.sp_group_forward_graph(self._handle, ids.data_ptr(), cu.data_ptr(), n_tokens, k_local,
+                                                    logits.data_ptr(), int(add_bias),
+                                                    _stream_handle(stream, self.device)))
+
     def forward_dense_device(self, x16: torch.Tensor, n_rows: int, k_local: int, rep: torch.Tensor | None,
                              logits: torch.Tensor, add_bias: bool = True,
                              stream: torch.cuda.Stream | None = None) -> None:

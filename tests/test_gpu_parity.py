@@ -249,3 +249,24 @@ def test_opt_in_kernel_variants_match_oracle(env):
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600,
                        env={**os.environ, key: val}, cwd=str(__import__("pathlib").Path(__file__).resolve().parents[1]))
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
+def test_device_graph_path_matches_eager():
+    """sp_group_forward_graph (device buffers, bucket-graph replay) equals the eager forward (the bucket's
+    tile configuration may change split-K summation order: fp32 rounding level)."""
+    import torch
+    from paper_2408_12526_b200 import PRESETS, StudentGroup, random_bert_group
+
+    cfg, K = PRESETS["base"]
+    g = StudentGroup(random_bert_group(cfg, 3, seed=11), max_tokens=512, max_seqs=1)
+    rng = np.random.default_rng(3)
+    out_g = torch.empty(1, cfg.n_classes, device="cuda")
+    out_e = torch.empty(1, cfg.n_classes, device="cuda")
+    for L in (1, 16, 17, 100, 129, 300, 512):
+        ids = torch.from_numpy(np.r_[101, rng.integers(1000, cfg.vocab, size=L - 1)].astype(np.int32)).cuda()
+        cu = torch.tensor([0, L], dtype=torch.int32, device="cuda")
+        for k in (3, 1):
+            g.forward_graph_device(ids, cu, L, k, out_g)
+            g.forward_packed_device(ids, cu, 1, L, L, k, None, out_e)
+            torch.cuda.synchronize()
+            torch.testing.assert_close(out_g, out_e, rtol=1e-4, atol=1e-6)
