@@ -198,6 +198,8 @@ int sp_op_attention(const void* qkv, void* ctx, const int32_t* cu_seqlens, int32
  * (entry, prologue done, first TMA, last TMA, first MMA, last commit, epilogue start, exit) into
  * this device buffer, indexed by CTA. */
 int sp_debug_set_gemm_trace(void* device_buf);
+/* Debug: per-CTA timeline (16 %globaltimer stamps) of the single-pass attention kernel, or NULL. */
+int sp_debug_set_attn_trace(void* device_buf);
 /* Debug: CTA count of every GEMM launch traced since the last sp_debug_set_gemm_trace. */
 int sp_debug_gemm_trace_launches(int32_t* ctas_per_launch, int32_t max_launches);
 

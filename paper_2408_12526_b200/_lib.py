@@ -97,6 +97,7 @@ SIGNATURES: dict[str, tuple] = {
          C.c_int32, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p],
     ),
     "sp_debug_set_gemm_trace": (C.c_int, [C.c_void_p]),
+    "sp_debug_set_attn_trace": (C.c_int, [C.c_void_p]),
     "sp_debug_gemm_trace_launches": (C.c_int, [C.c_void_p, C.c_int32]),
     "sp_op_attention": (
         C.c_int,

@@ -63,9 +63,11 @@ __device__ __forceinline__ float ex2(float x) {
 
 }  // namespace
 
+// TRACE (debug, tools/trace_attn.py): 16 %globaltimer stamps per CTA into `tr`.
+template <bool TRACE>
 __global__ void __launch_bounds__(kThreads2, 2)
     attn_tc2_kernel(const __grid_constant__ CUtensorMap map_qkv, half* __restrict__ ctx, const int* __restrict__ cu,
-                    int n_heads, int hidden, long long group_rows, float scale_log2) {
+                    int n_heads, int hidden, long long group_rows, float scale_log2, unsigned long long* tr) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;
@@ -81,6 +83,8 @@ __global__ void __launch_bounds__(kThreads2, 2)
   uint64_t* pv_done = bars + 8;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 9);
 
+  if (TRACE) tr += 16ull * (blockIdx.x + gridDim.x * (blockIdx.y + (unsigned long long)gridDim.y * blockIdx.z));
+  if (TRACE && threadIdx.x == 0) tr[0] = globaltimer();
   pdl_launch_dependents();
   // grid (student x head, sequence, query tile): the query tile is the slowest index, so the CTAs
   // of the last (partial, mostly dead-warp) tiles of every head are dispatched last and fill the
@@ -118,6 +122,7 @@ __global__ void __launch_bounds__(kThreads2, 2)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (TRACE && threadIdx.x == 0) tr[1] = globaltimer();
 
   if (warp == kProd) {
     if (elect_one()) {
@@ -128,6 +133,7 @@ __global__ void __launch_bounds__(kThreads2, 2)
       for (int j = 0; j < n_chunks; ++j) {
         const int st = j & 1;
         if (j >= 2) mbar_wait(&kv_empty[st], ((j >> 1) - 1) & 1);
+        if (TRACE && j < 4) tr[10 + j] = globaltimer();
         mbar_arrive_expect_tx(&kv_full[st], 2 * kTile);
         tma_load_2d(&map_qkv, &kv_full[st], sK + st * kTile, hidden + h * 64, row_base + j * 128, pol);
         tma_load_2d(&map_qkv, &kv_full[st], sV + st * kTile, 2 * hidden + h * 64, row_base + j * 128, pol);
@@ -184,6 +190,7 @@ __global__ void __launch_bounds__(kThreads2, 2)
         continue;
       }
       tc_fence_after();
+      if (TRACE && row == 0 && j < 4) tr[2 + j] = globaltimer();
       uint32_t r[4][32];
 #pragma unroll
       for (int c = 0; c < 4; ++c) tmem_ld32_nowait(tmem + lane_base + kColS + 32 * c, r[c]);
@@ -250,9 +257,11 @@ __global__ void __launch_bounds__(kThreads2, 2)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(p_full);
+      if (TRACE && row == 0 && j < 4) tr[6 + j] = globaltimer();
     }
     // epilogue: O / l -> fp16 -> ctx (one 128-byte row per thread)
     mbar_wait(pv_done, (n_chunks - 1) & 1);
+    if (TRACE && row == 0) tr[14] = globaltimer();
     if (!live) goto done;
     tc_fence_after();
     uint32_t o[2][32];
@@ -283,23 +292,33 @@ done:
     tc_fence_after();
     tmem_dealloc(tmem, 256);
   }
+  if (TRACE && threadIdx.x == 0) tr[15] = globaltimer();
 }
 
 size_t attn_tc2_smem_bytes() { return 1024 + 5 * kTile + 128; }
+
+static unsigned long long* g_attn_trace = nullptr;
+void set_attn_trace(unsigned long long* buf) { g_attn_trace = buf; }
 
 void launch_attention_tc2(const CUtensorMap& map_qkv, half* ctx, const int* cu_seqlens, int n_seqs, int max_len,
                           int groups, int n_heads, int hidden, long long group_rows, cudaStream_t stream) {
   if (n_seqs <= 0 || max_len <= 0 || groups <= 0) return;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(attn_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(attn_tc2_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(attn_tc2_smem_bytes()));
+    cudaFuncSetAttribute(attn_tc2_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(attn_tc2_smem_bytes()));
     attr_set = true;
   }
   const float scale_log2 = 1.4426950408889634f / 8.0f;  // log2(e) / sqrt(64)
   dim3 grid(groups * n_heads, n_seqs, (max_len + 127) / 128);
-  launch_pdl(attn_tc2_kernel, grid, dim3(kThreads2), attn_tc2_smem_bytes(), stream, map_qkv, ctx, cu_seqlens, n_heads,
-             hidden, group_rows, scale_log2);
+  if (g_attn_trace)
+    launch_pdl(attn_tc2_kernel<true>, grid, dim3(kThreads2), attn_tc2_smem_bytes(), stream, map_qkv, ctx, cu_seqlens,
+               n_heads, hidden, group_rows, scale_log2, g_attn_trace);
+  else
+    launch_pdl(attn_tc2_kernel<false>, grid, dim3(kThreads2), attn_tc2_smem_bytes(), stream, map_qkv, ctx, cu_seqlens,
+               n_heads, hidden, group_rows, scale_log2, static_cast<unsigned long long*>(nullptr));
 }
 
 }  // namespace sp

@@ -143,6 +143,8 @@ void launch_attention_tc(const CUtensorMap& map_qkv, half* ctx, const int* cu_se
 void launch_attention_tc2(const CUtensorMap& map_qkv, half* ctx, const int* cu_seqlens, int n_seqs, int max_len,
                           int groups, int n_heads, int hidden, long long group_rows, cudaStream_t stream);
 
+void set_attn_trace(unsigned long long* buf);  // debug: per-CTA timeline of attn_tc2 (16 stamps)
+
 // Embedding gather + LayerNorm: x = LN(E_word[g][id_t] + E_pos[g][pos_t] + E_type[g][0]).
 void launch_embed_ln(const int* ids, const int* cu_seqlens, int n_seqs, int n_tokens, int groups,
                      const half* word, const half* pos, const half* type, long long word_gs, long long pos_gs,

@@ -1233,6 +1233,11 @@ int sp_debug_set_gemm_trace(void* device_buf) {
   return SP_OK;
 }
 
+int sp_debug_set_attn_trace(void* device_buf) {
+  sp::set_attn_trace(static_cast<unsigned long long*>(device_buf));
+  return SP_OK;
+}
+
 int sp_debug_gemm_trace_launches(int32_t* ctas_per_launch, int32_t max_launches) {
   return sp::gemm_trace_counts(ctas_per_launch, max_launches);
 }
