@@ -1,6 +1,10 @@
 """Op-level attention timing (batch-1 shapes): K students x heads over one sequence of L tokens."""
-import sys, numpy as np, torch
+import os, sys, numpy as np, torch
 sys.path.insert(0, ".")
+if os.environ.get("SP_LIB_OVERRIDE"):  # A/B another build of the engine library
+    from pathlib import Path
+    import paper_2408_12526_b200._lib as _L
+    _L.LIB_PATH = Path(os.environ["SP_LIB_OVERRIDE"])
 from paper_2408_12526_b200 import _lib
 lib = _lib.load()
 G, NH, D = 8, 12, 64
