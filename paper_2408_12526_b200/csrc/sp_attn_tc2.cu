@@ -21,14 +21,23 @@
 #include "sp_kernels.cuh"
 #include "sp_ptx.cuh"
 
+#include <cstdlib>
+
 namespace sp {
 
 namespace {
 
 constexpr int kTile = 128 * 64 * 2;  // 128 rows x 64 fp16 = 16 KiB
-constexpr int kSoftWarps = 4;
-constexpr int kThreads2 = 32 * (kSoftWarps + 2);
-constexpr int kProd = 4, kMma = 5;
+// SPLIT softmax warps per TMEM lane quadrant, each owning 128 / SPLIT key columns of a chunk
+template <int SPLIT>
+struct Tc2Cfg {
+  static constexpr int kSoftWarps = 4 * SPLIT;
+  static constexpr int kThreads = 32 * (kSoftWarps + 2);
+  static constexpr int kProd = kSoftWarps, kMma = kSoftWarps + 1;
+  static constexpr int kCols = 128 / SPLIT;  // S columns per softmax thread
+  static constexpr int kGroups = kCols / 32;
+  static constexpr int kMinBlocks = 2;
+};
 constexpr uint32_t kColS = 0, kColP = 128, kColO = 192;
 constexpr float kRescaleLog2 = 8.f;
 
@@ -64,10 +73,12 @@ __device__ __forceinline__ float ex2(float x) {
 }  // namespace
 
 // TRACE (debug, tools/trace_attn.py): 16 %globaltimer stamps per CTA into `tr`.
-template <bool TRACE>
-__global__ void __launch_bounds__(kThreads2, 2)
+template <bool TRACE, int SPLIT>
+__global__ void __launch_bounds__(Tc2Cfg<SPLIT>::kThreads, Tc2Cfg<SPLIT>::kMinBlocks)
     attn_tc2_kernel(const __grid_constant__ CUtensorMap map_qkv, half* __restrict__ ctx, const int* __restrict__ cu,
                     int n_heads, int hidden, long long group_rows, float scale_log2, unsigned long long* tr) {
+  using C = Tc2Cfg<SPLIT>;
+  constexpr int kSoftWarps = C::kSoftWarps, kProd = C::kProd, kMma = C::kMma, NG = C::kGroups;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;
@@ -82,6 +93,7 @@ __global__ void __launch_bounds__(kThreads2, 2)
   uint64_t* p_full = bars + 7;
   uint64_t* pv_done = bars + 8;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 9);
+  float* xch = reinterpret_cast<float*>(bars + 10);  // SPLIT = 2: [2 chunk parities][2 halves][128 rows]
 
   if (TRACE) tr += 16ull * (blockIdx.x + gridDim.x * (blockIdx.y + (unsigned long long)gridDim.y * blockIdx.z));
   if (TRACE && threadIdx.x == 0) tr[0] = globaltimer();
@@ -171,14 +183,17 @@ __global__ void __launch_bounds__(kThreads2, 2)
     }
     __syncwarp();
   } else {
-    // softmax: thread = query row q0 + row = TMEM lane row
-    const int row = warp * 32 + lane;
-    const uint32_t lane_base = static_cast<uint32_t>(warp * 32) << 16;
+    // softmax: thread = query row q0 + row = TMEM lane row; with SPLIT = 2 the two warps of a lane
+    // quadrant take one half of the chunk's key columns each and exchange row maxima through smem
+    const int quad = warp & 3, hf = warp >> 2;
+    const int row = quad * 32 + lane;
+    const uint32_t lane_base = static_cast<uint32_t>(quad * 32) << 16;
+    const uint32_t col0 = static_cast<uint32_t>(hf * C::kCols);
     float m = 0.f, l = 0.f;
     // A warp whose 32 query rows all lie past the sequence end (the tail tile of a head) skips
     // the TMEM traffic and the exponentials; it still takes part in every barrier phase. Its P
     // lanes keep stale values: the O rows they feed are never stored.
-    const bool live = q0 + warp * 32 < L;
+    const bool live = q0 + quad * 32 < L;
     for (int j = 0; j < n_chunks; ++j) {
       mbar_wait(s_full, j & 1);
       if (!live) {
@@ -190,27 +205,33 @@ __global__ void __launch_bounds__(kThreads2, 2)
         continue;
       }
       tc_fence_after();
-      if (TRACE && row == 0 && j < 4) tr[2 + j] = globaltimer();
-      uint32_t r[4][32];
+      if (TRACE && threadIdx.x == 0 && j < 4) tr[2 + j] = globaltimer();
+      uint32_t r[NG][32];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) tmem_ld32_nowait(tmem + lane_base + kColS + 32 * c, r[c]);
+      for (int c = 0; c < NG; ++c) tmem_ld32_nowait(tmem + lane_base + kColS + col0 + 32 * c, r[c]);
       tmem_wait_ld();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(s_free);  // S may be overwritten by the next chunk's MMA
-      const int valid = L - j * 128;       // keys of this chunk inside the sequence (>= 1)
-      if (valid < 128) {  // last chunk only
+      const int valid = L - j * 128 - static_cast<int>(col0);  // keys of this warp's columns inside the sequence
+      if (valid < C::kCols) {  // last chunk only
 #pragma unroll
-        for (int c = 0; c < 4; ++c)
+        for (int c = 0; c < NG; ++c)
 #pragma unroll
           for (int i = 0; i < 32; ++i)
             if (32 * c + i >= valid) r[c][i] = __float_as_uint(-INFINITY);
       }
       float mx = -INFINITY;
 #pragma unroll
-      for (int c = 0; c < 4; ++c)
+      for (int c = 0; c < NG; ++c)
 #pragma unroll
         for (int i = 0; i < 32; ++i) mx = fmaxf(mx, __uint_as_float(r[c][i]));
+      if constexpr (SPLIT == 2) {
+        float* x = xch + (j & 1) * 256;
+        x[hf * 128 + row] = mx;
+        named_barrier_sync(1 + quad, 64);
+        mx = fmaxf(mx, x[(hf ^ 1) * 128 + row]);
+      }
       mx *= scale_log2;
       float alpha = 1.f;
       if (j == 0) {
@@ -221,9 +242,9 @@ __global__ void __launch_bounds__(kThreads2, 2)
         l *= alpha;
       }
       const float neg_m = -m;
-      uint32_t pk[2][32];
+      uint32_t pk[NG * 16];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
+      for (int c = 0; c < NG; ++c) {
         float ps = 0.f;
 #pragma unroll
         for (int i = 0; i < 32; i += 2) {
@@ -231,57 +252,72 @@ __global__ void __launch_bounds__(kThreads2, 2)
           const float p1 = ex2(fmaf(__uint_as_float(r[c][i + 1]), scale_log2, neg_m));
           ps += p0 + p1;
           __half2 hp = __floats2half2_rn(p0, p1);
-          pk[c >> 1][(c & 1) * 16 + (i >> 1)] = *reinterpret_cast<uint32_t*>(&hp);
+          pk[c * 16 + (i >> 1)] = *reinterpret_cast<uint32_t*>(&hp);
         }
         l += ps;
       }
       if (j >= 1) {
         mbar_wait(pv_done, (j - 1) & 1);  // PV_{j-1} has read P and updated O
         tc_fence_after();
-        if (__any_sync(0xffffffffu, alpha != 1.f)) {  // rare: rescale this warp's O rows
-          uint32_t o[2][32];
-          tmem_ld32_nowait(tmem + lane_base + kColO, o[0]);
-          tmem_ld32_nowait(tmem + lane_base + kColO + 32, o[1]);
-          tmem_wait_ld();
+        if (__any_sync(0xffffffffu, alpha != 1.f)) {  // rare: rescale this warp's share of its O rows
 #pragma unroll
-          for (int c = 0; c < 2; ++c)
+          for (int c = 0; c < 2 / SPLIT; ++c) {
+            uint32_t o[32];
+            const uint32_t oc = tmem + lane_base + kColO + 32 * (hf + c);
+            tmem_ld32_nowait(oc, o);
+            tmem_wait_ld();
 #pragma unroll
-            for (int i = 0; i < 32; ++i) o[c][i] = __float_as_uint(__uint_as_float(o[c][i]) * alpha);
-          tmem_st32(tmem + lane_base + kColO, o[0]);
-          tmem_st32(tmem + lane_base + kColO + 32, o[1]);
+            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+            tmem_st32(oc, o);
+          }
         }
       }
-      tmem_st32(tmem + lane_base + kColP, pk[0]);
-      tmem_st32(tmem + lane_base + kColP + 32, pk[1]);
+#pragma unroll
+      for (int c = 0; c < NG / 2; ++c) {
+        uint32_t w32[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) w32[i] = pk[c * 32 + i];
+        tmem_st32(tmem + lane_base + kColP + col0 / 2 + 32 * c, w32);
+      }
       tmem_wait_st();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(p_full);
-      if (TRACE && row == 0 && j < 4) tr[6 + j] = globaltimer();
+      if (TRACE && threadIdx.x == 0 && j < 4) tr[6 + j] = globaltimer();
     }
-    // epilogue: O / l -> fp16 -> ctx (one 128-byte row per thread)
+    // epilogue: O / l -> fp16 -> ctx (this warp's 64 / SPLIT columns of one row per thread)
+    if constexpr (SPLIT == 2) {  // row sums of the two column halves
+      float* x = xch + 512;
+      if (live) x[hf * 128 + row] = l;
+      named_barrier_sync(1 + quad, 64);
+      if (live) l += x[(hf ^ 1) * 128 + row];
+    }
     mbar_wait(pv_done, (n_chunks - 1) & 1);
-    if (TRACE && row == 0) tr[14] = globaltimer();
+    if (TRACE && threadIdx.x == 0) tr[14] = globaltimer();
     if (!live) goto done;
     tc_fence_after();
-    uint32_t o[2][32];
-    tmem_ld32_nowait(tmem + lane_base + kColO, o[0]);
-    tmem_ld32_nowait(tmem + lane_base + kColO + 32, o[1]);
-    tmem_wait_ld();
-    if (q0 + row < L) {
-      const float inv = 1.f / l;
-      uint4* out = reinterpret_cast<uint4*>(ctx + (static_cast<long long>(row_base) + q0 + row) * hidden + h * 64);
+    {
+      constexpr int OC = 64 / SPLIT;  // output columns of this thread
+      uint32_t o[OC];
 #pragma unroll
-      for (int v = 0; v < 8; ++v) {
-        uint32_t w[4];
+      for (int c = 0; c < OC / 32; ++c)
+        tmem_ld32_nowait(tmem + lane_base + kColO + hf * OC + 32 * c, *reinterpret_cast<uint32_t(*)[32]>(o + 32 * c));
+      tmem_wait_ld();
+      if (q0 + row < L) {
+        const float inv = 1.f / l;
+        uint4* out = reinterpret_cast<uint4*>(ctx + (static_cast<long long>(row_base) + q0 + row) * hidden + h * 64 +
+                                              hf * OC);
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int e = v * 8 + 2 * i;
-          __half2 hv = __floats2half2_rn(__uint_as_float(o[e >> 5][e & 31]) * inv,
-                                         __uint_as_float(o[(e + 1) >> 5][(e + 1) & 31]) * inv);
-          w[i] = *reinterpret_cast<uint32_t*>(&hv);
+        for (int v = 0; v < OC / 8; ++v) {
+          uint32_t w[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            __half2 hv = __floats2half2_rn(__uint_as_float(o[v * 8 + 2 * i]) * inv,
+                                           __uint_as_float(o[v * 8 + 2 * i + 1]) * inv);
+            w[i] = *reinterpret_cast<uint32_t*>(&hv);
+          }
+          out[v] = make_uint4(w[0], w[1], w[2], w[3]);
         }
-        out[v] = make_uint4(w[0], w[1], w[2], w[3]);
       }
     }
   }
@@ -295,30 +331,44 @@ done:
   if (TRACE && threadIdx.x == 0) tr[15] = globaltimer();
 }
 
-size_t attn_tc2_smem_bytes() { return 1024 + 5 * kTile + 128; }
+size_t attn_tc2_smem_bytes() { return 1024 + 5 * kTile + 128 + 3 * 1024; }
 
 static unsigned long long* g_attn_trace = nullptr;
 void set_attn_trace(unsigned long long* buf) { g_attn_trace = buf; }
 
-void launch_attention_tc2(const CUtensorMap& map_qkv, half* ctx, const int* cu_seqlens, int n_seqs, int max_len,
-                          int groups, int n_heads, int hidden, long long group_rows, cudaStream_t stream) {
-  if (n_seqs <= 0 || max_len <= 0 || groups <= 0) return;
+template <int SPLIT>
+static void launch_tc2_t(const CUtensorMap& map_qkv, half* ctx, const int* cu_seqlens, dim3 grid, int n_heads,
+                         int hidden, long long group_rows, float scale_log2, cudaStream_t stream) {
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(attn_tc2_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(attn_tc2_kernel<false, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(attn_tc2_smem_bytes()));
-    cudaFuncSetAttribute(attn_tc2_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(attn_tc2_kernel<true, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(attn_tc2_smem_bytes()));
     attr_set = true;
   }
-  const float scale_log2 = 1.4426950408889634f / 8.0f;  // log2(e) / sqrt(64)
-  dim3 grid(groups * n_heads, n_seqs, (max_len + 127) / 128);
+  const dim3 block(Tc2Cfg<SPLIT>::kThreads);
   if (g_attn_trace)
-    launch_pdl(attn_tc2_kernel<true>, grid, dim3(kThreads2), attn_tc2_smem_bytes(), stream, map_qkv, ctx, cu_seqlens,
+    launch_pdl(attn_tc2_kernel<true, SPLIT>, grid, block, attn_tc2_smem_bytes(), stream, map_qkv, ctx, cu_seqlens,
                n_heads, hidden, group_rows, scale_log2, g_attn_trace);
   else
-    launch_pdl(attn_tc2_kernel<false>, grid, dim3(kThreads2), attn_tc2_smem_bytes(), stream, map_qkv, ctx, cu_seqlens,
+    launch_pdl(attn_tc2_kernel<false, SPLIT>, grid, block, attn_tc2_smem_bytes(), stream, map_qkv, ctx, cu_seqlens,
                n_heads, hidden, group_rows, scale_log2, static_cast<unsigned long long*>(nullptr));
+}
+
+void launch_attention_tc2(const CUtensorMap& map_qkv, half* ctx, const int* cu_seqlens, int n_seqs, int max_len,
+                          int groups, int n_heads, int hidden, long long group_rows, cudaStream_t stream) {
+  if (n_seqs <= 0 || max_len <= 0 || groups <= 0) return;
+  static const int split = [] {  // SP_ATTN_SPLIT: softmax warps per TMEM lane quadrant (1 or 2)
+    const char* v = getenv("SP_ATTN_SPLIT");
+    return v ? atoi(v) : 2;
+  }();
+  const float scale_log2 = 1.4426950408889634f / 8.0f;  // log2(e) / sqrt(64)
+  dim3 grid(groups * n_heads, n_seqs, (max_len + 127) / 128);
+  if (split == 1)
+    launch_tc2_t<1>(map_qkv, ctx, cu_seqlens, grid, n_heads, hidden, group_rows, scale_log2, stream);
+  else
+    launch_tc2_t<2>(map_qkv, ctx, cu_seqlens, grid, n_heads, hidden, group_rows, scale_log2, stream);
 }
 
 }  // namespace sp
