@@ -62,6 +62,23 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32
       "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
       : "memory");
 }
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr)
+      : "memory");
+}
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 __device__ __forceinline__ float ex2(float x) {
@@ -369,6 +386,242 @@ void launch_attention_tc2(const CUtensorMap& map_qkv, half* ctx, const int* cu_s
     launch_tc2_t<1>(map_qkv, ctx, cu_seqlens, grid, n_heads, hidden, group_rows, scale_log2, stream);
   else
     launch_tc2_t<2>(map_qkv, ctx, cu_seqlens, grid, n_heads, hidden, group_rows, scale_log2, stream);
+}
+
+
+// ---------------------------------------------------------------------------------------------
+// Variant "tc3": 64-key chunks, three CTAs per SM (192 threads <= 113 registers, 51 KiB smem,
+// 128 TMEM columns: S in [0, 64) with P written back over its first 32 columns, O in [64, 128)).
+// With P aliased into S the next chunk's scores are issued after O += P V (in-order tensor pipe),
+// so a CTA's chunks are serial; the third resident CTA per SM supplies the overlap, and up to 444
+// CTAs (L <= 512: 4 query tiles x 96 heads = 384) run in one wave. Because S_j is issued after
+// PV_{j-1}, scores ready implies the previous PV finished: the softmax may rescale O right away.
+// Thread = query row (4 softmax warps), 64 keys per chunk; producer warp, MMA warp.
+namespace {
+constexpr int kKv64 = 64 * 64 * 2;  // 64 keys x 64 dims fp16 = 8 KiB
+constexpr int kT3Threads = 192;
+constexpr uint32_t k3ColS = 0, k3ColO = 64;
+}  // namespace
+
+__global__ void __launch_bounds__(kT3Threads, 3)
+    attn_tc3_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_kv,
+                    half* __restrict__ ctx, const int* __restrict__ cu, int n_heads, int hidden, long long group_rows,
+                    float scale_log2) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;                 // 16 KiB
+  uint8_t* sK = sQ + kTile;           // [2] x 8 KiB
+  uint8_t* sV = sK + 2 * kKv64;       // [2] x 8 KiB
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + 2 * kKv64);
+  uint64_t* q_full = bars;
+  uint64_t* kv_full = bars + 1;   // [2]
+  uint64_t* kv_empty = bars + 3;  // [2]
+  uint64_t* s_full = bars + 5;
+  uint64_t* p_full = bars + 6;
+  uint64_t* pv_done = bars + 7;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
+
+  pdl_launch_dependents();
+  const int b = blockIdx.y;
+  const int s0 = __ldg(cu + b);  // request input: read before the dependency wait
+  const int L = __ldg(cu + b + 1) - s0;
+  const int q0 = blockIdx.z * 128;
+  if (q0 >= L) return;
+  const int g = blockIdx.x / n_heads;
+  const int h = blockIdx.x % n_heads;
+  const int n_chunks = (L + 63) >> 6;
+  const int row_base = static_cast<int>(g * group_rows + s0);
+  const int warp = warp_id();
+  const int lane = lane_id();
+  constexpr int kProd3 = 4, kMma3 = 5;
+
+  if (warp == kProd3 && lane == 0) {
+    mbar_init(q_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
+    }
+    mbar_init(s_full, 1);
+    mbar_init(p_full, 4);
+    mbar_init(pv_done, 1);
+    fence_barrier_init();
+    tma_prefetch_desc(&map_q);
+    tma_prefetch_desc(&map_kv);
+  }
+  if (warp == kMma3) {
+    tmem_alloc(tmem_slot, 128);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == kProd3) {
+    if (elect_one()) {
+      const uint64_t pol = policy_evict_last();
+      pdl_wait();  // qkv is the previous kernel's output
+      mbar_arrive_expect_tx(q_full, kTile);
+      tma_load_2d(&map_q, q_full, sQ, h * 64, row_base + q0, pol);
+      for (int j = 0; j < n_chunks; ++j) {
+        const int st = j & 1;
+        if (j >= 2) mbar_wait(&kv_empty[st], ((j >> 1) - 1) & 1);
+        mbar_arrive_expect_tx(&kv_full[st], 2 * kKv64);
+        tma_load_2d(&map_kv, &kv_full[st], sK + st * kKv64, hidden + h * 64, row_base + j * 64, pol);
+        tma_load_2d(&map_kv, &kv_full[st], sV + st * kKv64, 2 * hidden + h * 64, row_base + j * 64, pol);
+      }
+    }
+    __syncwarp();
+  } else if (warp == kMma3) {
+    if (elect_one()) {
+      const uint32_t idesc_s = umma_idesc_f16(128, 64);
+      const uint32_t idesc_o = umma_idesc_f16(128, 64) | (1u << 16);  // B (= V) is MN-major
+      const uint64_t qdesc = umma_sdesc_sw128(smem_u32(sQ));
+      mbar_wait(q_full, 0);
+      auto issue_s = [&](int j) {
+        mbar_wait(&kv_full[j & 1], (j >> 1) & 1);
+        tc_fence_after();
+        const uint64_t kdesc = umma_sdesc_sw128(smem_u32(sK + (j & 1) * kKv64));
+#pragma unroll
+        for (int k = 0; k < 4; ++k) umma_f16_ss(tmem + k3ColS, qdesc + 2 * k, kdesc + 2 * k, idesc_s, k > 0 ? 1u : 0u);
+        umma_commit(s_full);
+      };
+      issue_s(0);
+      for (int j = 0; j < n_chunks; ++j) {
+        mbar_wait(p_full, j & 1);  // P_j is in TMEM columns [0, 32)
+        tc_fence_after();
+        const uint8_t* vb = sV + (j & 1) * kKv64;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)  // 16 keys per step: P columns 8k.. (2 fp16 each), V rows 16k..
+          umma_f16_ts(tmem + k3ColO, tmem + k3ColS + 8 * k, umma_sdesc_sw128(smem_u32(vb + k * 2048)), idesc_o,
+                      (j > 0 || k > 0) ? 1u : 0u);
+        umma_commit(pv_done);
+        umma_commit(&kv_empty[j & 1]);
+        if (j + 1 < n_chunks) issue_s(j + 1);  // after PV_j in the tensor pipe: P_j is consumed first
+      }
+    }
+    __syncwarp();
+  } else {
+    const int row = warp * 32 + lane;
+    const uint32_t lane_base = static_cast<uint32_t>(warp * 32) << 16;
+    const bool live = q0 + warp * 32 < L;
+    float m = 0.f, l = 0.f;
+    for (int j = 0; j < n_chunks; ++j) {
+      mbar_wait(s_full, j & 1);  // also: PV_{j-1} has completed (issued before S_j)
+      if (!live) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(p_full);
+        continue;
+      }
+      tc_fence_after();
+      uint32_t r[2][32];
+      tmem_ld32_nowait(tmem + lane_base + k3ColS, r[0]);
+      tmem_ld32_nowait(tmem + lane_base + k3ColS + 32, r[1]);
+      tmem_wait_ld();
+      const int valid = L - j * 64;
+      if (valid < 64) {
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (32 * c + i >= valid) r[c][i] = __float_as_uint(-INFINITY);
+      }
+      float mx = -INFINITY;
+#pragma unroll
+      for (int c = 0; c < 2; ++c)
+#pragma unroll
+        for (int i = 0; i < 32; ++i) mx = fmaxf(mx, __uint_as_float(r[c][i]));
+      mx *= scale_log2;
+      float alpha = 1.f;
+      if (j == 0) {
+        m = mx;
+      } else if (mx > m + kRescaleLog2) {
+        alpha = ex2(m - mx);
+        m = mx;
+        l *= alpha;
+      }
+      const float neg_m = -m;
+      float ps = 0.f;
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {  // P over the (already read) scores, 16 packed columns at a time
+        uint32_t pk[16];
+#pragma unroll
+        for (int i = 0; i < 32; i += 2) {
+          const float p0 = ex2(fmaf(__uint_as_float(r[c][i]), scale_log2, neg_m));
+          const float p1 = ex2(fmaf(__uint_as_float(r[c][i + 1]), scale_log2, neg_m));
+          ps += p0 + p1;
+          __half2 hp = __floats2half2_rn(p0, p1);
+          pk[i >> 1] = *reinterpret_cast<uint32_t*>(&hp);
+        }
+        tmem_st16(tmem + lane_base + k3ColS + 16 * c, pk);
+      }
+      l += ps;
+      if (j >= 1 && __any_sync(0xffffffffu, alpha != 1.f)) {  // rare: rescale this warp's O rows
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t o[16];
+          tmem_ld16_nowait(tmem + lane_base + k3ColO + 16 * c, o);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+          tmem_st16(tmem + lane_base + k3ColO + 16 * c, o);
+        }
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(p_full);
+    }
+    mbar_wait(pv_done, (n_chunks - 1) & 1);
+    if (live) {
+      tc_fence_after();
+      const float inv = 1.f / l;
+      uint4* out = reinterpret_cast<uint4*>(ctx + (static_cast<long long>(row_base) + q0 + row) * hidden + h * 64);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {  // 16 output columns at a time
+        uint32_t o[16];
+        tmem_ld16_nowait(tmem + lane_base + k3ColO + 16 * c, o);
+        tmem_wait_ld();
+        if (q0 + row < L) {
+#pragma unroll
+          for (int v = 0; v < 2; ++v) {
+            uint32_t w[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              __half2 hv = __floats2half2_rn(__uint_as_float(o[v * 8 + 2 * i]) * inv,
+                                             __uint_as_float(o[v * 8 + 2 * i + 1]) * inv);
+              w[i] = *reinterpret_cast<uint32_t*>(&hv);
+            }
+            out[2 * c + v] = make_uint4(w[0], w[1], w[2], w[3]);
+          }
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == kMma3) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 128);
+  }
+}
+
+size_t attn_tc3_smem_bytes() { return 1024 + kTile + 4 * kKv64 + 128; }
+
+void launch_attention_tc3(const CUtensorMap& map_q, const CUtensorMap& map_kv, half* ctx, const int* cu_seqlens,
+                          int n_seqs, int max_len, int groups, int n_heads, int hidden, long long group_rows,
+                          cudaStream_t stream) {
+  if (n_seqs <= 0 || max_len <= 0 || groups <= 0) return;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(attn_tc3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(attn_tc3_smem_bytes()));
+    attr_set = true;
+  }
+  const float scale_log2 = 1.4426950408889634f / 8.0f;
+  dim3 grid(groups * n_heads, n_seqs, (max_len + 127) / 128);
+  launch_pdl(attn_tc3_kernel, grid, dim3(kT3Threads), attn_tc3_smem_bytes(), stream, map_q, map_kv, ctx, cu_seqlens,
+             n_heads, hidden, group_rows, scale_log2);
 }
 
 }  // namespace sp

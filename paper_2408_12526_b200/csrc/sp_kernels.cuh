@@ -143,7 +143,11 @@ void launch_attention_tc(const CUtensorMap& map_qkv, half* ctx, const int* cu_se
 void launch_attention_tc2(const CUtensorMap& map_qkv, half* ctx, const int* cu_seqlens, int n_seqs, int max_len,
                           int groups, int n_heads, int hidden, long long group_rows, cudaStream_t stream);
 
-void set_attn_trace(unsigned long long* buf);  // debug: per-CTA timeline of attn_tc2 (16 stamps)
+void set_attn_trace(unsigned long long* buf);
+// 64-key-chunk variant, three CTAs per SM; map_kv: the qkv buffer with a {64, 64} box.
+void launch_attention_tc3(const CUtensorMap& map_q, const CUtensorMap& map_kv, half* ctx, const int* cu_seqlens,
+                          int n_seqs, int max_len, int groups, int n_heads, int hidden, long long group_rows,
+                          cudaStream_t stream);  // debug: per-CTA timeline of attn_tc2 (16 stamps)
 
 // Embedding gather + LayerNorm: x = LN(E_word[g][id_t] + E_pos[g][pos_t] + E_type[g][0]).
 void launch_embed_ln(const int* ids, const int* cu_seqlens, int n_seqs, int n_tokens, int groups,

@@ -159,6 +159,7 @@ struct sp_group {
   std::vector<CUtensorMap> m_qkv, m_o, m_f1, m_f2, m_layers;
   CUtensorMap m_pool, m_in;
   CUtensorMap m_qkv_attn;  // qkv buffer viewed with a {64, 128} box (tensor-core attention)
+  CUtensorMap m_qkv_kv64;  // the same with a {64, 64} box (64-key chunks of the three-CTA kernel)
   XMaps xm_x16, xm_ctx, xm_ffn, xm_cls, xm_ha, xm_hb;
   int last_launches = 0;
   // CUDA graphs of the batch-1 host path, keyed by (16-token bucket, k_active, add_bias)
@@ -352,6 +353,7 @@ int sp_group_create(const sp_config* cfg, const sp_weights* weights, int device,
     ok &= make_xmaps(&g->xm_ffn, g->ffn, S * T, F);
     ok &= make_xmaps(&g->xm_cls, g->cls16, S * B, H);
     ok &= make_map(&g->m_qkv_attn, g->qkv, S * T, 3 * H, 128);
+    ok &= make_map(&g->m_qkv_kv64, g->qkv, S * T, 3 * H, 64);
     // rows past a request's tokens are read (masked) by the attention tiles: keep them finite
     if (cudaMemset(g->qkv, 0, S * T * 3 * H * sizeof(half)) != cudaSuccess) ok = false;
     if (!ok) return bail(fail(SP_EINVAL, "tensor-map creation failed (pointer alignment / shape)"));
@@ -424,7 +426,8 @@ namespace {
 // (tools/len_probe.py): tcgen05 wins up to 128 keys and beyond 384 (one CTA per SM: at 160-384 the
 // mma.sync kernel's two CTAs per SM win). SP_ATTN_TC=0 / 1 forces either kernel.
 // Attention kernel by length: 0 = mma.sync (sp_attn.cu), 1 = two-pass tcgen05 (sp_attn_tc.cu),
-// 2 = single-pass tcgen05, two CTAs per SM (sp_attn_tc2.cu). SP_ATTN_TC forces one.
+// 2 = single-pass tcgen05, two CTAs per SM, 3 = the same with 64-key chunks at three CTAs per SM
+// (sp_attn_tc2.cu). SP_ATTN_TC forces one.
 int attn_kind(int head_dim, int max_len) {
   static const int mode = [] {
     const char* v = getenv("SP_ATTN_TC");
@@ -432,13 +435,17 @@ int attn_kind(int head_dim, int max_len) {
   }();
   if (head_dim != 64 || max_len > 512) return 0;
   if (mode >= 0) return mode;
-  return max_len <= 128 ? 1 : 2;  // measured in-graph (tools/len_probe.py): tc2 from 129 tokens
+  // measured in-graph (tools/len_probe.py): tc2 from 129 tokens; above 384 (4 query tiles per head)
+  // tc3's one wave at three CTAs per SM beats tc2's two waves (-6..-10 us per request)
+  return max_len <= 128 ? 1 : (max_len <= 384 ? 2 : 3);
 }
 
-void launch_attention_any(int kind, const CUtensorMap& map_qkv, const half* qkv, half* ctx, const int* cu,
-                          int n_seqs, int max_len, int groups, int n_heads, int head_dim, int hidden,
-                          long long group_rows, cudaStream_t st) {
-  if (kind == 2)
+void launch_attention_any(int kind, const CUtensorMap& map_qkv, const CUtensorMap& map_kv64, const half* qkv,
+                          half* ctx, const int* cu, int n_seqs, int max_len, int groups, int n_heads, int head_dim,
+                          int hidden, long long group_rows, cudaStream_t st) {
+  if (kind == 3)
+    sp::launch_attention_tc3(map_qkv, map_kv64, ctx, cu, n_seqs, max_len, groups, n_heads, hidden, group_rows, st);
+  else if (kind == 2)
     sp::launch_attention_tc2(map_qkv, ctx, cu, n_seqs, max_len, groups, n_heads, hidden, group_rows, st);
   else if (kind == 1)
     sp::launch_attention_tc(map_qkv, ctx, cu, n_seqs, max_len, groups, n_heads, hidden, group_rows, st);
@@ -871,7 +878,8 @@ int bert_forward(sp_group* g, const int32_t* ids, const int32_t* cu, int n_seqs,
       launches += run_gemm(g, SP_LAUNCH_GEMM_QKV, g->m_qkv[l], g->xm_x16, k, 3 * H, H, n_tokens, T, w.b_qkv + lS * 3 * H, 3 * H,
                            sp::ACT_NONE, g->qkv, (long long)T * 3 * H, 0, 1, 0, st, t_dev);
       g->rec_begin(SP_LAUNCH_ATTENTION, GTH * 8.0, 4.0 * k * H * g->sum_len_sq);
-      launch_attention_any(attn_kind(H / c.n_heads, max_len), g->m_qkv_attn, g->qkv, g->ctx, cu, n_seqs, max_len, k,
+      launch_attention_any(attn_kind(H / c.n_heads, max_len), g->m_qkv_attn, g->m_qkv_kv64, g->qkv, g->ctx, cu, n_seqs,
+                           max_len, k,
                            c.n_heads, H / c.n_heads, H, T, st);
       g->rec_end();
       ++launches;
@@ -1249,10 +1257,11 @@ int sp_op_attention(const void* qkv, void* ctx, const int32_t* cu_seqlens, int32
   if (n_seqs < 1 || groups < 1 || n_heads < 1 || max_seq_len < 1) return fail(SP_EINVAL, "bad attention shape");
   const int hidden = n_heads * head_dim;
   const int kind = attn_kind(head_dim, max_seq_len);
-  CUtensorMap m{};
-  if (kind != 0 && !make_map(&m, qkv, (uint64_t)groups * group_rows, 3 * hidden, 128))
+  CUtensorMap m{}, m64{};
+  if (kind != 0 && (!make_map(&m, qkv, (uint64_t)groups * group_rows, 3 * hidden, 128) ||
+                    !make_map(&m64, qkv, (uint64_t)groups * group_rows, 3 * hidden, 64)))
     return fail(SP_EINVAL, "attention tensor map failed");
-  launch_attention_any(kind, m, static_cast<const half*>(qkv), static_cast<half*>(ctx), cu_seqlens, n_seqs,
+  launch_attention_any(kind, m, m64, static_cast<const half*>(qkv), static_cast<half*>(ctx), cu_seqlens, n_seqs,
                        max_seq_len, groups, n_heads, head_dim, hidden, group_rows, static_cast<cudaStream_t>(stream));
   SP_CUDA(cudaGetLastError());
   return SP_OK;

@@ -145,7 +145,7 @@ print('ok')
 """
 
 
-@pytest.mark.parametrize("kind", ["0", "1", "2"])
+@pytest.mark.parametrize("kind", ["0", "1", "2", "3"])
 def test_attention_kernels_forced(kind):
     """Every attention kernel (mma.sync, two-pass tcgen05, single-pass two-CTA tcgen05) against the
     fp32 reference at every length class, with and without key scores that rise along the sequence
