@@ -435,8 +435,10 @@ int attn_kind(int head_dim, int max_len) {
   }();
   if (head_dim != 64 || max_len > 512) return 0;
   if (mode >= 0) return mode;
-  // measured in-graph (tools/len_probe.py): tc2 from 129 tokens; above 384 (4 query tiles per head)
-  // tc3's one wave at three CTAs per SM beats tc2's two waves (-6..-10 us per request)
+  // measured in-graph (tools/len_probe.py): tc3 (fewest threads / TMEM columns: the shortest
+  // latency chain) up to 64 tokens (-2 us), tc1 to 128, tc2 from 129; above 384 (4 query tiles per
+  // head) tc3's one wave at three CTAs per SM beats tc2's two waves (-6..-10 us per request)
+  if (max_len <= 64) return 3;
   return max_len <= 128 ? 1 : (max_len <= 384 ? 2 : 3);
 }
 
