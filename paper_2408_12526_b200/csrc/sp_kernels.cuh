@@ -170,7 +170,8 @@ void launch_reduce_ln(const float* part, int splits, long long part_split_stride
 void launch_head(const float* final_rep, long long final_gs, long long split_stride, int splits,
                  const float* b_pool, int groups, const float* alpha, const float* w_cls, const float* b_cls,
                  int n_classes, int hidden, int n_rows, int add_bias, float* rep, float* logits,
-                 cudaStream_t stream, float* finals = nullptr);
+                 cudaStream_t stream, float* finals = nullptr, int* ready_flag = nullptr,
+                 const int* seq_src = nullptr);
 
 // Training-side evaluation (distill.py:483-494): logits of every prefix k = 1..groups from the
 // per-student finals written by launch_head. out [groups][n_rows][n_classes].

@@ -122,7 +122,8 @@ __global__ void __launch_bounds__(1024)
     head_kernel(const float* __restrict__ final_rep, long long final_gs, long long split_stride, int splits,
                 const float* __restrict__ b_pool, int groups, const float* __restrict__ alpha,
                 const float* __restrict__ w_cls, const float* __restrict__ b_cls, int n_classes, int hidden,
-                int add_bias, float* __restrict__ rep, float* __restrict__ logits, float* __restrict__ finals) {
+                int add_bias, float* __restrict__ rep, float* __restrict__ logits, float* __restrict__ finals,
+                int* ready_flag, const int* __restrict__ seq_src) {
   pdl_enter();
   __shared__ float red[32][4];
   const int b = blockIdx.x;
@@ -179,8 +180,14 @@ __global__ void __launch_bounds__(1024)
       for (int w = 0; w < warps; ++w) z += red[w][c];
       if (add_bias) z += b_cls[c0 + c];
       logits[(long long)b * n_classes + c0 + c] = z;
+      if (ready_flag) __threadfence_system();  // logits (mapped host memory) before the flag
     }
     __syncthreads();
+  }
+  // batch-1 host path: publish the request's sequence number to the host-mapped flag it polls
+  if (ready_flag != nullptr && threadIdx.x == 0) {
+    __threadfence_system();
+    *reinterpret_cast<volatile int*>(ready_flag) = __ldg(seq_src);
   }
 }
 
@@ -252,11 +259,11 @@ void launch_reduce_ln(const float* part, int splits, long long part_split_stride
 void launch_head(const float* final_rep, long long final_gs, long long split_stride, int splits,
                  const float* b_pool, int groups, const float* alpha, const float* w_cls, const float* b_cls,
                  int n_classes, int hidden, int n_rows, int add_bias, float* rep, float* logits,
-                 cudaStream_t stream, float* finals) {
+                 cudaStream_t stream, float* finals, int* ready_flag, const int* seq_src) {
   if (n_rows <= 0) return;
   const int threads = ((hidden + 31) / 32) * 32;
   launch_pdl(head_kernel, dim3(n_rows), dim3(threads), 0, stream, final_rep, final_gs, split_stride, splits, b_pool,
-             groups, alpha, w_cls, b_cls, n_classes, hidden, add_bias, rep, logits, finals);
+             groups, alpha, w_cls, b_cls, n_classes, hidden, add_bias, rep, logits, finals, ready_flag, seq_src);
 }
 
 // Logits of every prefix k = 1..groups from the students' final representations — the forward half

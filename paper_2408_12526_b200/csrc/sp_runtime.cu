@@ -147,6 +147,15 @@ struct sp_group {
   int cu_pad = 0;             // max_seqs + 1 rounded up to 32 ints (128 B)
   int32_t* h_stage = nullptr;  // pinned mirror of the staging block: one H2D copy per request
   float* h_logits = nullptr;   // pinned logits landing buffer
+  // batch-1 host path without a stream sync: the head kernel writes the logits into mapped pinned
+  // memory, then the request's sequence number (staged with its ids) into a mapped flag the host
+  // polls; the graph has no device-to-host copy node
+  void* h_mapped = nullptr;     // [logits f32 x n_classes | pad | flag int]
+  float* d_out = nullptr;       // device alias of the logits slot
+  int* d_flag = nullptr;        // device alias of the flag
+  int seq = 0;
+  int* head_flag = nullptr;     // set while capturing a host-path graph
+  const int* head_seq = nullptr;
   float* d_logits = nullptr;
   int* mlp_done = nullptr;  // fused FFN kernel: FFN1 tiles finished per student + exit counter
   // weight streamer (sp_stream.cu): [progress, base, finished CTAs], side stream + fork/join events
@@ -239,6 +248,8 @@ void free_all(sp_group* g) {
   g->allocs.clear();
   if (g->h_stage) cudaFreeHost(g->h_stage);
   if (g->h_logits) cudaFreeHost(g->h_logits);
+  if (g->h_mapped) cudaFreeHost(g->h_mapped);
+  g->h_mapped = nullptr;
   g->h_stage = nullptr;
   g->h_logits = nullptr;
   for (auto& r : g->recs) {
@@ -310,6 +321,16 @@ int sp_group_create(const sp_config* cfg, const sp_weights* weights, int device,
                     cudaHostAllocDefault) != cudaSuccess)
     return bail(fail(SP_ENOMEM, "pinned staging buffers"));
   if ((rc = dev_alloc(g, &g->d_logits, R * c.n_classes))) return bail(rc);
+  {
+    const size_t flag_off = ((sizeof(float) * (size_t)c.n_classes + 127) / 128) * 128;
+    void* dev = nullptr;
+    if (cudaHostAlloc(&g->h_mapped, flag_off + 128, cudaHostAllocMapped) != cudaSuccess ||
+        cudaHostGetDevicePointer(&dev, g->h_mapped, 0) != cudaSuccess)
+      return bail(fail(SP_ENOMEM, "mapped logits buffer"));
+    memset(g->h_mapped, 0, flag_off + 128);
+    g->d_out = static_cast<float*>(dev);
+    g->d_flag = reinterpret_cast<int*>(static_cast<uint8_t*>(dev) + flag_off);
+  }
   if ((rc = dev_alloc(g, &g->mlp_done, sp::kReqMaxStudents + 1))) return bail(rc);
   if (cudaMemset(g->mlp_done, 0, sizeof(int) * (sp::kReqMaxStudents + 1)) != cudaSuccess)
     return bail(fail(SP_ECUDA, "memset"));
@@ -943,7 +964,7 @@ int bert_forward(sp_group* g, const int32_t* ids, const int32_t* cu, int n_seqs,
                                    (double)c.n_classes * H * 4.0 + n_seqs * H * 4.0, 0.0);
   sp::launch_head(g->final32, (long long)g->rows_cap * H, (long long)S * g->rows_cap * H,
                   pool_splits > 1 ? pool_splits : 0, w.b_pool, k, w.alpha, w.w_cls, w.b_cls, c.n_classes, H, n_seqs,
-                  add_bias, rep, logits, st, g->eval_finals);
+                  add_bias, rep, logits, st, g->eval_finals, g->head_flag, g->head_seq);
   g->rec_end();
   ++launches;
   if (ws) {
@@ -985,8 +1006,11 @@ int get_graph(sp_group* g, int n_tokens, int k, int add_bias, cudaGraphExec_t* o
   // kernels read the live length from cu), forward, logits -> pinned
   cudaMemcpyAsync(g->d_cu, g->h_stage, sizeof(int32_t) * ((size_t)g->cu_pad + std::min(bucket, g->cfg.max_tokens)),
                   cudaMemcpyHostToDevice, g->cap_stream);
-  int rc = bert_forward(g, g->d_ids, g->d_cu, 1, bucket, max_len, k, nullptr, g->d_logits, add_bias, g->cap_stream, true);
-  cudaMemcpyAsync(g->h_logits, g->d_logits, sizeof(float) * g->cfg.n_classes, cudaMemcpyDeviceToHost, g->cap_stream);
+  g->head_flag = g->d_flag;  // the head kernel publishes the request's sequence number (staged in
+  g->head_seq = g->d_cu + g->cu_pad - 1;  // the last cu slot) after writing the mapped logits
+  int rc = bert_forward(g, g->d_ids, g->d_cu, 1, bucket, max_len, k, nullptr, g->d_out, add_bias, g->cap_stream, true);
+  g->head_flag = nullptr;
+  g->head_seq = nullptr;
   cudaGraph_t graph = nullptr;
   cudaError_t e = cudaStreamEndCapture(g->cap_stream, &graph);
   if (rc) return rc;
@@ -1198,11 +1222,22 @@ int sp_group_forward_host(sp_group* g, const int32_t* ids, const int32_t* cu, in
   // stream sync, so the previous request no longer reads h_stage.
   memcpy(g->h_stage, cu, sizeof(int32_t) * (n_seqs + 1));
   memcpy(g->h_stage + g->cu_pad, ids, sizeof(int32_t) * n_tokens);
-  if (use_graph) {  // H2D copy, forward and D2H copy are all nodes of the bucket's graph
+  if (use_graph) {  // H2D copy and forward are nodes of the bucket's graph; logits land in mapped memory
+    const int seq = (g->seq = g->seq == 0x7fffffff ? 1 : g->seq + 1);
+    g->h_stage[g->cu_pad - 1] = seq;
     SP_CUDA(cudaGraphLaunch(exec, st));
     g->last_launches = g->graph_launches;
-    SP_CUDA(cudaStreamSynchronize(st));
-    memcpy(logits_out, g->h_logits, sizeof(float) * c.n_classes);
+    const size_t flag_off = ((sizeof(float) * (size_t)c.n_classes + 127) / 128) * 128;
+    volatile int* flag = reinterpret_cast<volatile int*>(static_cast<uint8_t*>(g->h_mapped) + flag_off);
+    for (unsigned spins = 1; *flag != seq; ++spins) {
+      if ((spins & 0xfff) == 0) {  // every few microseconds: surface a failed launch instead of spinning
+        const cudaError_t e = cudaStreamQuery(st);
+        if (e != cudaSuccess && e != cudaErrorNotReady) return fail(SP_ECUDA, "forward: %s", cudaGetErrorString(e));
+        if (e == cudaSuccess && *flag != seq) return fail(SP_ECUDA, "forward finished without publishing its logits");
+      }
+    }
+    const volatile float* out = static_cast<const volatile float*>(g->h_mapped);
+    for (int i = 0; i < c.n_classes; ++i) logits_out[i] = out[i];
     return SP_OK;
   }
   SP_CUDA(cudaMemcpyAsync(g->d_cu, g->h_stage, sizeof(int32_t) * ((size_t)g->cu_pad + n_tokens),
