@@ -70,7 +70,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   const int split = bid / p.n_tiles;
   const bool pair = p.cluster == 2;
   const uint32_t crank = pair ? cluster_ctarank() : 0u;
-  const int g = blockIdx.y;
+  const int g = blockIdx.y + p.g0;
   const int m0 = mt * kBlockM;
   const int n0 = nt * p.bn;
   const int nkb = p.k_dim / kBlockK;
@@ -339,7 +339,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
   pdl_launch_dependents();
 
   auto decode = [&](int u, int& g, int& mt, int& nt) {
-    g = u / units_per_group;
+    g = u / units_per_group + p.g0;
     const int r = u % units_per_group;
     nt = r / m_per;
     mt = pair ? 2 * (r % m_per) + static_cast<int>(crank) : r % m_per;

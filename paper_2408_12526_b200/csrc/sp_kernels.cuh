@@ -69,6 +69,7 @@ struct GemmParams {
   const int* t_dev;           // if set: live token count (device), t_rows is only the tile bound
   int direct_store;           // persistent epilogue: warp-wide stores from registers (no smem staging)
   int epi_warps;              // small-T kernel: 4 or 8 epilogue warps (gemm_epi_warps)
+  int g0;                     // first student of the launch (student-split request chains)
   unsigned long long* progress;  // weight streamer pacing (sp_stream.cu): += weight bytes requested, or null
 };
 

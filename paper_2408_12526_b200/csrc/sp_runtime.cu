@@ -169,6 +169,11 @@ struct sp_group {
   CUtensorMap m_pool, m_in;
   CUtensorMap m_qkv_attn;  // qkv buffer viewed with a {64, 128} box (tensor-core attention)
   CUtensorMap m_qkv_kv64;  // the same with a {64, 64} box (64-key chunks of the three-CTA kernel)
+  // the two maps with their origin at student g0 (second chain of a student-split request)
+  std::vector<CUtensorMap> m_qkv_attn_at, m_qkv_kv64_at;
+  // student-split batch-1 requests: the second half of the students runs as its own kernel chain
+  cudaStream_t chain_stream = nullptr;
+  cudaEvent_t chain_fork = nullptr, chain_join = nullptr;
   XMaps xm_x16, xm_ctx, xm_ffn, xm_cls, xm_ha, xm_hb;
   int last_launches = 0;
   // CUDA graphs of the batch-1 host path, keyed by (16-token bucket, k_active, add_bias)
@@ -239,6 +244,9 @@ void free_all(sp_group* g) {
   for (auto& kv : g->graphs) cudaGraphExecDestroy(kv.second);
   for (auto& kv : g->dgraphs) cudaGraphExecDestroy(kv.second);
   if (g->ws_stream) cudaStreamDestroy(g->ws_stream);
+  if (g->chain_stream) cudaStreamDestroy(g->chain_stream);
+  if (g->chain_fork) cudaEventDestroy(g->chain_fork);
+  if (g->chain_join) cudaEventDestroy(g->chain_join);
   if (g->ws_fork) cudaEventDestroy(g->ws_fork);
   if (g->ws_join) cudaEventDestroy(g->ws_join);
   g->graphs.clear();
@@ -375,6 +383,16 @@ int sp_group_create(const sp_config* cfg, const sp_weights* weights, int device,
     ok &= make_xmaps(&g->xm_cls, g->cls16, S * B, H);
     ok &= make_map(&g->m_qkv_attn, g->qkv, S * T, 3 * H, 128);
     ok &= make_map(&g->m_qkv_kv64, g->qkv, S * T, 3 * H, 64);
+    g->m_qkv_attn_at.resize(S);
+    g->m_qkv_kv64_at.resize(S);
+    for (int s0 = 0; s0 < S; ++s0) {
+      const half* base = g->qkv + (size_t)s0 * T * 3 * H;
+      ok &= make_map(&g->m_qkv_attn_at[s0], base, (uint64_t)(S - s0) * T, 3 * H, 128);
+      ok &= make_map(&g->m_qkv_kv64_at[s0], base, (uint64_t)(S - s0) * T, 3 * H, 64);
+    }
+    ok &= cudaStreamCreateWithFlags(&g->chain_stream, cudaStreamNonBlocking) == cudaSuccess &&
+          cudaEventCreateWithFlags(&g->chain_fork, cudaEventDisableTiming) == cudaSuccess &&
+          cudaEventCreateWithFlags(&g->chain_join, cudaEventDisableTiming) == cudaSuccess;
     // rows past a request's tokens are read (masked) by the attention tiles: keep them finite
     if (cudaMemset(g->qkv, 0, S * T * 3 * H * sizeof(half)) != cudaSuccess) ok = false;
     if (!ok) return bail(fail(SP_EINVAL, "tensor-map creation failed (pointer alignment / shape)"));
@@ -479,7 +497,8 @@ void launch_attention_any(int kind, const CUtensorMap& map_qkv, const CUtensorMa
 // Launch one grouped projection. Returns the number of kernels launched (1).
 int run_gemm(sp_group* grp, int kind, const CUtensorMap& wmap, const XMaps& xm, int groups, int n_out, int k_dim,
              int t_rows, int x_group_rows, const float* bias, int bias_gs, int act, void* out, long long out_gs,
-             int out_f32, int splits, long long split_stride, cudaStream_t st, const int* t_dev = nullptr) {
+             int out_f32, int splits, long long split_stride, cudaStream_t st, const int* t_dev = nullptr,
+             int g0 = 0) {
   static const int persist_min_rows = [] {
     const char* v = getenv("SP_GEMM_PERSIST_MIN_ROWS");  // one-split projections from 17 tokens on: measured
     return v ? atoi(v) : 17;                                 // equal or 2-4 us faster than the small-T kernel
@@ -490,6 +509,7 @@ int run_gemm(sp_group* grp, int kind, const CUtensorMap& wmap, const XMaps& xm, 
   }();
   if (splits == 1 && t_rows >= persist_min_rows) {
     sp::GemmParams p{};
+    p.g0 = g0;
     p.progress = grp ? grp->ws_active : nullptr;
     p.l2_prefetch = l2_prefetch;
     p.t_dev = t_dev;
@@ -537,6 +557,7 @@ int run_gemm(sp_group* grp, int kind, const CUtensorMap& wmap, const XMaps& xm, 
     return 1;
   }
   sp::GemmParams p{};
+  p.g0 = g0;
   p.progress = grp ? grp->ws_active : nullptr;
   p.l2_prefetch = l2_prefetch;
   p.t_dev = t_dev;
@@ -849,6 +870,20 @@ int weight_stream_end(sp_group* g, cudaStream_t st) {
   return SP_OK;
 }
 
+// Kernel chains per request (see bert_forward): opt-in SP_CHAINS=2 for 17..112-token requests.
+// Measured: in graph replay -2..-5.5 us at 32..96 tokens, equal at 16, +2.5..8 us at 112..128; in the
+// eager launch path (twice the host launches) -1.7% req/s on the bench mix, so off by default.
+int request_chains(const sp_group* g, int n_tokens, int k) {
+  static const int chains = env_int("SP_CHAINS", 1);
+  static const int min_tokens = env_int("SP_CHAINS_MIN_TOKENS", 17);
+  static const int max_tokens = env_int("SP_CHAINS_MAX_TOKENS", 112);
+  static const bool ln_fused = env_int("SP_LN_FUSE", 0) != 0;
+  if (chains < 2 || k < 2 || n_tokens < min_tokens || n_tokens > max_tokens || n_tokens > 128 || ln_fused ||
+      g->profiling || g->ws_active)
+    return 1;
+  return 2;
+}
+
 int bert_forward(sp_group* g, const int32_t* ids, const int32_t* cu, int n_seqs, int n_tokens, int max_len, int k,
                  float* rep, float* logits, int add_bias, cudaStream_t st, bool dyn = false) {
   const int n_rows_arg = dyn ? -n_tokens : n_tokens;  // row kernels: negative = live count on device
@@ -893,31 +928,46 @@ int bert_forward(sp_group* g, const int32_t* ids, const int32_t* cu, int n_seqs,
     ++launches;
     int bn, n_tiles, stages;
     sp::gemm_configure_tiles(n_tokens, false, &bn, &n_tiles, &stages);
-    const int s_o = choose_splits(k * (H / 128) * n_tiles, H / 64, kMaxSplits);
-    const int s_f = choose_splits(k * (H / 128) * n_tiles, F / 64, kMaxSplits);
     const long long part_ss = (long long)S * xgs;
-    for (int l = 0; l < c.n_layers; ++l) {
+    // Student-split request (short requests, SP_CHAINS=2): the students' second half runs as its own
+    // kernel chain on a second stream, one projection behind the first, so each chain's latency-bound
+    // stages (attention, LayerNorm, fills and drains) overlap the other's weight streaming. Students
+    // are independent until the head, which sums them in order after the join.
+    const int n_chains = request_chains(g, n_tokens, k);
+    const int kc0 = n_chains == 2 ? (k + 1) / 2 : k;
+    struct Chain {
+      int g0, kc;
+      cudaStream_t cs;
+    } chains[2] = {{0, kc0, st}, {kc0, k - kc0, g->chain_stream}};
+    auto layer = [&](const Chain& ch, int l, bool fork_after_qkv) {
+      const int g0 = ch.g0, kc = ch.kc;
+      cudaStream_t cs = ch.cs;
+      const double GTHc = (double)kc * n_tokens * H;
+      const int s_o = choose_splits(kc * (H / 128) * n_tiles, H / 64, kMaxSplits);
+      const int s_f = choose_splits(kc * (H / 128) * n_tiles, F / 64, kMaxSplits);
       const size_t lS = (size_t)l * S;
-      launches += run_gemm(g, SP_LAUNCH_GEMM_QKV, g->m_qkv[l], g->xm_x16, k, 3 * H, H, n_tokens, T, w.b_qkv + lS * 3 * H, 3 * H,
-                           sp::ACT_NONE, g->qkv, (long long)T * 3 * H, 0, 1, 0, st, t_dev);
-      g->rec_begin(SP_LAUNCH_ATTENTION, GTH * 8.0, 4.0 * k * H * g->sum_len_sq);
-      launch_attention_any(attn_kind(H / c.n_heads, max_len), g->m_qkv_attn, g->m_qkv_kv64, g->qkv, g->ctx, cu, n_seqs,
-                           max_len, k,
-                           c.n_heads, H / c.n_heads, H, T, st);
+      const long long o16 = (long long)g0 * xgs;  // activation offset of the chain's first student
+      launches += run_gemm(g, SP_LAUNCH_GEMM_QKV, g->m_qkv[l], g->xm_x16, kc, 3 * H, H, n_tokens, T, w.b_qkv + lS * 3 * H,
+                           3 * H, sp::ACT_NONE, g->qkv, (long long)T * 3 * H, 0, 1, 0, cs, t_dev, g0);
+      if (fork_after_qkv) cudaEventRecord(g->chain_fork, cs);
+      g->rec_begin(SP_LAUNCH_ATTENTION, GTHc * 8.0, 4.0 * kc * H * g->sum_len_sq);
+      launch_attention_any(attn_kind(H / c.n_heads, max_len), g->m_qkv_attn_at[g0], g->m_qkv_kv64_at[g0],
+                           g->qkv + (size_t)g0 * T * 3 * H, g->ctx + o16, cu, n_seqs, max_len, kc, c.n_heads,
+                           H / c.n_heads, H, T, cs);
       g->rec_end();
       ++launches;
       // O and FFN2 write raw partial sums; the reduce+LN kernel owns bias, residual and LayerNorm
-      if (use_ln_fused(H / 128, n_tiles, k, H, H)) {
+      if (use_ln_fused(H / 128, n_tiles, kc, H, H)) {
         sp::LnParams ln{w.b_o + lS * H, w.ln1_gamma + lS * H, w.ln1_beta + lS * H, c.ln_eps, g->x32, g->x16, xgs,
                         nullptr, 0, cu, n_seqs, H};
-        launches += run_gemm_ln(g, SP_LAUNCH_GEMM_O, g->m_o[l], g->xm_ctx, k, H, H, n_tokens, T, ln, t_dev, st);
+        launches += run_gemm_ln(g, SP_LAUNCH_GEMM_O, g->m_o[l], g->xm_ctx, kc, H, H, n_tokens, T, ln, t_dev, cs);
       } else {
-        launches += run_gemm(g, SP_LAUNCH_GEMM_O, g->m_o[l], g->xm_ctx, k, H, H, n_tokens, T, nullptr, H, sp::ACT_NONE,
-                             g->part, xgs, 1, s_o, part_ss, st, t_dev);
-        g->rec_begin(SP_LAUNCH_REDUCE_LN, GTH * (4.0 * s_o + 10.0), 0.0);
-        sp::launch_reduce_ln(g->part, s_o, part_ss, w.b_o + lS * H, w.ln1_gamma + lS * H, w.ln1_beta + lS * H, H,
-                             c.ln_eps, g->x32, g->x16, xgs, n_rows_arg, k, cu, n_seqs, nullptr, 0, st,
-                             PF(pf(w1 + lS * F * H, (size_t)k * F * H)));
+        launches += run_gemm(g, SP_LAUNCH_GEMM_O, g->m_o[l], g->xm_ctx, kc, H, H, n_tokens, T, nullptr, H,
+                             sp::ACT_NONE, g->part, xgs, 1, s_o, part_ss, cs, t_dev, g0);
+        g->rec_begin(SP_LAUNCH_REDUCE_LN, GTHc * (4.0 * s_o + 10.0), 0.0);
+        sp::launch_reduce_ln(g->part + o16, s_o, part_ss, w.b_o + (lS + g0) * H, w.ln1_gamma + (lS + g0) * H,
+                             w.ln1_beta + (lS + g0) * H, H, c.ln_eps, g->x32 + o16, g->x16 + o16, xgs, n_rows_arg, kc,
+                             cu, n_seqs, nullptr, 0, cs, PF(pf(w1 + lS * F * H, (size_t)k * F * H)));
         g->rec_end();
         ++launches;
       }
@@ -925,40 +975,57 @@ int bert_forward(sp_group* g, const int32_t* ids, const int32_t* cu, int n_seqs,
       // (only where FFN2 itself would be a one-split persistent GEMM: measured -2% at L=512, but
       // +3% at L=256 where FFN2's split-K tiles beat the fused kernel's 96-token phase-B tiles)
       const bool mlp = mlp_fusion_enabled() && s_f == 1 && n_tokens >= 129 &&
-                       !sp::gemm_persistent_pair(n_tokens, F / 128, k) && !sp::gemm_persistent_pair(n_tokens, H / 128, k) &&
-                       !use_ln_fused(H / 128, n_tiles, k, F, H);
+                       !sp::gemm_persistent_pair(n_tokens, F / 128, kc) &&
+                       !sp::gemm_persistent_pair(n_tokens, H / 128, kc) && !use_ln_fused(H / 128, n_tiles, kc, F, H);
       if (mlp) {
-        launches += run_mlp(g, l, k, n_tokens, t_dev, st);
+        launches += run_mlp(g, l, kc, n_tokens, t_dev, cs);  // (single-chain requests only: >= 129 tokens)
       } else {
-        launches += run_gemm(g, SP_LAUNCH_GEMM_FFN1, g->m_f1[l], g->xm_x16, k, F, H, n_tokens, T, w.b_ffn1 + lS * F, F,
-                             sp::ACT_GELU, g->ffn, (long long)T * F, 0, 1, 0, st, t_dev);
+        launches += run_gemm(g, SP_LAUNCH_GEMM_FFN1, g->m_f1[l], g->xm_x16, kc, F, H, n_tokens, T, w.b_ffn1 + lS * F,
+                             F, sp::ACT_GELU, g->ffn, (long long)T * F, 0, 1, 0, cs, t_dev, g0);
       }
       const bool last = (l == c.n_layers - 1);
-      if (!mlp && use_ln_fused(H / 128, n_tiles, k, F, H)) {
+      if (!mlp && use_ln_fused(H / 128, n_tiles, kc, F, H)) {
         sp::LnParams ln{w.b_ffn2 + lS * H, w.ln2_gamma + lS * H, w.ln2_beta + lS * H, c.ln_eps, g->x32, g->x16, xgs,
                         last ? g->cls16 : nullptr, (long long)B * H, cu, n_seqs, H};
-        launches += run_gemm_ln(g, SP_LAUNCH_GEMM_FFN2, g->m_f2[l], g->xm_ffn, k, H, F, n_tokens, T, ln, t_dev, st);
+        launches += run_gemm_ln(g, SP_LAUNCH_GEMM_FFN2, g->m_f2[l], g->xm_ffn, kc, H, F, n_tokens, T, ln, t_dev, cs);
       } else {
         if (!mlp)
-          launches += run_gemm(g, SP_LAUNCH_GEMM_FFN2, g->m_f2[l], g->xm_ffn, k, H, F, n_tokens, T, nullptr, H,
-                               sp::ACT_NONE, g->part, xgs, 1, s_f, part_ss, st, t_dev);
+          launches += run_gemm(g, SP_LAUNCH_GEMM_FFN2, g->m_f2[l], g->xm_ffn, kc, H, F, n_tokens, T, nullptr, H,
+                               sp::ACT_NONE, g->part, xgs, 1, s_f, part_ss, cs, t_dev, g0);
         const int s_ln2 = mlp ? 1 : s_f;  // the fused MLP kernel writes one (complete) projection
-        g->rec_begin(SP_LAUNCH_REDUCE_LN, GTH * (4.0 * s_ln2 + 10.0), 0.0);
-        sp::launch_reduce_ln(g->part, s_ln2, part_ss, w.b_ffn2 + lS * H, w.ln2_gamma + lS * H, w.ln2_beta + lS * H, H,
-                             c.ln_eps, g->x32, g->x16, xgs, n_rows_arg, k, cu, n_seqs, last ? g->cls16 : nullptr,
-                             (long long)B * H, st,
-                             PF(last ? pf(w.w_pool, (size_t)k * H * H) : pf(wq + (lS + S) * 3 * H * H, (size_t)k * 3 * H * H)));
+        g->rec_begin(SP_LAUNCH_REDUCE_LN, GTHc * (4.0 * s_ln2 + 10.0), 0.0);
+        sp::launch_reduce_ln(g->part + o16, s_ln2, part_ss, w.b_ffn2 + (lS + g0) * H, w.ln2_gamma + (lS + g0) * H,
+                             w.ln2_beta + (lS + g0) * H, H, c.ln_eps, g->x32 + o16, g->x16 + o16, xgs, n_rows_arg,
+                             kc, cu, n_seqs, last ? g->cls16 + (long long)g0 * B * H : nullptr, (long long)B * H, cs,
+                             PF(last ? pf(w.w_pool, (size_t)k * H * H)
+                                     : pf(wq + (lS + S) * 3 * H * H, (size_t)k * 3 * H * H)));
         g->rec_end();
         ++launches;
       }
-    }
+    };
     // pooler on the CLS rows: tanh(W_p h_CLS + b_p). Few rows: split-K partials (more CTAs stream the
-    // pooler weights), finished by the head kernel; many rows: one pass with the tanh epilogue.
+    // pooler weights), finished by the head kernel (one split count for both chains); many rows: one
+    // pass with the tanh epilogue.
     const int s_p = n_seqs <= 128 ? choose_splits(k * (H / 128), H / 64, kMaxSplits) : 1;
     pool_splits = s_p;
-    launches += run_gemm(g, SP_LAUNCH_GEMM_POOL, g->m_pool, g->xm_cls, k, H, H, n_seqs, B, s_p > 1 ? nullptr : w.b_pool,
-                         H, sp::ACT_TANH, g->final32, (long long)g->rows_cap * H, 1, s_p,
-                         (long long)S * g->rows_cap * H, st);
+    auto pool = [&](const Chain& ch) {
+      launches += run_gemm(g, SP_LAUNCH_GEMM_POOL, g->m_pool, g->xm_cls, ch.kc, H, H, n_seqs, B,
+                           s_p > 1 ? nullptr : w.b_pool, H, sp::ACT_TANH, g->final32, (long long)g->rows_cap * H, 1,
+                           s_p, (long long)S * g->rows_cap * H, ch.cs, nullptr, ch.g0);
+    };
+    for (int l = 0; l < c.n_layers; ++l) {
+      layer(chains[0], l, n_chains == 2 && l == 0);
+      if (n_chains == 2) {
+        if (l == 0) SP_CUDA(cudaStreamWaitEvent(g->chain_stream, g->chain_fork, 0));
+        layer(chains[1], l, false);
+      }
+    }
+    pool(chains[0]);
+    if (n_chains == 2) {
+      pool(chains[1]);
+      SP_CUDA(cudaEventRecord(g->chain_join, g->chain_stream));
+      SP_CUDA(cudaStreamWaitEvent(st, g->chain_join, 0));
+    }
   }
   g->rec_begin(SP_LAUNCH_HEAD, (double)k * n_seqs * H * 4.0 * (pool_splits > 1 ? pool_splits : 1) +
                                    (double)c.n_classes * H * 4.0 + n_seqs * H * 4.0, 0.0);
