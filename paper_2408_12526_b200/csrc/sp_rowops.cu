@@ -124,11 +124,17 @@ __global__ void __launch_bounds__(1024)
                 const float* __restrict__ w_cls, const float* __restrict__ b_cls, int n_classes, int hidden,
                 int add_bias, float* __restrict__ rep, float* __restrict__ logits, float* __restrict__ finals,
                 int* ready_flag, const int* __restrict__ seq_src) {
-  pdl_enter();
+  // weights (the first classifier rows) are read before the dependency wait;
+  // the dependents are released first so these loads never delay them
+  pdl_launch_dependents();
   __shared__ float red[32][4];
   const int b = blockIdx.x;
   const int j = threadIdx.x;
   const int nsp = splits > 0 ? splits : 1;
+  float wc0[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) wc0[c] = (j < hidden && c < n_classes) ? __ldg(w_cls + (long long)c * hidden + j) : 0.f;
+  pdl_wait();
   float r = 0.f;
   if (j < hidden) {
     for (int m0 = 0; m0 < groups; m0 += 8) {
@@ -167,7 +173,9 @@ __global__ void __launch_bounds__(1024)
     float acc[4];
 #pragma unroll
     for (int c = 0; c < 4; ++c)
-      acc[c] = (j < hidden && c0 + c < n_classes) ? __ldg(w_cls + (long long)(c0 + c) * hidden + j) * r : 0.f;
+      acc[c] = (j < hidden && c0 + c < n_classes)
+                   ? (c0 == 0 ? wc0[c] : __ldg(w_cls + (long long)(c0 + c) * hidden + j)) * r
+                   : 0.f;
 #pragma unroll
     for (int c = 0; c < 4; ++c) acc[c] = warp_sum(acc[c]);
     if (lane_id() == 0)
