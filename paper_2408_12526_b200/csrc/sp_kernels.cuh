@@ -240,8 +240,10 @@ struct MlpParams {
   int out_a_ld;
   const float* bias_a;
   int bias_a_gs;
-  float* out_b;  // raw FFN2 projection [S][x_group_rows][H]
+  float* out_b;  // raw FFN2 projection [split][S][x_group_rows][H] (split-K partials, summed by the LayerNorm)
   long long out_b_gs;
+  long long out_b_ss;  // split stride (elements)
+  int splits_b;        // FFN2 split-K count (phase-B units = students x tiles x splits)
   int out_b_ld;
   int* done;  // [kReqMaxStudents + 1] FFN1 tiles finished per student + exit counter (zero between launches)
 };

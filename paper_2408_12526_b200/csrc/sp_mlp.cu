@@ -40,22 +40,26 @@ __device__ __forceinline__ int ld_acquire_gpu(const int* p) {
 }
 
 struct MlpPhase {
-  int n_out, nkb, bn, n_tiles, m_tiles, units;
+  int n_out, nkb, bn, n_tiles, m_tiles, splits, units;  // nkb: k-blocks per unit (one split's share)
 };
 
 __device__ __forceinline__ MlpPhase mlp_phase(const MlpParams& p, int ph) {
   MlpPhase f;
   f.n_out = ph == 0 ? p.n_a : p.n_b;
-  f.nkb = (ph == 0 ? p.k_a : p.k_b) / kMBlockK;
+  f.splits = ph == 0 ? 1 : p.splits_b;
+  f.nkb = (ph == 0 ? p.k_a : p.k_b) / kMBlockK / f.splits;
   f.bn = ph == 0 ? p.bn_a : p.bn_b;
   f.n_tiles = ph == 0 ? p.n_tiles_a : p.n_tiles_b;
   f.m_tiles = f.n_out / kMBlockM;
-  f.units = p.groups * f.m_tiles * f.n_tiles;
+  f.units = p.groups * f.m_tiles * f.n_tiles * f.splits;
   return f;
 }
 
-// Unit -> (student, feature tile, token tile), feature tile fastest.
-__device__ __forceinline__ void mlp_decode(const MlpPhase& f, int u, int& g, int& mt, int& nt) {
+// Unit -> (student, feature tile, token tile, split), feature tile fastest, split slowest.
+__device__ __forceinline__ void mlp_decode(const MlpPhase& f, int u, int& g, int& mt, int& nt, int& sp) {
+  const int per_split = f.units / f.splits;
+  sp = u / per_split;
+  u -= sp * per_split;
   const int per = f.m_tiles * f.n_tiles;
   g = u / per;
   const int r = u - g * per;
@@ -119,10 +123,11 @@ __global__ void __launch_bounds__(kMThreads, 1)
         for (int k = 0;; ++k) {
           const int u = mlp_unit(f, phase, k);
           if (u < 0) break;
-          int g, mt, nt;
-          mlp_decode(f, u, g, mt, nt);
+          int g, mt, nt, sp;
+          mlp_decode(f, u, g, mt, nt, sp);
           const int wrow = g * f.n_out + mt * kMBlockM;
-          for (int kb = 0; kb < f.nkb; ++kb) {
+          const int kb0 = sp * f.nkb;
+          for (int kb = kb0; kb < kb0 + f.nkb; ++kb) {
             mbar_wait(&empty[s], ph ^ 1);
             mbar_arrive_expect_tx(&full[s], kMATileBytes);
             tma_load_2d(map, &full[s], smem + s * stage_bytes, kb * kMBlockK, wrow, pol);
@@ -151,8 +156,8 @@ __global__ void __launch_bounds__(kMThreads, 1)
         for (int k = 0;; ++k) {
           const int u = mlp_unit(f, phase, k);
           if (u < 0) break;
-          int g, mt, nt;
-          mlp_decode(f, u, g, mt, nt);
+          int g, mt, nt, sp;
+          mlp_decode(f, u, g, mt, nt, sp);
           if (phase == 1 && g != dep_g) {  // every FFN1 tile of this student published
             const long long t0 = clock64();
             while (ld_acquire_gpu(p.done + g) < a_tiles_per_student) {
@@ -163,7 +168,8 @@ __global__ void __launch_bounds__(kMThreads, 1)
             dep_g = g;
           }
           const int xrow = g * p.x_group_rows + nt * f.bn;
-          for (int kb = 0; kb < f.nkb; ++kb) {
+          const int kb0 = sp * f.nkb;
+          for (int kb = kb0; kb < kb0 + f.nkb; ++kb) {
             mbar_wait(&empty[s], ph ^ 1);
             mbar_arrive_expect_tx(&full[s], x_bytes);
             uint8_t* sb = smem + s * stage_bytes + kMATileBytes;
@@ -227,8 +233,8 @@ __global__ void __launch_bounds__(kMThreads, 1)
       for (int k = 0;; ++k, ++j) {
         const int u = mlp_unit(f, phase, k);
         if (u < 0) break;
-        int g, mt, nt;
-        mlp_decode(f, u, g, mt, nt);
+        int g, mt, nt, sp;
+        mlp_decode(f, u, g, mt, nt, sp);
         const int b = j & 1;
         const int m0 = mt * kMBlockM, n0 = nt * f.bn;
         const int feat = m0 + q * 32 + lane;
@@ -266,7 +272,7 @@ __global__ void __launch_bounds__(kMThreads, 1)
           } else {  // raw fp32 projection (bias + residual + LayerNorm in the next kernel), 8 columns at a time
             constexpr int kRow = 128, kLanes = kRow / 16, kRowsPass = 32 / kLanes;
             float* st = reinterpret_cast<float*>(stage_base);
-            float* out = p.out_b + (long long)g * p.out_b_gs + m0 + q * 32;
+            float* out = p.out_b + (long long)sp * p.out_b_ss + (long long)g * p.out_b_gs + m0 + q * 32;
             const int sub = lane % kLanes;
             for (int h8 = 0; h8 < n; h8 += 8) {
               if (h8) __syncwarp();

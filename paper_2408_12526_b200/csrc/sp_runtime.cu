@@ -777,7 +777,7 @@ bool mlp_fusion_enabled() {  // SP_MLP_FUSE=0 falls back to two launches
 
 // FFN1 (+GELU) and FFN2 of layer l as one persistent kernel (sp_mlp.cu); FFN2's raw projection
 // lands in g->part (one split) for the LayerNorm kernel.
-int run_mlp(sp_group* g, int l, int k, int n_tokens, const int* t_dev, cudaStream_t st) {
+int run_mlp(sp_group* g, int l, int k, int n_tokens, const int* t_dev, cudaStream_t st, int* splits_b) {
   const sp_config& c = g->cfg;
   const sp_weights& w = g->w;
   const int H = c.hidden, F = c.ffn, T = c.max_tokens;
@@ -803,6 +803,21 @@ int run_mlp(sp_group* g, int l, int k, int n_tokens, const int* t_dev, cudaStrea
   p.out_b = g->part;
   p.out_b_gs = (long long)T * H;
   p.out_b_ld = H;
+  p.out_b_ss = (long long)c.n_students * T * H;
+  // FFN2 split-K (opt-in SP_MLP_SPLITS=n, 0 = until two units per SM): measured +5..18 us at
+  // L = 384..512 — phase B already fills one round (144 deep units at bn = 192), and the static
+  // reverse-order dealing puts the extra split units on the CTAs that also ran three FFN1 tiles
+  static const int split_env = env_int("SP_MLP_SPLITS", 1);
+  const int units_b = k * (H / 128) * p.n_tiles_b;
+  int sb = 1;
+  if (split_env > 0) {
+    sb = split_env;
+  } else {
+    while (sb < kMaxSplits && units_b * sb < 2 * sp::sm_count() && (F / 64) % (sb + 1) == 0) ++sb;
+  }
+  if ((F / 64) % sb != 0 || sb > kMaxSplits) sb = 1;
+  p.splits_b = sb;
+  *splits_b = sb;
   p.done = g->mlp_done;
   sp::MlpMaps m;
   m.w_a = g->m_f1[l];
@@ -977,8 +992,9 @@ int bert_forward(sp_group* g, const int32_t* ids, const int32_t* cu, int n_seqs,
       const bool mlp = mlp_fusion_enabled() && s_f == 1 && n_tokens >= 129 &&
                        !sp::gemm_persistent_pair(n_tokens, F / 128, kc) &&
                        !sp::gemm_persistent_pair(n_tokens, H / 128, kc) && !use_ln_fused(H / 128, n_tiles, kc, F, H);
+      int mlp_splits = 1;
       if (mlp) {
-        launches += run_mlp(g, l, kc, n_tokens, t_dev, cs);  // (single-chain requests only: >= 129 tokens)
+        launches += run_mlp(g, l, kc, n_tokens, t_dev, cs, &mlp_splits);  // (single-chain: >= 129 tokens)
       } else {
         launches += run_gemm(g, SP_LAUNCH_GEMM_FFN1, g->m_f1[l], g->xm_x16, kc, F, H, n_tokens, T, w.b_ffn1 + lS * F,
                              F, sp::ACT_GELU, g->ffn, (long long)T * F, 0, 1, 0, cs, t_dev, g0);
@@ -992,7 +1008,7 @@ int bert_forward(sp_group* g, const int32_t* ids, const int32_t* cu, int n_seqs,
         if (!mlp)
           launches += run_gemm(g, SP_LAUNCH_GEMM_FFN2, g->m_f2[l], g->xm_ffn, kc, H, F, n_tokens, T, nullptr, H,
                                sp::ACT_NONE, g->part, xgs, 1, s_f, part_ss, cs, t_dev, g0);
-        const int s_ln2 = mlp ? 1 : s_f;  // the fused MLP kernel writes one (complete) projection
+        const int s_ln2 = mlp ? mlp_splits : s_f;  // the fused MLP kernel's FFN2 split-K partials
         g->rec_begin(SP_LAUNCH_REDUCE_LN, GTHc * (4.0 * s_ln2 + 10.0), 0.0);
         sp::launch_reduce_ln(g->part + o16, s_ln2, part_ss, w.b_ffn2 + (lS + g0) * H, w.ln2_gamma + (lS + g0) * H,
                              w.ln2_beta + (lS + g0) * H, H, c.ln_eps, g->x32 + o16, g->x16 + o16, xgs, n_rows_arg,

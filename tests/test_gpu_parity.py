@@ -223,7 +223,7 @@ def test_host_graph_path_bit_identical_to_device_path():
             np.testing.assert_array_equal(z_host, z_dev)
 
 
-@pytest.mark.parametrize("env", ["SP_LN_FUSE=1", "SP_ATTN_TC=1", "SP_ATTN_TC=0", "SP_ATTN_TC=2", "SP_ATTN_TC=3", "SP_CHAINS=2", "SP_WS_MAX_TOKENS=128", "SP_GEMM_CLUSTER=1", "SP_PERSIST_PAIR=1", "SP_FUSED=1", "SP_MLP_FUSE=0"])
+@pytest.mark.parametrize("env", ["SP_LN_FUSE=1", "SP_ATTN_TC=1", "SP_ATTN_TC=0", "SP_ATTN_TC=2", "SP_ATTN_TC=3", "SP_CHAINS=2", "SP_WS_MAX_TOKENS=128", "SP_GEMM_CLUSTER=1", "SP_PERSIST_PAIR=1", "SP_FUSED=1", "SP_MLP_FUSE=0", "SP_MLP_SPLITS=3"])
 def test_opt_in_kernel_variants_match_oracle(env):
     """The opt-in kernel variants (fused projection+LayerNorm, tcgen05 attention, cluster-multicast
     GEMM, paired persistent GEMM, whole-request persistent kernel) stay correct: run a fresh process with the knob set (knobs are read once per process)."""
