@@ -89,6 +89,14 @@ __global__ void __launch_bounds__(kThreads, 2)
     mbar_init(tmem_full, 1);
     fence_barrier_init();
     tma_prefetch_desc(&map_w);
+    if (!pair) {  // first weight stages right away: independent of the TMEM allocation and the CTA barrier
+      const uint64_t pol_w = (p.n_tiles > 1 && p.w_keep) ? policy_evict_last() : policy_evict_first();
+      const int n_pre = min(p.stages, kb1 - kb0);
+      for (int i = 0; i < n_pre; ++i) {
+        mbar_arrive_expect_tx(&full[i], stage_bytes);
+        tma_load_2d(&map_w, &full[i], smem + i * stage_bytes, (kb0 + i) * kBlockK, g * p.n_out + m0, pol_w);
+      }
+    }
     tma_prefetch_desc(&map_x64);
     tma_prefetch_desc(&map_x16);
   }
@@ -130,10 +138,11 @@ __global__ void __launch_bounds__(kThreads, 2)
       // 1) weight prefetch: independent of the previous kernel. The first stages go straight to
       //    smem; the rest of this CTA's weight slab is optionally pulled into L2.
       const int n_pre = min(p.stages, kb1 - kb0);
-      for (int i = 0; i < n_pre; ++i) {
-        mbar_arrive_expect_tx(&full[i], stage_bytes);
-        tma_load_2d(&map_w, &full[i], smem + i * stage_bytes, (kb0 + i) * kBlockK, wrow, pol_w);
-      }
+      if (pair)  // (pair: the peer's barriers are initialised only after cluster_sync)
+        for (int i = 0; i < n_pre; ++i) {
+          mbar_arrive_expect_tx(&full[i], stage_bytes);
+          tma_load_2d(&map_w, &full[i], smem + i * stage_bytes, (kb0 + i) * kBlockK, wrow, pol_w);
+        }
       if (p.l2_prefetch)
         for (int kb = kb0 + n_pre; kb < kb1; ++kb) tma_prefetch_l2_2d(&map_w, kb * kBlockK, wrow);
       if (tr) tr[2] = globaltimer();
@@ -319,6 +328,19 @@ __global__ void __launch_bounds__(kPThreads, 1)
     }
     fence_barrier_init();
     tma_prefetch_desc(&map_w);
+    if constexpr (!PAIR) {  // first unit's weight stages right away (before TMEM allocation / CTA barrier)
+      if (u_first < units) {
+        const int g = u_first / units_per_group + p.g0;
+        const int mt = (u_first % units_per_group) % m_per;
+        const uint64_t pol_w = p.w_keep == 2 ? policy_evict_last() : (p.w_keep == 1 ? policy_evict_normal()
+                                                                                     : policy_evict_first());
+        const int n_pre = min(p.stages, nkb);
+        for (int i = 0; i < n_pre; ++i) {
+          mbar_arrive_expect_tx(&full[i], full_bytes);
+          tma_load_2d(&map_w, &full[i], smem + i * stage_bytes, i * kBlockK, g * p.n_out + mt * kBlockM, pol_w);
+        }
+      }
+    }
     tma_prefetch_desc(&map_x64);
     tma_prefetch_desc(&map_x16);
   }
@@ -376,10 +398,11 @@ __global__ void __launch_bounds__(kPThreads, 1)
         int kb = 0;
         if (first) {  // weight prefetch of the first stages before the dependency wait
           const int n_pre = min(p.stages, nkb);
-          for (int i = 0; i < n_pre; ++i) {
-            if (leader) mbar_arrive_expect_tx(&full[i], full_bytes);
-            load_w(i, i, wrow);
-          }
+          if constexpr (PAIR)  // (single CTA: already issued at entry)
+            for (int i = 0; i < n_pre; ++i) {
+              if (leader) mbar_arrive_expect_tx(&full[i], full_bytes);
+              load_w(i, i, wrow);
+            }
           if (p.l2_prefetch)
             for (int i = n_pre; i < nkb; ++i) tma_prefetch_l2_2d(&map_w, i * kBlockK, wrow);
           if (tr) tr[2] = globaltimer();
