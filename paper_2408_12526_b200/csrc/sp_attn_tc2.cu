@@ -1,12 +1,13 @@
-// sp_attn_tc2.cu — single-pass varlen attention on 5th-gen tensor cores, two CTAs per SM
-// (head_dim 64, L <= 512).
+// sp_attn_tc2.cu — single-pass varlen attention on 5th-gen tensor cores (head_dim 64, L <= 512).
 //
-// One CTA per (student, sequence, head, 128-query block), 192 threads and 256 TMEM columns so two
-// CTAs share an SM (one's softmax runs while the other waits on its MMAs or loads):
-//   warps 0-3  softmax: thread = query row = TMEM lane (warp w owns lanes 32w..32w+31); each
-//              thread keeps its row's running max m and sum l (online softmax, log2 domain)
-//   warp 4     TMA producer: Q once, then 128-key K/V chunks through a 2-stage ring
-//   warp 5     TMEM allocation + MMA issue (one elected lane)
+// attn_tc2_kernel<TRACE, SPLIT>: one CTA per (student, sequence, head, 128-query block), two CTAs
+// per SM (320 threads at SPLIT = 2, 256 TMEM columns); one's softmax runs while the other waits on
+// its MMAs or loads:
+//   softmax warps: 4 * SPLIT; thread = query row = TMEM lane (warp w owns lanes 32(w%4)..+31) and
+//              128 / SPLIT key columns of each chunk; running max m and sum l per row (online
+//              softmax, log2 domain), row maxima / sums of the SPLIT column groups via smem
+//   warp 4*SPLIT     TMA producer: Q once, then 128-key K/V chunks through a 2-stage ring
+//   warp 4*SPLIT+1   TMEM allocation + MMA issue (one elected lane)
 // TMEM: S = Q K^T of the current chunk in columns [0, 128) (fp32), P = exp2(S - m) as packed fp16
 // in [128, 192), O in [192, 256). O += P V reads P straight from TMEM (tcgen05.mma A operand in
 // tensor memory), so P never touches shared memory.
@@ -17,6 +18,8 @@
 // 2^8 (P <= 256 stays exact in fp16, l in fp32); then the thread rescales its O row in TMEM
 // (after PV_{j-1} completed) — rare after the first chunk. Keys past the sequence end are masked;
 // query rows past it are not stored.
+// attn_tc3_kernel (below): the same algorithm with 64-key chunks and P written over its own scores
+// (128 TMEM columns), three CTAs per SM — one wave for up to 512 tokens.
 // No reference counterpart; semantics = oracle/bert.py:attention.
 #include "sp_kernels.cuh"
 #include "sp_ptx.cuh"
