@@ -769,11 +769,11 @@ static void launch_gemm_t(const GemmMaps& maps, const GemmParams& p, int groups,
   cudaLaunchKernelEx(&cfg, gemm_kernel<ACT, OUT_F32>, maps.w, maps.x64, maps.x16, q);
 }
 
-// Epilogue warps of the small-T kernel: 4 for narrow token tiles (192 threads: with 32-column TMEM
-// and fewer stages, CTAs of the next projection fit beside this one's), else 8.
-int gemm_epi_warps(int bn) {
-  static const int max_bn4 = env_int("SP_GEMM_EPI4_MAXBN", 32, 0, 256);
-  return bn <= max_bn4 ? 4 : 8;
+// Epilogue warps of the small-T kernel: 4 (192 threads) unless the launch has several wide token
+// tiles (measured in-graph: 4 warps -1..-3 us at 96-192 tokens, 8 warps better at 256 = 2 x 128).
+int gemm_epi_warps(int bn, int n_tiles) {
+  static const int max_bn4 = env_int("SP_GEMM_EPI4_MAXBN", 96, 0, 256);
+  return (bn <= max_bn4 || n_tiles == 1) ? 4 : 8;
 }
 
 void launch_gemm(const GemmMaps& maps, const GemmParams& p, int groups, cudaStream_t stream) {

@@ -125,7 +125,7 @@ void gemm_configure_persistent(int t_rows, bool out_f32, int units_per_tile, int
 int sm_count();
 size_t gemm_smem_bytes(int bn, int stages);
 void gemm_configure_tiles(int t_rows, bool cluster2, int* bn, int* n_tiles, int* stages);
-int gemm_epi_warps(int bn);
+int gemm_epi_warps(int bn, int n_tiles);
 
 // Unpadded multi-head attention over cu_seqlens-packed sequences.
 //   qkv: fp16 [groups][x_group_rows][3H] (Q | K | V, head h at columns h*D within each third)

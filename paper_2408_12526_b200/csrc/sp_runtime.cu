@@ -577,7 +577,7 @@ int run_gemm(sp_group* grp, int kind, const CUtensorMap& wmap, const XMaps& xm, 
   }();
   p.w_keep = w_keep;
   sp::gemm_configure_tiles(t_rows, p.cluster == 2, &p.bn, &p.n_tiles, &p.stages);
-  p.epi_warps = sp::gemm_epi_warps(p.bn);
+  p.epi_warps = sp::gemm_epi_warps(p.bn, p.n_tiles);
   p.splits = splits;
   p.kb_per_split = (k_dim / 64) / splits;
   p.out = out;
