@@ -720,7 +720,10 @@ static int env_int(const char* name, int dflt, int lo, int hi) {
 }
 
 void gemm_configure_tiles(int t_rows, bool cluster2, int* bn, int* n_tiles, int* stages) {
-  static const int max_bn = env_int("SP_GEMM_MAXBN", 128, 16, kMaxBn);
+  // token-tile cap: 64 up to 128 tokens (two tiles at 65-128 tokens: more CTAs stream the split-K
+  // weights, -4..-6 us at 96-128 measured in-graph), else 128; SP_GEMM_MAXBN overrides
+  static const int max_bn_env = env_int("SP_GEMM_MAXBN", 0, 0, kMaxBn);
+  const int max_bn = max_bn_env >= 16 ? max_bn_env : (t_rows <= 128 ? 64 : 128);
   static const int smem_kb = env_int("SP_GEMM_SMEM_KB", 96, 40, 200);
   int tiles = (t_rows + max_bn - 1) / max_bn;
   if (tiles < 1) tiles = 1;

@@ -572,8 +572,8 @@ int run_gemm(sp_group* grp, int kind, const CUtensorMap& wmap, const XMaps& xm, 
   }();
   p.cluster = (cluster_on && p.m_tiles % 2 == 0 && t_rows > 16) ? 2 : 1;
   static const int w_keep = [] {
-    const char* v = getenv("SP_GEMM_WKEEP");
-    return v == nullptr ? 1 : atoi(v);
+    const char* v = getenv("SP_GEMM_WKEEP");  // evict_last weights when token tiles re-read them:
+    return v == nullptr ? 0 : atoi(v);          // measured 1-4 us slower at 160-256 tokens (default off)
   }();
   p.w_keep = w_keep;
   sp::gemm_configure_tiles(t_rows, p.cluster == 2, &p.bn, &p.n_tiles, &p.stages);
