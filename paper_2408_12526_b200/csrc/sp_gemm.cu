@@ -711,7 +711,7 @@ size_t gemm_smem_bytes(int bn, int stages) {
   return static_cast<size_t>(stages) * (kATileBytes + bn * 128) + 1024 /*align*/ + 256 /*barriers*/;
 }
 
-// Tile policy knobs (tuning sweeps): SP_GEMM_MAXBN (16..256, default 128), SP_GEMM_SMEM_KB.
+// Tile policy knobs (tuning sweeps): SP_GEMM_MAXBN (16..256; default 64 up to 128 tokens, else 128), SP_GEMM_SMEM_KB.
 static int env_int(const char* name, int dflt, int lo, int hi) {
   const char* v = getenv(name);
   if (!v) return dflt;
@@ -724,7 +724,7 @@ void gemm_configure_tiles(int t_rows, bool cluster2, int* bn, int* n_tiles, int*
   // weights, -4..-6 us at 96-128 measured in-graph), else 128; SP_GEMM_MAXBN overrides
   static const int max_bn_env = env_int("SP_GEMM_MAXBN", 0, 0, kMaxBn);
   const int max_bn = max_bn_env >= 16 ? max_bn_env : (t_rows <= 128 ? 64 : 128);
-  static const int smem_kb = env_int("SP_GEMM_SMEM_KB", 96, 40, 200);
+  static const int smem_kb = env_int("SP_GEMM_SMEM_KB", 110, 40, 200);  // 6 stages at <= 32-token tiles
   int tiles = (t_rows + max_bn - 1) / max_bn;
   if (tiles < 1) tiles = 1;
   const int per = (t_rows + tiles - 1) / tiles;
@@ -733,8 +733,8 @@ void gemm_configure_tiles(int t_rows, bool cluster2, int* bn, int* n_tiles, int*
   if (b < gran) b = gran;
   *bn = b;
   *n_tiles = tiles;
-  // ~96 KiB per CTA so that two CTAs (e.g. the tail of one projection and the prefetching head
-  // of the next, or two tiles of one projection) share an SM: smem 2 x ~97 KiB, TMEM 2 x 256 cols.
+  // ~110 KiB per CTA so that two CTAs (e.g. the tail of one projection and the prefetching head
+  // of the next, or two tiles of one projection) share an SM: smem 2 x <= 111 KiB, TMEM <= 2 x 128 cols.
   int st = (smem_kb * 1024) / (kATileBytes + b * 128);
   if (st > 6) st = 6;
   if (st < 2) st = 2;
