@@ -136,7 +136,10 @@ int sp_group_forward_dense_eval(sp_group* group, const void* x, int32_t n_rows, 
                                 float* prefix_logits_out, void* stream);
 
 /* BERT kind end to end with HOST buffers: validates ids/cu_seqlens like the reference validates its
- * inputs, copies them to the device, runs the group, copies logits back and synchronizes `stream`. */
+ * inputs, copies them to the device, runs the group and returns once the logits are in
+ * `logits_out`. One sequence: the bucket's CUDA graph is replayed and the logits arrive through
+ * mapped pinned memory plus a sequence flag the call polls (no stream synchronize; a failed launch
+ * is detected with cudaStreamQuery); several sequences: eager launches, D2H copy, stream sync. */
 int sp_group_forward_host(sp_group* group, const int32_t* ids, const int32_t* cu_seqlens, int32_t n_seqs,
                           int32_t n_tokens, int32_t k_active, float* logits_out, int32_t add_bias, void* stream);
 

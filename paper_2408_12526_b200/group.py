@@ -332,7 +332,8 @@ class StudentGroup:
     def forward_host(self, ids: np.ndarray, cu: np.ndarray, k: int | None = None, add_bias: bool = True,
                      out: np.ndarray | None = None, stream: torch.cuda.Stream | None = None) -> np.ndarray:
         """End-to-end call with HOST buffers (ids in, logits out; the serving seam servesim.py:486).
-        One C call: H2D of ids/cu_seqlens, the whole group forward, D2H of logits, stream sync."""
+        One C call: H2D of ids/cu_seqlens, the whole group forward, logits back on the host
+        (batch-1: bucket-graph replay, logits via mapped pinned memory; else D2H + stream sync)."""
         if self.kind != "bert":
             raise ValueError("forward_host serves BERT-kind groups")
         ids = np.ascontiguousarray(ids, dtype=np.int32)
