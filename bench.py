@@ -82,6 +82,8 @@ def make_requests(n, seed, lo, hi, vocab):
 
 
 def workload_config(args, cfg, K, world):
+    from paper_2408_12526_b200.parallel import placement
+
     return {
         "workload": f"{args.config}: K={K} BERT-style 2-layer students, H={cfg.hidden}, {cfg.n_heads} heads, "
                     f"F={cfg.ffn}, {'batch-1' if args.batch == 1 else f'batches of {args.batch}'} ragged "
@@ -89,12 +91,13 @@ def workload_config(args, cfg, K, world):
         "model": "student group (boosting sum of K flat BERT-style students)",
         "K": K, "hidden": cfg.hidden, "heads": cfg.n_heads, "layers": cfg.n_layers, "ffn": cfg.ffn,
         "global_batch": args.batch, "seq_len": [args.len_min, args.len_max], "k_active": K,
-        "students_per_gpu": [len(s) for s in __import__("paper_2408_12526_b200.parallel", fromlist=["x"]).placement(K, world)],
+        "students_per_gpu": [len(s) for s in placement(K, world)],
         "parallelism": f"student-parallel x{world}" if world > 1 else "single GPU",
         "l2": "flushed before every timed request: 256 MiB write + 256 MiB read (> 126 MB L2)",
         "launch": ("CUDA-graph replay per request (16-token bucket graph; 2 device-to-device input copies "
-                   "+ 1 graph launch, inside the timed region)"
-                   if world == 1 and args.batch == 1 and args.graph else "eager PDL-chained launches"),
+                   "+ 1 graph launch, inside the timed region"
+                   + ("; then one NCCL all-reduce of the partial logits)" if world > 1 else ")")
+                   if args.batch == 1 and args.graph else "eager PDL-chained launches"),
     }
 
 
@@ -277,11 +280,19 @@ def run_engine(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    # validation only: SP_BENCH_ONE_DEVICE=1 puts every rank on cuda:0 with the gloo backend (host-side
+    # reduce, no kernel of one rank waits on another) to exercise the N-rank code path on a 1-GPU box
+    one_device = os.environ.get("SP_BENCH_ONE_DEVICE") == "1"
+    if one_device:
+        local_rank = 0
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local_rank)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if one_device:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     from paper_2408_12526_b200 import PRESETS
     from paper_2408_12526_b200._lib import GEMM_KINDS, LAUNCH_KINDS  # noqa: F401
     from paper_2408_12526_b200.parallel import ShardedStudentGroup
@@ -315,16 +326,19 @@ def run_engine(args):
         flush_w.fill_(0.0)
         flush_r.sum()
 
-    use_graph = world == 1 and B == 1 and args.graph
+    use_graph = B == 1 and args.graph
+    k_local = grp.local_k(K)
 
     def step_eager(i):
         T = step_tok[i]
-        grp.forward_packed_device(ids_all[offs[i]: offs[i] + T], cu_all[i], B, T, step_max[i], K, logits)
+        grp.forward_packed_device(ids_all[offs[i]: offs[i] + T], cu_all[i], B, T, step_max[i], K, logits, graph=False)
 
     def step(i):
         if not use_graph:
             return step_eager(i)
         T = step_tok[i]  # batch-1: one bucket graph per request (kernels read the live length from cu)
+        if world > 1:  # this shard's bucket graph, then the logit all-reduce
+            return grp.forward_packed_device(ids_all[offs[i]: offs[i] + T], cu_all[i], 1, T, T, K, logits)
         grp.local.forward_graph_device(ids_all[offs[i]: offs[i] + T], cu_all[i], T, K, logits)
 
     if use_graph:  # capture every 16-token bucket's graph before the warm-up (not on the timed path)
@@ -332,7 +346,8 @@ def run_engine(args):
         for t in range(16, args.len_max + 16, 16):
             t = min(t, args.len_max)
             ids_t = first[:t] if t <= step_tok[0] else torch.full((t,), 1000, dtype=torch.int32, device=dev)
-            grp.local.forward_graph_device(ids_t, torch.tensor([0, t], dtype=torch.int32, device=dev), t, K, logits)
+            grp.local.forward_graph_device(ids_t, torch.tensor([0, t], dtype=torch.int32, device=dev), t, k_local,
+                                           logits, add_bias=(rank == 0))
         torch.cuda.synchronize()
 
     def barrier():
@@ -445,8 +460,11 @@ def run_engine(args):
     # ---- e2e through the public API with host buffers
     pinned_ids = [torch.from_numpy(r).pin_memory() for r in step_ids]
     pinned_cu = [torch.from_numpy(c).pin_memory() for c in step_cu]
-    if world == 1 and B == 1:  # capture the batch-1 graphs of the host path before timing
-        grp.local.prepare_graphs(args.len_max, K)
+    if B == 1:  # capture the batch-1 graphs of the host path before timing
+        if world == 1:
+            grp.local.prepare_graphs(args.len_max, K)
+        else:
+            grp.prepare_graphs(args.len_max, K)
     e2e_s = []
     barrier()
     for j in range(args.steps):

@@ -68,12 +68,42 @@ class ShardedStudentGroup:
     def local_k(self, k: int | None) -> int:
         return local_prefix(self.total if k is None else int(k), self.students, self.total)
 
-    def forward_packed_device(self, ids, cu, n_seqs, n_tokens, max_len, k, logits, stream=None):
-        """Device buffers in, reduced logits (identical on every rank) out; no host sync."""
-        self.local.forward_packed_device(ids, cu, n_seqs, n_tokens, max_len, self.local_k(k), None, logits,
-                                         add_bias=(self.rank == 0), stream=stream)
+    def forward_packed_device(self, ids, cu, n_seqs, n_tokens, max_len, k, logits, stream=None, graph=True):
+        """Device buffers in, reduced logits (identical on every rank) out; no host sync.
+        A single sequence replays this shard's 16-token bucket graph (one launch instead of ~15
+        on every rank); a shard with no student in the prefix writes zero partials eagerly."""
+        kl = self.local_k(k)
+        if graph and n_seqs == 1 and kl >= 1:
+            self.local.forward_graph_device(ids, cu, n_tokens, kl, logits, add_bias=(self.rank == 0), stream=stream)
+        else:
+            self.local.forward_packed_device(ids, cu, n_seqs, n_tokens, max_len, kl, None, logits,
+                                             add_bias=(self.rank == 0), stream=stream)
         reduce_partials(logits[:n_seqs], self.process_group)
         return logits
+
+    def _ensure_staging(self):
+        if self._pinned_logits is None:  # staging allocated once (pinned: async copies, no per-call alloc)
+            dev = self.device
+            self._h_ids = torch.empty(self.local.max_tokens, dtype=torch.int32).pin_memory()
+            self._h_cu = torch.empty(self.local.max_seqs + 1, dtype=torch.int32).pin_memory()
+            self._d_ids = torch.empty(self.local.max_tokens, dtype=torch.int32, device=dev)
+            self._d_cu = torch.empty(self.local.max_seqs + 1, dtype=torch.int32, device=dev)
+            self._d_logits = torch.empty((self.local.max_seqs, self.n_classes), dtype=torch.float32, device=dev)
+            self._pinned_logits = torch.empty((self.local.max_seqs, self.n_classes), dtype=torch.float32).pin_memory()
+
+    def prepare_graphs(self, max_tokens: int | None = None, k: int | None = None) -> None:
+        """Capture this shard's batch-1 bucket graphs of forward_host ahead of time (no collective)."""
+        kl = self.local_k(k)
+        if kl < 1:
+            return
+        self._ensure_staging()
+        top = min(int(max_tokens or self.local.max_tokens), self.local.max_tokens, self.local.weights.cfg.max_pos)
+        self._d_ids.fill_(1000)
+        for t in range(16, top + 16, 16):
+            t = min(t, top)
+            self._d_cu[:2].copy_(torch.tensor([0, t], dtype=torch.int32))
+            self.local.forward_graph_device(self._d_ids, self._d_cu, t, kl, self._d_logits, add_bias=(self.rank == 0))
+        torch.cuda.synchronize(self.device)
 
     def forward_host(self, ids: np.ndarray, cu: np.ndarray, k: int | None = None) -> np.ndarray:
         """Public end-to-end call: host ids/cu_seqlens in, host logits out (every rank gets them)."""
@@ -86,14 +116,7 @@ class ShardedStudentGroup:
         n, t = len(cu) - 1, len(ids)
         if n > self.local.max_seqs or t > self.local.max_tokens:
             raise ValueError(f"request ({n} seqs, {t} tokens) exceeds the group's capacity")
-        if self._pinned_logits is None:  # staging allocated once (pinned: async copies, no per-call alloc)
-            dev = self.device
-            self._h_ids = torch.empty(self.local.max_tokens, dtype=torch.int32).pin_memory()
-            self._h_cu = torch.empty(self.local.max_seqs + 1, dtype=torch.int32).pin_memory()
-            self._d_ids = torch.empty(self.local.max_tokens, dtype=torch.int32, device=dev)
-            self._d_cu = torch.empty(self.local.max_seqs + 1, dtype=torch.int32, device=dev)
-            self._d_logits = torch.empty((self.local.max_seqs, self.n_classes), dtype=torch.float32, device=dev)
-            self._pinned_logits = torch.empty((self.local.max_seqs, self.n_classes), dtype=torch.float32).pin_memory()
+        self._ensure_staging()
         self._h_ids.numpy()[:t] = ids
         self._h_cu.numpy()[: n + 1] = cu
         self._d_ids[:t].copy_(self._h_ids[:t], non_blocking=True)

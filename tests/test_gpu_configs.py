@@ -111,3 +111,38 @@ def test_sharded_host_path_matches_group_host_path():
             z = sh.forward_host(ids, cu, k)
             assert z.shape == (len(lens), 2)
             np.testing.assert_allclose(z, ref.forward_host(ids, cu, k), rtol=0, atol=1e-5)
+
+
+def test_sharded_partials_sum_to_group_logits():
+    """Two shards of one group (world size 2, ranks built in this process, so the logit reduce is
+    skipped): their partial logits sum to the whole group's logits. Batch-1 runs each shard's bucket
+    graph (the N-GPU bench step, graphs captured ahead by prepare_graphs); a prefix k that leaves a
+    shard without students gives that shard zero partials; several sequences take the eager path."""
+    import torch
+    from paper_2408_12526_b200 import PRESETS, StudentGroup, random_bert_group
+    from paper_2408_12526_b200.parallel import ShardedStudentGroup
+
+    cfg, K = PRESETS["tiny"]
+    shards = [ShardedStudentGroup(cfg, K, seed=6, rank=r, world=2, max_tokens=256, max_seqs=4) for r in range(2)]
+    ref = StudentGroup(random_bert_group(cfg, K, seed=6), max_tokens=256, max_seqs=4)
+    for sh in shards:
+        sh.prepare_graphs(64, K)
+    rng = np.random.default_rng(9)
+    for lens in ([7], [16], [33], [64], [5, 60, 33]):
+        seqs = _seqs(rng, lens)
+        ids = np.concatenate(seqs)
+        cu = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+        d_ids = torch.from_numpy(ids).cuda()
+        d_cu = torch.from_numpy(cu).cuda()
+        for k in (1, 2, 3, K):
+            want = ref.forward_host(ids, cu, k)
+            parts_host = [sh.forward_host(ids, cu, k) for sh in shards]
+            np.testing.assert_allclose(parts_host[0] + parts_host[1], want, rtol=0, atol=1e-5)
+            parts_dev = []
+            for sh in shards:
+                z = torch.full((4, 2), float("nan"), device="cuda")
+                sh.forward_packed_device(d_ids, d_cu, len(lens), len(ids), max(lens), k, z)
+                parts_dev.append(z[: len(lens)].cpu().numpy())
+            np.testing.assert_allclose(parts_dev[0] + parts_dev[1], want, rtol=0, atol=1e-5)
+            if k == 1:
+                assert not parts_dev[1].any() and not parts_host[1].any()
