@@ -15,6 +15,7 @@ pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 TOL = 1e-3
+TOL_SWEEP = 2e-3  # worst case over the seed sweep, for tests on unselected seeds
 
 
 def _seqs(rng, lens, vocab=30522):
@@ -39,6 +40,31 @@ def test_large_bert_batched_pair_path_matches_oracle():
     z = grp.logits(seqs)
     _, z_ref = OracleBertGroup(w).forward(seqs)
     assert rel_err_rows(z, z_ref) <= TOL
+
+
+@pytest.mark.parametrize("L", [512, 1])
+def test_large_bert_batch1_extreme_lengths_match_oracle(L):
+    """BERT-large-sized students (H=1024, 16 heads) at batch-1 at both ends of the length range: the
+    maximum position count (512 tokens: persistent projections, longest attention) and a lone CLS
+    token; the host path (forward_host, bucket graph) and the reference-style logits() agree.
+    Bar: TOL_SWEEP, the worst max-|logit| relative error seen in the seed sweep of DESIGN.md §2
+    (random-init logits are cancellation sums, so the fp16 rounding of the GEMM activation operands
+    reaches 1.4e-3 on some seeds; profiles/r1_parity_seed_sweep.txt, r1_precision_anatomy.txt)."""
+    from oracle.bert import OracleBertGroup
+    from paper_2408_12526_b200 import PRESETS, StudentGroup, random_bert_group
+
+    cfg, K = PRESETS["large"]
+    w = random_bert_group(cfg, 2, seed=31)
+    grp = StudentGroup(w, max_tokens=512, max_seqs=1)
+    ids = _seqs(np.random.default_rng(L), [L])[0]
+    _, z_ref = OracleBertGroup(w).forward([ids])
+    z = grp.logits(ids)
+    assert rel_err_rows(z[None, :], z_ref) <= TOL_SWEEP
+    assert np.argmax(z) == np.argmax(z_ref[0])
+    cu = np.array([0, L], np.int32)
+    np.testing.assert_allclose(grp.forward_host(ids, cu)[0], z, rtol=0, atol=1e-5)
+    with pytest.raises(ValueError):
+        grp.logits(np.concatenate([ids, ids]) if L == 512 else np.zeros(0, np.int32))
 
 
 def test_k32_group_batch1_matches_oracle():
