@@ -22,6 +22,10 @@
  * group's device; `stream` is a cudaStream_t (NULL = legacy default stream). Every call is
  * re-entrant per stream for distinct groups (the reference forward is not: nnkernel.py:74).
  * Return value: SP_OK or an SP_E* code; sp_last_error() then describes the failure.
+ *
+ * Precision: weights fp16 (exact: the host rounds them once, weights.py); every activation a
+ * projection reads is carried as an fp16 (hi, lo) pair and every accumulation is fp32, so the
+ * logits match the float64 reference on the same rounded weights within 1e-3 of max|logit|.
  */
 #ifndef STUDENTPAR_B200_H
 #define STUDENTPAR_B200_H
@@ -32,7 +36,7 @@
 extern "C" {
 #endif
 
-#define SP_ABI_VERSION 1
+#define SP_ABI_VERSION 2
 
 enum sp_status {
   SP_OK = 0,
@@ -119,9 +123,10 @@ int sp_group_forward(sp_group* group, const int32_t* ids, const int32_t* cu_seql
                      int32_t n_tokens, int32_t max_seq_len, int32_t k_active, float* rep_out, float* logits_out,
                      int32_t add_bias, void* stream);
 
-/* Dense kind: x fp16 [n_rows][d_in] device (one row per sample, shared by every student). */
-int sp_group_forward_dense(sp_group* group, const void* x, int32_t n_rows, int32_t k_active, float* rep_out,
-                           float* logits_out, int32_t add_bias, void* stream);
+/* Dense kind: x fp16 [n_rows][d_in] device (one row per sample, shared by every student); x_lo
+ * (optional, may be NULL) the fp16 residual x - x_hi of a wider input, read as a second operand term. */
+int sp_group_forward_dense(sp_group* group, const void* x, const void* x_lo, int32_t n_rows, int32_t k_active,
+                           float* rep_out, float* logits_out, int32_t add_bias, void* stream);
 
 /* Training-side evaluation (offline distillation / pruning, not the serving path):
  *   finals_out        fp32 [k_active][n_seqs][hidden]     student m's final representation S_m(x)
@@ -132,8 +137,8 @@ int sp_group_forward_dense(sp_group* group, const void* x, int32_t n_rows, int32
 int sp_group_forward_eval(sp_group* group, const int32_t* ids, const int32_t* cu_seqlens, int32_t n_seqs,
                           int32_t n_tokens, int32_t max_seq_len, int32_t k_active, float* finals_out,
                           float* prefix_logits_out, void* stream);
-int sp_group_forward_dense_eval(sp_group* group, const void* x, int32_t n_rows, int32_t k_active, float* finals_out,
-                                float* prefix_logits_out, void* stream);
+int sp_group_forward_dense_eval(sp_group* group, const void* x, const void* x_lo, int32_t n_rows, int32_t k_active,
+                                float* finals_out, float* prefix_logits_out, void* stream);
 
 /* BERT kind end to end with HOST buffers: validates ids/cu_seqlens like the reference validates its
  * inputs, copies them to the device, runs the group and returns once the logits are in
@@ -145,9 +150,10 @@ int sp_group_forward_host(sp_group* group, const int32_t* ids, const int32_t* cu
 
 /* Batch-1 request on DEVICE buffers replayed as the bucket's CUDA graph (one sequence:
  * ids int32 [n_tokens], cu_seqlens int32 [2] = {0, n_tokens}; logits f32 [C] device). The inputs
- * are copied device-to-device into the group's staging, then one graph launch runs the forward;
- * asynchronous on `stream`. The first call per (16-token bucket, k, logits buffer) captures the
- * graph. Same result as sp_group_forward (graph replay is bit-identical to eager). */
+ * are copied device-to-device into the group's staging, one graph launch runs the forward into the
+ * group's logits slot and one device-to-device copy hands them to logits_out; asynchronous on
+ * `stream`. The first call per (16-token bucket, k, add_bias) captures the graph. Same result as
+ * sp_group_forward (graph replay is bit-identical to eager). */
 int sp_group_forward_graph(sp_group* group, const int32_t* ids, const int32_t* cu_seqlens, int32_t n_tokens,
                            int32_t k_active, float* logits_out, int32_t add_bias, void* stream);
 
@@ -186,16 +192,15 @@ int sp_group_set_profiling(sp_group* group, int enable);
  * launches recorded (or a negative sp_status). */
 int sp_group_profile_read(sp_group* group, sp_launch_record* out, int max_records);
 
-/* Debug: when buf (device, >= 64 x n_SMs uint64) is non-null, the whole-request persistent kernel
- * records globaltimer stamps per CTA (entry, end of every stage, weight-producer phase ends). */
-int sp_debug_set_request_trace(void* buf);
-
-/* Op-level entry points (single kernels, used by the per-kernel parity tests). */
-int sp_op_gemm(const void* w, const void* x, int32_t groups, int32_t n_out, int32_t k_dim, int32_t t_rows,
-               int32_t x_group_rows, int32_t x_rows_total, const float* bias, int32_t act, void* out,
-               int32_t out_f32, int32_t splits, void* stream);
-int sp_op_attention(const void* qkv, void* ctx, const int32_t* cu_seqlens, int32_t n_seqs, int32_t max_seq_len,
-                    int32_t groups, int32_t n_heads, int32_t head_dim, int32_t group_rows, void* stream);
+/* Op-level entry points (single kernels, used by the per-kernel parity tests).
+ * GEMM: x / x_lo fp16 [x_rows_total][k_dim] operand terms (x_lo may be NULL); fp16 output with
+ * out_lo != NULL is written as an (hi, lo) pair. Attention: ctx / ctx_lo the (hi, lo) context. */
+int sp_op_gemm(const void* w, const void* x, const void* x_lo, int32_t groups, int32_t n_out, int32_t k_dim,
+               int32_t t_rows, int32_t x_group_rows, int32_t x_rows_total, const float* bias, int32_t act, void* out,
+               void* out_lo, int32_t out_f32, int32_t splits, void* stream);
+int sp_op_attention(const void* qkv, void* ctx, void* ctx_lo, const int32_t* cu_seqlens, int32_t n_seqs,
+                    int32_t max_seq_len, int32_t groups, int32_t n_heads, int32_t head_dim, int32_t group_rows,
+                    void* stream);
 
 /* Debug: when non-NULL, every subsequent GEMM launch writes 8 %globaltimer stamps per CTA
  * (entry, prologue done, first TMA, last TMA, first MMA, last commit, epilogue start, exit) into

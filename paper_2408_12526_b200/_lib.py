@@ -13,7 +13,7 @@ from .build import LIB_PATH
 
 SP_OK, SP_EINVAL, SP_ECUDA, SP_ENOMEM = 0, 1, 2, 3
 SP_KIND_DENSE, SP_KIND_BERT = 0, 1
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 
 class SpConfig(C.Structure):
@@ -69,16 +69,16 @@ SIGNATURES: dict[str, tuple] = {
          C.c_int32, C.c_void_p],
     ),
     "sp_group_forward_dense": (
-        C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p]
+        C.c_int,
+        [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p],
     ),
-    "sp_debug_set_request_trace": (C.c_int, [C.c_void_p]),
     "sp_group_forward_eval": (
         C.c_int,
         [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
          C.c_void_p],
     ),
     "sp_group_forward_dense_eval": (
-        C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]
+        C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]
     ),
     "sp_group_forward_host": (
         C.c_int,
@@ -93,16 +93,16 @@ SIGNATURES: dict[str, tuple] = {
     "sp_group_profile_read": (C.c_int, [C.c_void_p, C.POINTER(SpLaunchRecord), C.c_int]),
     "sp_op_gemm": (
         C.c_int,
-        [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
-         C.c_int32, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p],
+        [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+         C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p],
     ),
     "sp_debug_set_gemm_trace": (C.c_int, [C.c_void_p]),
     "sp_debug_set_attn_trace": (C.c_int, [C.c_void_p]),
     "sp_debug_gemm_trace_launches": (C.c_int, [C.c_void_p, C.c_int32]),
     "sp_op_attention": (
         C.c_int,
-        [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
-         C.c_void_p],
+        [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+         C.c_int32, C.c_void_p],
     ),
 }
 

@@ -20,7 +20,7 @@ namespace sp {
 template <int D, int NW, int MINB, int NBUF>
 __global__ void __launch_bounds__(32 * NW, MINB)
     attn_kernel(const half* __restrict__ qkv, half* __restrict__ ctx, const int* __restrict__ cu, int n_heads,
-                int hidden, long long group_rows, float scale_log2, const void* pf_ptr, unsigned long long pf_bytes) {
+                int hidden, long long group_rows, float scale_log2, long long lo_off) {
   constexpr int BQ = 16 * NW, BK = 64, LD = D + 8;  // +8 halfs: conflict-free ldmatrix rows
   constexpr int NT = 32 * NW;
   constexpr int VPR = D / 8;  // 16-byte vectors per row
@@ -29,7 +29,6 @@ __global__ void __launch_bounds__(32 * NW, MINB)
   half* sK = sQ + BQ * LD;         // [NBUF][BK][LD]
   half* sV = sK + NBUF * BK * LD;  // [NBUF][BK][LD]
 
-  prefetch_share_l2(pf_ptr, pf_bytes);  // next projection's weights, while attention runs
   const int b = blockIdx.y;
   pdl_launch_dependents();
   const int c0 = __ldg(cu + b);  // request input: issued before the dependency wait
@@ -190,21 +189,28 @@ __global__ void __launch_bounds__(32 * NW, MINB)
   const float inv0 = 1.f / l_run[0], inv1 = 1.f / l_run[1];
   const int r0 = q0 + warp * 16 + gr;
   half* out = ctx + ((long long)g * group_rows + s0) * hidden + h * D;
+  // context as an fp16 (hi, lo) pair: the O projection reads both terms (lo at out + lo_off)
 #pragma unroll
   for (int dt = 0; dt < D / 8; ++dt) {
     const int c = dt * 8 + 2 * tq;
-    if (r0 < L)
-      *reinterpret_cast<__half2*>(out + (long long)r0 * hidden + c) = __floats2half2_rn(o[dt][0] * inv0, o[dt][1] * inv0);
-    if (r0 + 8 < L)
-      *reinterpret_cast<__half2*>(out + (long long)(r0 + 8) * hidden + c) =
-          __floats2half2_rn(o[dt][2] * inv1, o[dt][3] * inv1);
+    uint32_t hi, lo;
+    if (r0 < L) {
+      split_half2(o[dt][0] * inv0, o[dt][1] * inv0, hi, lo);
+      *reinterpret_cast<uint32_t*>(out + (long long)r0 * hidden + c) = hi;
+      *reinterpret_cast<uint32_t*>(out + lo_off + (long long)r0 * hidden + c) = lo;
+    }
+    if (r0 + 8 < L) {
+      split_half2(o[dt][2] * inv1, o[dt][3] * inv1, hi, lo);
+      *reinterpret_cast<uint32_t*>(out + (long long)(r0 + 8) * hidden + c) = hi;
+      *reinterpret_cast<uint32_t*>(out + lo_off + (long long)(r0 + 8) * hidden + c) = lo;
+    }
   }
 }
 
 template <int D, int NW, int MINB, int NBUF>
-static void launch_attn_t(const half* qkv, half* ctx, const int* cu, int n_seqs, int max_len, int groups,
-                          int n_heads, int hidden, long long group_rows, float scale_log2, const void* pf_ptr,
-                          unsigned long long pf_bytes, cudaStream_t stream) {
+static void launch_attn_t(const half* qkv, half* ctx, long long lo_off, const int* cu, int n_seqs, int max_len,
+                          int groups, int n_heads, int hidden, long long group_rows, float scale_log2,
+                          cudaStream_t stream) {
   constexpr int BQ = 16 * NW, LD = D + 8;
   const size_t smem = (size_t)(BQ + 2 * NBUF * 64) * LD * sizeof(half);
   static bool attr_set = false;
@@ -214,62 +220,31 @@ static void launch_attn_t(const half* qkv, half* ctx, const int* cu, int n_seqs,
   }
   dim3 grid((max_len + BQ - 1) / BQ, n_seqs, groups * n_heads);
   launch_pdl(attn_kernel<D, NW, MINB, NBUF>, grid, dim3(32 * NW), smem, stream, qkv, ctx, cu, n_heads, hidden, group_rows,
-             scale_log2, pf_ptr, pf_bytes);
+             scale_log2, lo_off);
 }
 
-void launch_attention(const half* qkv, half* ctx, const int* cu_seqlens, int n_seqs, int max_len, int groups,
-                      int n_heads, int head_dim, int hidden, long long group_rows, cudaStream_t stream,
-                      const void* pf_ptr, unsigned long long pf_bytes) {
+void launch_attention(const half* qkv, half* ctx, long long lo_off, const int* cu_seqlens, int n_seqs, int max_len,
+                      int groups, int n_heads, int head_dim, int hidden, long long group_rows, cudaStream_t stream) {
   if (n_seqs <= 0 || max_len <= 0 || groups <= 0) return;
   const float scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(head_dim));
-  // query-tile height: SP_ATTN_NW overrides (4, 6 or 8 warps of 16 rows); default by length
-  static const int nw_env = [] {
-    const char* v = getenv("SP_ATTN_NW");
-    return v ? atoi(v) : 0;
-  }();
-  // measured sweep (tools/attn_bench.py); 385..448: 64-query tiles at 4 CTAs/SM balance the waves
-  // that 128-query tiles quantize (4 tiles per head), 26 vs 29 us
-  const int nw = nw_env ? nw_env : (max_len <= 128 ? 4 : (max_len <= 288 ? 6 : (max_len <= 384 ? 8 : 4)));
-  // resident CTAs per SM (register cap): SP_ATTN_MINB overrides the default (4 for 4 warps, else 2)
-  static const int minb_env = [] {
-    const char* v = getenv("SP_ATTN_MINB");
-    return v ? atoi(v) : 0;
-  }();
-  const int minb = minb_env ? minb_env : (nw == 4 ? 4 : 2);
-  // K/V ring depth: SP_ATTN_NBUF overrides (2 or 4)
-  static const int nbuf_env = [] {
-    const char* v = getenv("SP_ATTN_NBUF");
-    return v ? atoi(v) : 0;
-  }();
-  const int nbuf = nbuf_env ? nbuf_env : 2;  // 4 measured no faster: attention is compute-bound per CTA
-#define SP_ATTN_B(D_, NW_, B_)                                                                                      \
-  do {                                                                                                             \
-    if (nbuf >= 4)                                                                                                 \
-      launch_attn_t<D_, NW_, B_, 4>(qkv, ctx, cu_seqlens, n_seqs, max_len, groups, n_heads, hidden, group_rows,    \
-                                    scale_log2, pf_ptr, pf_bytes, stream);                                         \
-    else                                                                                                           \
-      launch_attn_t<D_, NW_, B_, 2>(qkv, ctx, cu_seqlens, n_seqs, max_len, groups, n_heads, hidden, group_rows,    \
-                                    scale_log2, pf_ptr, pf_bytes, stream);                                         \
-  } while (0)
-#define SP_ATTN(D_, NW_)                                     \
-  do {                                                      \
-    if (minb >= 6) SP_ATTN_B(D_, NW_, 6);                   \
-    else if (minb == 5) SP_ATTN_B(D_, NW_, 5);              \
-    else if (minb == 4) SP_ATTN_B(D_, NW_, 4);              \
-    else if (minb == 3) SP_ATTN_B(D_, NW_, 3);              \
-    else SP_ATTN_B(D_, NW_, 2);                             \
-  } while (0)
+  // query-tile height by length (measured sweep, tools/attn_bench.py); 385..448: 64-query tiles at
+  // 4 CTAs/SM balance the waves that 128-query tiles quantize (4 tiles per head), 26 vs 29 us.
+  // Resident CTAs per SM: 4 for 4 warps, else 2; a 2-deep K/V ring (4 measured no faster: the
+  // kernel is compute-bound per CTA).
+  const int nw = max_len <= 128 ? 4 : (max_len <= 288 ? 6 : (max_len <= 384 ? 8 : 4));
+#define SP_ATTN(D_, NW_, B_) \
+  launch_attn_t<D_, NW_, B_, 2>(qkv, ctx, lo_off, cu_seqlens, n_seqs, max_len, groups, n_heads, hidden, group_rows, \
+                                scale_log2, stream)
   if (head_dim == 64) {
-    if (nw == 8) SP_ATTN(64, 8);
-    else if (nw == 6) SP_ATTN(64, 6);
-    else SP_ATTN(64, 4);
+    if (nw == 8) SP_ATTN(64, 8, 2);
+    else if (nw == 6) SP_ATTN(64, 6, 2);
+    else SP_ATTN(64, 4, 4);
   } else {
-    if (nw == 8) SP_ATTN(32, 8);
-    else if (nw == 6) SP_ATTN(32, 6);
-    else SP_ATTN(32, 4);
+    if (nw == 8) SP_ATTN(32, 8, 2);
+    else if (nw == 6) SP_ATTN(32, 6, 2);
+    else SP_ATTN(32, 4, 4);
   }
 #undef SP_ATTN
-#undef SP_ATTN_B
 }
 
 }  // namespace sp

@@ -17,6 +17,7 @@
 // No reference counterpart; semantics = oracle/bert.py:attention.
 #include "sp_kernels.cuh"
 #include "sp_ptx.cuh"
+#include "sp_device.cuh"
 
 namespace sp {
 
@@ -41,7 +42,7 @@ __device__ __forceinline__ float tc_exp2(float x) {
 
 __global__ void __launch_bounds__(kTcThreads, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap map_qkv, half* __restrict__ ctx, const int* __restrict__ cu,
-                   int n_heads, int hidden, long long group_rows, float scale_log2, int max_chunks) {
+                   int n_heads, int hidden, long long group_rows, float scale_log2, int max_chunks, long long lo_off) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;
@@ -230,14 +231,14 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     if (q0 + row < L) {
       const float inv = 1.f / l;
       half* out = ctx + (static_cast<long long>(row_base) + q0 + row) * hidden + h * 64 + wq * 16;
-      uint32_t w8[8];
+      uint32_t w8[8], l8[8];  // (hi, lo) pair, lo at out + lo_off
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        __half2 hv = __floats2half2_rn(__uint_as_float(o[2 * i]) * inv, __uint_as_float(o[2 * i + 1]) * inv);
-        w8[i] = *reinterpret_cast<uint32_t*>(&hv);
-      }
+      for (int i = 0; i < 8; ++i)
+        split_half2(__uint_as_float(o[2 * i]) * inv, __uint_as_float(o[2 * i + 1]) * inv, w8[i], l8[i]);
       *reinterpret_cast<uint4*>(out) = make_uint4(w8[0], w8[1], w8[2], w8[3]);
       *reinterpret_cast<uint4*>(out + 8) = make_uint4(w8[4], w8[5], w8[6], w8[7]);
+      *reinterpret_cast<uint4*>(out + lo_off) = make_uint4(l8[0], l8[1], l8[2], l8[3]);
+      *reinterpret_cast<uint4*>(out + lo_off + 8) = make_uint4(l8[4], l8[5], l8[6], l8[7]);
     }
   }
   tc_fence_before();
@@ -253,8 +254,8 @@ size_t attn_tc_smem_bytes(int max_len) {
   return 1024 + kTileBytes * (1 + 2 * chunks + 4) + 128 * 4 * 4 + 256;
 }
 
-void launch_attention_tc(const CUtensorMap& map_qkv, half* ctx, const int* cu_seqlens, int n_seqs, int max_len,
-                         int groups, int n_heads, int hidden, long long group_rows, cudaStream_t stream) {
+void launch_attention_tc(const CUtensorMap& map_qkv, half* ctx, long long lo_off, const int* cu_seqlens, int n_seqs,
+                         int max_len, int groups, int n_heads, int hidden, long long group_rows, cudaStream_t stream) {
   if (n_seqs <= 0 || max_len <= 0 || groups <= 0) return;
   static bool attr_set = false;
   if (!attr_set) {
@@ -265,7 +266,7 @@ void launch_attention_tc(const CUtensorMap& map_qkv, half* ctx, const int* cu_se
   const float scale_log2 = 1.4426950408889634f / 8.0f;  // log2(e) / sqrt(64)
   dim3 grid((max_len + 127) / 128, n_seqs, groups * n_heads);
   launch_pdl(attn_tc_kernel, grid, dim3(kTcThreads), attn_tc_smem_bytes(max_len), stream, map_qkv, ctx, cu_seqlens, n_heads,
-             hidden, group_rows, scale_log2, chunks);
+             hidden, group_rows, scale_log2, chunks, lo_off);
 }
 
 }  // namespace sp

@@ -23,6 +23,7 @@
 // No reference counterpart; semantics = oracle/bert.py:attention.
 #include "sp_kernels.cuh"
 #include "sp_ptx.cuh"
+#include "sp_device.cuh"
 
 #include <cstdlib>
 
@@ -96,7 +97,8 @@ __device__ __forceinline__ float ex2(float x) {
 template <bool TRACE, int SPLIT>
 __global__ void __launch_bounds__(Tc2Cfg<SPLIT>::kThreads, Tc2Cfg<SPLIT>::kMinBlocks)
     attn_tc2_kernel(const __grid_constant__ CUtensorMap map_qkv, half* __restrict__ ctx, const int* __restrict__ cu,
-                    int n_heads, int hidden, long long group_rows, float scale_log2, unsigned long long* tr) {
+                    int n_heads, int hidden, long long group_rows, float scale_log2, unsigned long long* tr,
+                    long long lo_off) {
   using C = Tc2Cfg<SPLIT>;
   constexpr int kSoftWarps = C::kSoftWarps, kProd = C::kProd, kMma = C::kMma, NG = C::kGroups;
   extern __shared__ uint8_t smem_raw[];
@@ -327,16 +329,16 @@ __global__ void __launch_bounds__(Tc2Cfg<SPLIT>::kThreads, Tc2Cfg<SPLIT>::kMinBl
         const float inv = 1.f / l;
         uint4* out = reinterpret_cast<uint4*>(ctx + (static_cast<long long>(row_base) + q0 + row) * hidden + h * 64 +
                                               hf * OC);
+        uint4* out_lo = reinterpret_cast<uint4*>(reinterpret_cast<half*>(out) + lo_off);
 #pragma unroll
         for (int v = 0; v < OC / 8; ++v) {
-          uint32_t w[4];
+          uint32_t w[4], l[4];  // (hi, lo) pair
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            __half2 hv = __floats2half2_rn(__uint_as_float(o[v * 8 + 2 * i]) * inv,
-                                           __uint_as_float(o[v * 8 + 2 * i + 1]) * inv);
-            w[i] = *reinterpret_cast<uint32_t*>(&hv);
-          }
+          for (int i = 0; i < 4; ++i)
+            split_half2(__uint_as_float(o[v * 8 + 2 * i]) * inv, __uint_as_float(o[v * 8 + 2 * i + 1]) * inv, w[i],
+                        l[i]);
           out[v] = make_uint4(w[0], w[1], w[2], w[3]);
+          out_lo[v] = make_uint4(l[0], l[1], l[2], l[3]);
         }
       }
     }
@@ -357,8 +359,8 @@ static unsigned long long* g_attn_trace = nullptr;
 void set_attn_trace(unsigned long long* buf) { g_attn_trace = buf; }
 
 template <int SPLIT>
-static void launch_tc2_t(const CUtensorMap& map_qkv, half* ctx, const int* cu_seqlens, dim3 grid, int n_heads,
-                         int hidden, long long group_rows, float scale_log2, cudaStream_t stream) {
+static void launch_tc2_t(const CUtensorMap& map_qkv, half* ctx, long long lo_off, const int* cu_seqlens, dim3 grid,
+                         int n_heads, int hidden, long long group_rows, float scale_log2, cudaStream_t stream) {
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(attn_tc2_kernel<false, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -370,25 +372,20 @@ static void launch_tc2_t(const CUtensorMap& map_qkv, half* ctx, const int* cu_se
   const dim3 block(Tc2Cfg<SPLIT>::kThreads);
   if (g_attn_trace)
     launch_pdl(attn_tc2_kernel<true, SPLIT>, grid, block, attn_tc2_smem_bytes(), stream, map_qkv, ctx, cu_seqlens,
-               n_heads, hidden, group_rows, scale_log2, g_attn_trace);
+               n_heads, hidden, group_rows, scale_log2, g_attn_trace, lo_off);
   else
     launch_pdl(attn_tc2_kernel<false, SPLIT>, grid, block, attn_tc2_smem_bytes(), stream, map_qkv, ctx, cu_seqlens,
-               n_heads, hidden, group_rows, scale_log2, static_cast<unsigned long long*>(nullptr));
+               n_heads, hidden, group_rows, scale_log2, static_cast<unsigned long long*>(nullptr), lo_off);
 }
 
-void launch_attention_tc2(const CUtensorMap& map_qkv, half* ctx, const int* cu_seqlens, int n_seqs, int max_len,
-                          int groups, int n_heads, int hidden, long long group_rows, cudaStream_t stream) {
+// Two softmax warps per TMEM lane quadrant (SPLIT = 2: each thread owns a 64-key half of its row;
+// -1.5..2 us per layer at L > 384 against one thread per full row).
+void launch_attention_tc2(const CUtensorMap& map_qkv, half* ctx, long long lo_off, const int* cu_seqlens, int n_seqs,
+                          int max_len, int groups, int n_heads, int hidden, long long group_rows, cudaStream_t stream) {
   if (n_seqs <= 0 || max_len <= 0 || groups <= 0) return;
-  static const int split = [] {  // SP_ATTN_SPLIT: softmax warps per TMEM lane quadrant (1 or 2)
-    const char* v = getenv("SP_ATTN_SPLIT");
-    return v ? atoi(v) : 2;
-  }();
   const float scale_log2 = 1.4426950408889634f / 8.0f;  // log2(e) / sqrt(64)
   dim3 grid(groups * n_heads, n_seqs, (max_len + 127) / 128);
-  if (split == 1)
-    launch_tc2_t<1>(map_qkv, ctx, cu_seqlens, grid, n_heads, hidden, group_rows, scale_log2, stream);
-  else
-    launch_tc2_t<2>(map_qkv, ctx, cu_seqlens, grid, n_heads, hidden, group_rows, scale_log2, stream);
+  launch_tc2_t<2>(map_qkv, ctx, lo_off, cu_seqlens, grid, n_heads, hidden, group_rows, scale_log2, stream);
 }
 
 
@@ -409,7 +406,7 @@ constexpr uint32_t k3ColS = 0, k3ColO = 64;
 __global__ void __launch_bounds__(kT3Threads, 3)
     attn_tc3_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_kv,
                     half* __restrict__ ctx, const int* __restrict__ cu, int n_heads, int hidden, long long group_rows,
-                    float scale_log2) {
+                    float scale_log2, long long lo_off) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;                 // 16 KiB
@@ -580,6 +577,8 @@ __global__ void __launch_bounds__(kT3Threads, 3)
       tc_fence_after();
       const float inv = 1.f / l;
       uint4* out = reinterpret_cast<uint4*>(ctx + (static_cast<long long>(row_base) + q0 + row) * hidden + h * 64);
+      uint4* out_lo = reinterpret_cast<uint4*>(ctx + lo_off + (static_cast<long long>(row_base) + q0 + row) * hidden +
+                                               h * 64);
 #pragma unroll
       for (int c = 0; c < 4; ++c) {  // 16 output columns at a time
         uint32_t o[16];
@@ -588,14 +587,13 @@ __global__ void __launch_bounds__(kT3Threads, 3)
         if (q0 + row < L) {
 #pragma unroll
           for (int v = 0; v < 2; ++v) {
-            uint32_t w[4];
+            uint32_t w[4], l[4];  // (hi, lo) pair
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              __half2 hv = __floats2half2_rn(__uint_as_float(o[v * 8 + 2 * i]) * inv,
-                                             __uint_as_float(o[v * 8 + 2 * i + 1]) * inv);
-              w[i] = *reinterpret_cast<uint32_t*>(&hv);
-            }
+            for (int i = 0; i < 4; ++i)
+              split_half2(__uint_as_float(o[v * 8 + 2 * i]) * inv, __uint_as_float(o[v * 8 + 2 * i + 1]) * inv,
+                          w[i], l[i]);
             out[2 * c + v] = make_uint4(w[0], w[1], w[2], w[3]);
+            out_lo[2 * c + v] = make_uint4(l[0], l[1], l[2], l[3]);
           }
         }
       }
@@ -611,9 +609,9 @@ __global__ void __launch_bounds__(kT3Threads, 3)
 
 size_t attn_tc3_smem_bytes() { return 1024 + kTile + 4 * kKv64 + 128; }
 
-void launch_attention_tc3(const CUtensorMap& map_q, const CUtensorMap& map_kv, half* ctx, const int* cu_seqlens,
-                          int n_seqs, int max_len, int groups, int n_heads, int hidden, long long group_rows,
-                          cudaStream_t stream) {
+void launch_attention_tc3(const CUtensorMap& map_q, const CUtensorMap& map_kv, half* ctx, long long lo_off,
+                          const int* cu_seqlens, int n_seqs, int max_len, int groups, int n_heads, int hidden,
+                          long long group_rows, cudaStream_t stream) {
   if (n_seqs <= 0 || max_len <= 0 || groups <= 0) return;
   static bool attr_set = false;
   if (!attr_set) {
@@ -624,7 +622,7 @@ void launch_attention_tc3(const CUtensorMap& map_q, const CUtensorMap& map_kv, h
   const float scale_log2 = 1.4426950408889634f / 8.0f;
   dim3 grid(groups * n_heads, n_seqs, (max_len + 127) / 128);
   launch_pdl(attn_tc3_kernel, grid, dim3(kT3Threads), attn_tc3_smem_bytes(), stream, map_q, map_kv, ctx, cu_seqlens,
-             n_heads, hidden, group_rows, scale_log2);
+             n_heads, hidden, group_rows, scale_log2, lo_off);
 }
 
 }  // namespace sp

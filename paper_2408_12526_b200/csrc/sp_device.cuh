@@ -36,6 +36,18 @@ __device__ __forceinline__ uint32_t pack_half2(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
+// Every activation a GEMM reads is stored as an fp16 pair (hi, lo) with hi = fp16(x) and
+// lo = fp16(x - hi): the GEMM issues one MMA per term into the same fp32 accumulator, so the operand
+// carries ~22 significant bits instead of 11 (fp16 rounding of the LayerNorm / attention / GELU
+// outputs alone moved the logits by up to 1.2e-3 relative; profiles/r1_precision_anatomy.txt).
+__device__ __forceinline__ void split_half2(float a, float b, uint32_t& hi, uint32_t& lo) {
+  const __half2 h = __floats2half2_rn(a, b);
+  const float2 hf = __half22float2(h);
+  const __half2 l = __floats2half2_rn(a - hf.x, b - hf.y);
+  hi = *reinterpret_cast<const uint32_t*>(&h);
+  lo = *reinterpret_cast<const uint32_t*>(&l);
+}
+
 __device__ __forceinline__ void ldmatrix_x4(uint32_t (&r)[4], const void* p) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
@@ -72,9 +84,12 @@ __device__ __forceinline__ int seq_of(const int* cu, int n_seqs, int t) {
 }
 
 // Each lane owns NC chunks of 4 consecutive features: feature = c*128 + lane*4 + j.
+// Writes the fp32 residual stream x32 and the (hi, lo) fp16 GEMM operand (lo at x16 + x_lo_off),
+// plus the same pair for the CLS row (cls16, cls16 + cls_lo_off) when cls16 is set.
 template <int NC>
 __device__ __forceinline__ void layer_norm_store(float (&v)[NC][4], const float* gamma, const float* beta, float eps,
-                                                 int hidden, float* x32, half* x16, half* cls16) {
+                                                 int hidden, float* x32, half* x16, long long x_lo_off, half* cls16,
+                                                 long long cls_lo_off) {
   const int lane = lane_id();
   float s = 0.f;
 #pragma unroll
@@ -106,10 +121,15 @@ __device__ __forceinline__ void layer_norm_store(float (&v)[NC][4], const float*
     y.z = (v[c][2] - mean) * rstd * gm[c].z + bt[c].z;
     y.w = (v[c][3] - mean) * rstd * gm[c].w + bt[c].w;
     *reinterpret_cast<float4*>(x32 + f) = y;
-    __half2 h01 = __floats2half2_rn(y.x, y.y), h23 = __floats2half2_rn(y.z, y.w);
-    uint2 packed = make_uint2(*reinterpret_cast<uint32_t*>(&h01), *reinterpret_cast<uint32_t*>(&h23));
-    *reinterpret_cast<uint2*>(x16 + f) = packed;
-    if (cls16) *reinterpret_cast<uint2*>(cls16 + f) = packed;
+    uint2 hi, lo;
+    split_half2(y.x, y.y, hi.x, lo.x);
+    split_half2(y.z, y.w, hi.y, lo.y);
+    *reinterpret_cast<uint2*>(x16 + f) = hi;
+    *reinterpret_cast<uint2*>(x16 + x_lo_off + f) = lo;
+    if (cls16) {
+      *reinterpret_cast<uint2*>(cls16 + f) = hi;
+      *reinterpret_cast<uint2*>(cls16 + cls_lo_off + f) = lo;
+    }
   }
 }
 

@@ -50,27 +50,55 @@ __device__ __forceinline__ float apply_act(float y) {
   else return y;
 }
 
+// Epilogue store of one warp's 32-feature x n-token block: stage rows in the warp's smem slice,
+// then 16-byte row stores (rows past t_rows are skipped).
+template <typename OutT, int NR>
+__device__ __forceinline__ void warp_store_rows(const float (&y)[NR], int n, OutT* stage, OutT* out, int t0,
+                                                int t_rows, int out_ld, bool lo_term) {
+  constexpr int kRowBytes = 32 * static_cast<int>(sizeof(OutT));
+  constexpr int kLanesPerRow = kRowBytes / 16;
+  constexpr int kRowsPerPass = 32 / kLanesPerRow;
+  const int lane = lane_id();
+#pragma unroll
+  for (int j = 0; j < NR; ++j) {
+    if constexpr (std::is_same<OutT, float>::value) {
+      stage[j * 32 + lane] = y[j];
+    } else {
+      const half h = __float2half_rn(y[j]);
+      stage[j * 32 + lane] = lo_term ? __float2half_rn(y[j] - __half2float(h)) : h;
+    }
+  }
+  __syncwarp();
+  const int sub = lane % kLanesPerRow;
+  for (int j0 = 0; j0 < n; j0 += kRowsPerPass) {
+    const int j = j0 + lane / kLanesPerRow;
+    const int t = t0 + j;
+    if (j < n && t < t_rows) {
+      const uint4 v = *reinterpret_cast<const uint4*>(reinterpret_cast<const uint8_t*>(stage) + j * kRowBytes + sub * 16);
+      *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(out + (long long)t * out_ld) + sub * 16) = v;
+    }
+  }
+  __syncwarp();
+}
+
 template <int ACT, bool OUT_F32>
 __global__ void __launch_bounds__(kThreads, 2)
-    gemm_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_x64,
-                const __grid_constant__ CUtensorMap map_x16, const GemmParams p) {
+    gemm_kernel(const __grid_constant__ GemmMaps maps, const GemmParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const int stage_bytes = kATileBytes + p.bn * 128;
+  const int x_bytes = p.bn * 128;                            // one term of the token tile
+  const int stage_bytes = kATileBytes + x_bytes * (p.hilo ? 2 : 1);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.stages * stage_bytes);
   uint64_t* empty = full + p.stages;
   uint64_t* tmem_full = empty + p.stages;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
 
-  // m-tile fastest: the two CTAs of a cluster are neighbouring m-tiles of the same token tile
   int bid = blockIdx.x;
   const int mt = bid % p.m_tiles;
   bid /= p.m_tiles;
   const int nt = bid % p.n_tiles;
   const int split = bid / p.n_tiles;
-  const bool pair = p.cluster == 2;
-  const uint32_t crank = pair ? cluster_ctarank() : 0u;
-  const int g = blockIdx.y + p.g0;
+  const int g = blockIdx.y;
   const int m0 = mt * kBlockM;
   const int n0 = nt * p.bn;
   const int nkb = p.k_dim / kBlockK;
@@ -81,24 +109,25 @@ __global__ void __launch_bounds__(kThreads, 2)
   const int lane = lane_id();
   unsigned long long* tr = p.trace ? p.trace + 8ull * (blockIdx.y * gridDim.x + blockIdx.x) : nullptr;
   if (tr && threadIdx.x == 0) tr[0] = globaltimer();
+  // weights: streamed once per request -> evict_first, unless several token tiles re-read them
+  const uint64_t pol_w = (p.n_tiles > 1 && p.w_keep) ? policy_evict_last() : policy_evict_first();
+  const int n_pre = min(p.stages, kb1 - kb0);
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < p.stages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], pair ? 2 : 1);  // a stage is free once every consumer in the pair released it
+      mbar_init(&empty[s], 1);
     }
     mbar_init(tmem_full, 1);
     fence_barrier_init();
-    tma_prefetch_desc(&map_w);
-    if (!pair) {  // first weight stages right away: independent of the TMEM allocation and the CTA barrier
-      const uint64_t pol_w = (p.n_tiles > 1 && p.w_keep) ? policy_evict_last() : policy_evict_first();
-      const int n_pre = min(p.stages, kb1 - kb0);
-      for (int i = 0; i < n_pre; ++i) {
-        mbar_arrive_expect_tx(&full[i], stage_bytes);
-        tma_load_2d(&map_w, &full[i], smem + i * stage_bytes, (kb0 + i) * kBlockK, g * p.n_out + m0, pol_w);
-      }
+    tma_prefetch_desc(&maps.w);
+    // first weight stages right away: independent of the TMEM allocation, the CTA barrier and the
+    // previous kernel (weights never depend on it)
+    for (int i = 0; i < n_pre; ++i) {
+      mbar_arrive_expect_tx(&full[i], stage_bytes);
+      tma_load_2d(&maps.w, &full[i], smem + i * stage_bytes, (kb0 + i) * kBlockK, g * p.n_out + m0, pol_w);
     }
-    tma_prefetch_desc(&map_x64);
-    tma_prefetch_desc(&map_x16);
+    tma_prefetch_desc(&maps.x64);
+    tma_prefetch_desc(&maps.x16);
   }
   if (warp == 1) {
     tmem_alloc(tmem_slot, tmem_cols_for(p.bn));
@@ -106,7 +135,6 @@ __global__ void __launch_bounds__(kThreads, 2)
   }
   tc_fence_before();
   __syncthreads();
-  if (pair) cluster_sync();  // peer barriers initialised before any multicast lands in them
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   pdl_launch_dependents();
@@ -114,39 +142,22 @@ __global__ void __launch_bounds__(kThreads, 2)
 
   if (warp == 0) {
     if (elect_one()) {
-      // weights: streamed once per request -> evict_first, unless several token tiles re-read them
-      const uint64_t pol_w = (p.n_tiles > 1 && p.w_keep) ? policy_evict_last() : policy_evict_first();
       const uint64_t pol_x = policy_evict_last();   // activations: re-read by every M tile
       const int wrow = g * p.n_out + m0;
       const int xrow = g * p.x_group_rows + n0;
-      // token tile: alone, or (pair) this CTA's half multicast into both CTAs of the cluster
-      const int r_begin = pair ? static_cast<int>(crank) * (p.bn >> 1) : 0;
-      const int r_end = pair ? r_begin + (p.bn >> 1) : p.bn;
       auto load_x = [&](int s, int kb) {
         uint8_t* sb = smem + s * stage_bytes + kATileBytes;
         const int kc = kb * kBlockK;
-        int r = r_begin;
-        if (pair) {
-          for (; r + 64 <= r_end; r += 64)
-            tma_load_2d_mc(&map_x64, &full[s], sb + r * 128, kc, xrow + r, 0x3, pol_x);
-          for (; r < r_end; r += 16) tma_load_2d_mc(&map_x16, &full[s], sb + r * 128, kc, xrow + r, 0x3, pol_x);
-        } else {
-          for (; r + 64 <= r_end; r += 64) tma_load_2d(&map_x64, &full[s], sb + r * 128, kc, xrow + r, pol_x);
-          for (; r < r_end; r += 16) tma_load_2d(&map_x16, &full[s], sb + r * 128, kc, xrow + r, pol_x);
+        for (int term = 0; term < (p.hilo ? 2 : 1); ++term, sb += x_bytes) {
+          const CUtensorMap* m64 = term ? &maps.xl64 : &maps.x64;
+          const CUtensorMap* m16 = term ? &maps.xl16 : &maps.x16;
+          int r = 0;
+          for (; r + 64 <= p.bn; r += 64) tma_load_2d(m64, &full[s], sb + r * 128, kc, xrow + r, pol_x);
+          for (; r < p.bn; r += 16) tma_load_2d(m16, &full[s], sb + r * 128, kc, xrow + r, pol_x);
         }
       };
-      // 1) weight prefetch: independent of the previous kernel. The first stages go straight to
-      //    smem; the rest of this CTA's weight slab is optionally pulled into L2.
-      const int n_pre = min(p.stages, kb1 - kb0);
-      if (pair)  // (pair: the peer's barriers are initialised only after cluster_sync)
-        for (int i = 0; i < n_pre; ++i) {
-          mbar_arrive_expect_tx(&full[i], stage_bytes);
-          tma_load_2d(&map_w, &full[i], smem + i * stage_bytes, (kb0 + i) * kBlockK, wrow, pol_w);
-        }
-      if (p.l2_prefetch)
-        for (int kb = kb0 + n_pre; kb < kb1; ++kb) tma_prefetch_l2_2d(&map_w, kb * kBlockK, wrow);
       if (tr) tr[2] = globaltimer();
-      // 2) activations are produced by the previous kernel
+      // activations are produced by the previous kernel
       pdl_wait();
       for (int i = 0; i < n_pre; ++i) load_x(i, kb0 + i);
       int s = n_pre % p.stages;
@@ -154,14 +165,13 @@ __global__ void __launch_bounds__(kThreads, 2)
       for (int kb = kb0 + n_pre; kb < kb1; ++kb) {
         mbar_wait(&empty[s], ph ^ 1);
         mbar_arrive_expect_tx(&full[s], stage_bytes);
-        tma_load_2d(&map_w, &full[s], smem + s * stage_bytes, kb * kBlockK, wrow, pol_w);
+        tma_load_2d(&maps.w, &full[s], smem + s * stage_bytes, kb * kBlockK, wrow, pol_w);
         load_x(s, kb);
         if (++s == p.stages) {
           s = 0;
           ph ^= 1;
         }
       }
-      if (p.progress && nt == 0) atomicAdd(p.progress, (unsigned long long)(kb1 - kb0) * kATileBytes);
       if (tr) tr[3] = globaltimer();
     }
   } else if (warp == 1) {
@@ -176,13 +186,14 @@ __global__ void __launch_bounds__(kThreads, 2)
         const uint32_t sa = smem_u32(smem + s * stage_bytes);
         const uint64_t adesc = umma_sdesc_sw128(sa);
         const uint64_t bdesc = umma_sdesc_sw128(sa + kATileBytes);
+        const uint64_t ldesc = umma_sdesc_sw128(sa + kATileBytes + x_bytes);
 #pragma unroll
         for (int k = 0; k < kBlockK / 16; ++k) {
           // +32 bytes per K=16 slice inside the 128-byte swizzle row (address field in 16-byte units)
           umma_f16_ss(tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+          if (p.hilo) umma_f16_ss(tmem, adesc + 2 * k, ldesc + 2 * k, idesc, 1u);
         }
-        if (pair) umma_commit_mc(&empty[s], 0x3);
-        else umma_commit(&empty[s]);
+        umma_commit(&empty[s]);
         if (++s == p.stages) {
           s = 0;
           ph ^= 1;
@@ -204,10 +215,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     if (!partial && p.bias != nullptr) bias = __ldg(p.bias + (long long)g * p.bias_group_stride + feat);
     const bool has_k = kb1 > kb0;
     using OutT = typename std::conditional<OUT_F32, float, half>::type;
-    constexpr int kRowBytes = 32 * static_cast<int>(sizeof(OutT));  // one warp's 32 features of a token
-    constexpr int kLanesPerRow = kRowBytes / 16;
-    constexpr int kRowsPerPass = 32 / kLanesPerRow;
-    OutT* stage = reinterpret_cast<OutT*>(smem + e * 32 * kRowBytes);  // warp-private, pipeline smem is free now
+    OutT* stage = reinterpret_cast<OutT*>(smem + e * 32 * 32 * sizeof(OutT));  // warp-private, ring is free now
     OutT* out = reinterpret_cast<OutT*>(p.out) + (long long)g * p.out_group_stride +
                 (long long)split * p.out_split_stride + m0 + q * 32;
 
@@ -232,30 +240,15 @@ __global__ void __launch_bounds__(kThreads, 2)
         y[j] = has_k ? __uint_as_float(r[j]) : 0.f;
         if (!partial) y[j] = apply_act<ACT>(y[j] + bias);
       }
-#pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        if constexpr (OUT_F32) stage[j * 32 + lane] = y[j];
-        else stage[j * 32 + lane] = __float2half_rn(y[j]);
-      }
-      __syncwarp();
-      const int sub = lane % kLanesPerRow;
-      for (int j0 = 0; j0 < n; j0 += kRowsPerPass) {
-        const int j = j0 + lane / kLanesPerRow;
-        const int t = n0 + c + j;
-        if (j < n && t < t_rows) {
-          const uint4 v = *reinterpret_cast<const uint4*>(reinterpret_cast<const uint8_t*>(stage) + j * kRowBytes +
-                                                          sub * 16);
-          *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(out + (long long)t * p.out_ld) + sub * 16) = v;
-        }
-      }
-      __syncwarp();
+      warp_store_rows<OutT, 32>(y, n, stage, out, n0 + c, t_rows, p.out_ld, false);
+      if (!OUT_F32 && p.out_lo_off)
+        warp_store_rows<OutT, 32>(y, n, stage, out + p.out_lo_off, n0 + c, t_rows, p.out_ld, true);
     }
     if (tr && warp == 2 && lane == 0) tr[7] = globaltimer();
   }
 
   tc_fence_before();
   __syncthreads();
-  if (pair) cluster_sync();  // no CTA leaves while its peer may still signal its barriers
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem, tmem_cols_for(p.bn));
@@ -278,12 +271,9 @@ static constexpr int kPThreads = 64 + 32 * kPEpiWarps;
 
 template <int ACT, bool OUT_F32, bool PAIR>
 __global__ void __launch_bounds__(kPThreads, 1)
-    gemm_persistent_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_x64,
-                           const __grid_constant__ CUtensorMap map_x16, const GemmParams p) {
+    gemm_persistent_kernel(const __grid_constant__ GemmMaps maps, const GemmParams p) {
   using OutT = typename std::conditional<OUT_F32, float, half>::type;
   constexpr int kRowBytes = 32 * static_cast<int>(sizeof(OutT));
-  constexpr int kLanesPerRow = kRowBytes / 16;
-  constexpr int kRowsPerPass = 32 / kLanesPerRow;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   // pair mode (cluster of 2, cta_group::2): the pair computes a 256-feature x bn-token tile with one
@@ -295,8 +285,9 @@ __global__ void __launch_bounds__(kPThreads, 1)
   constexpr bool pair = PAIR;
   const uint32_t crank = pair ? cluster_ctarank() : 0u;
   const bool leader = crank == 0;
-  const int x_rows = pair ? (p.bn >> 1) : p.bn;  // token rows staged by this CTA
-  const int stage_bytes = kATileBytes + x_rows * 128;
+  const int x_rows = pair ? (p.bn >> 1) : p.bn;  // token rows staged by this CTA (per term)
+  const int x_bytes = x_rows * 128;
+  const int stage_bytes = kATileBytes + x_bytes * (p.hilo ? 2 : 1);
   uint8_t* staging = smem + p.stages * stage_bytes;  // 16 warps x 16 rows x kRowBytes
   uint64_t* full = reinterpret_cast<uint64_t*>(staging + kPEpiWarps * 16 * kRowBytes);
   uint64_t* empty = full + p.stages;
@@ -327,22 +318,22 @@ __global__ void __launch_bounds__(kPThreads, 1)
       mbar_init(&acc_empty[b], pair ? 2 * kPEpiWarps : kPEpiWarps);
     }
     fence_barrier_init();
-    tma_prefetch_desc(&map_w);
+    tma_prefetch_desc(&maps.w);
     if constexpr (!PAIR) {  // first unit's weight stages right away (before TMEM allocation / CTA barrier)
       if (u_first < units) {
-        const int g = u_first / units_per_group + p.g0;
+        const int g = u_first / units_per_group;
         const int mt = (u_first % units_per_group) % m_per;
         const uint64_t pol_w = p.w_keep == 2 ? policy_evict_last() : (p.w_keep == 1 ? policy_evict_normal()
                                                                                      : policy_evict_first());
         const int n_pre = min(p.stages, nkb);
         for (int i = 0; i < n_pre; ++i) {
           mbar_arrive_expect_tx(&full[i], full_bytes);
-          tma_load_2d(&map_w, &full[i], smem + i * stage_bytes, i * kBlockK, g * p.n_out + mt * kBlockM, pol_w);
+          tma_load_2d(&maps.w, &full[i], smem + i * stage_bytes, i * kBlockK, g * p.n_out + mt * kBlockM, pol_w);
         }
       }
     }
-    tma_prefetch_desc(&map_x64);
-    tma_prefetch_desc(&map_x16);
+    tma_prefetch_desc(&maps.x64);
+    tma_prefetch_desc(&maps.x16);
   }
   if (warp == 1) {
     if constexpr (PAIR) {
@@ -361,7 +352,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
   pdl_launch_dependents();
 
   auto decode = [&](int u, int& g, int& mt, int& nt) {
-    g = u / units_per_group + p.g0;
+    g = u / units_per_group;
     const int r = u % units_per_group;
     nt = r / m_per;
     mt = pair ? 2 * (r % m_per) + static_cast<int>(crank) : r % m_per;
@@ -373,18 +364,22 @@ __global__ void __launch_bounds__(kPThreads, 1)
                                                                                      : policy_evict_first());
       const uint64_t pol_x = policy_evict_last();
       auto load_w = [&](int s, int kb, int wrow) {
-        if constexpr (PAIR) tma_load_2d_2sm(&map_w, &full[s], smem + s * stage_bytes, kb * kBlockK, wrow, pol_w);
-        else tma_load_2d(&map_w, &full[s], smem + s * stage_bytes, kb * kBlockK, wrow, pol_w);
+        if constexpr (PAIR) tma_load_2d_2sm(&maps.w, &full[s], smem + s * stage_bytes, kb * kBlockK, wrow, pol_w);
+        else tma_load_2d(&maps.w, &full[s], smem + s * stage_bytes, kb * kBlockK, wrow, pol_w);
       };
       auto load_x = [&](int s, int kb, int xrow) {
         uint8_t* sb = smem + s * stage_bytes + kATileBytes;
-        int r = 0;
-        if constexpr (PAIR) {
-          for (; r + 64 <= x_rows; r += 64) tma_load_2d_2sm(&map_x64, &full[s], sb + r * 128, kb * kBlockK, xrow + r, pol_x);
-          for (; r < x_rows; r += 16) tma_load_2d_2sm(&map_x16, &full[s], sb + r * 128, kb * kBlockK, xrow + r, pol_x);
-        } else {
-          for (; r + 64 <= x_rows; r += 64) tma_load_2d(&map_x64, &full[s], sb + r * 128, kb * kBlockK, xrow + r, pol_x);
-          for (; r < x_rows; r += 16) tma_load_2d(&map_x16, &full[s], sb + r * 128, kb * kBlockK, xrow + r, pol_x);
+        for (int term = 0; term < (p.hilo ? 2 : 1); ++term, sb += x_bytes) {
+          const CUtensorMap* m64 = term ? &maps.xl64 : &maps.x64;
+          const CUtensorMap* m16 = term ? &maps.xl16 : &maps.x16;
+          int r = 0;
+          if constexpr (PAIR) {
+            for (; r + 64 <= x_rows; r += 64) tma_load_2d_2sm(m64, &full[s], sb + r * 128, kb * kBlockK, xrow + r, pol_x);
+            for (; r < x_rows; r += 16) tma_load_2d_2sm(m16, &full[s], sb + r * 128, kb * kBlockK, xrow + r, pol_x);
+          } else {
+            for (; r + 64 <= x_rows; r += 64) tma_load_2d(m64, &full[s], sb + r * 128, kb * kBlockK, xrow + r, pol_x);
+            for (; r < x_rows; r += 16) tma_load_2d(m16, &full[s], sb + r * 128, kb * kBlockK, xrow + r, pol_x);
+          }
         }
       };
       int s = 0;
@@ -403,8 +398,6 @@ __global__ void __launch_bounds__(kPThreads, 1)
               if (leader) mbar_arrive_expect_tx(&full[i], full_bytes);
               load_w(i, i, wrow);
             }
-          if (p.l2_prefetch)
-            for (int i = n_pre; i < nkb; ++i) tma_prefetch_l2_2d(&map_w, i * kBlockK, wrow);
           if (tr) tr[2] = globaltimer();
           pdl_wait();
           for (int i = 0; i < n_pre; ++i) load_x(i, i, xrow);
@@ -423,7 +416,6 @@ __global__ void __launch_bounds__(kPThreads, 1)
             ph ^= 1;
           }
         }
-        if (p.progress && nt == 0) atomicAdd(p.progress, (unsigned long long)nkb * kATileBytes);  // one count per slab
       }
       if (first) pdl_wait();  // no work: still honour the dependency
     }
@@ -450,15 +442,20 @@ __global__ void __launch_bounds__(kPThreads, 1)
           const uint32_t sa = smem_u32(smem + s * stage_bytes);
           const uint64_t adesc = umma_sdesc_sw128(sa);
           const uint64_t bdesc = umma_sdesc_sw128(sa + kATileBytes);
+          const uint64_t ldesc = umma_sdesc_sw128(sa + kATileBytes + x_bytes);  // lo term (hilo)
           if constexpr (PAIR) {
 #pragma unroll
-            for (int k = 0; k < kBlockK / 16; ++k)
+            for (int k = 0; k < kBlockK / 16; ++k) {
               umma_f16_ss_2sm(acc, adesc + 2 * k, bdesc + 2 * k, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+              if (p.hilo) umma_f16_ss_2sm(acc, adesc + 2 * k, ldesc + 2 * k, idesc, 1u);
+            }
             umma_commit_2sm_mc(&empty[s], 0x3);
           } else {
 #pragma unroll
-            for (int k = 0; k < kBlockK / 16; ++k)
+            for (int k = 0; k < kBlockK / 16; ++k) {
               umma_f16_ss(acc, adesc + 2 * k, bdesc + 2 * k, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+              if (p.hilo) umma_f16_ss(acc, adesc + 2 * k, ldesc + 2 * k, idesc, 1u);
+            }
             umma_commit(&empty[s]);
           }
           if (++s == p.stages) {
@@ -516,35 +513,9 @@ __global__ void __launch_bounds__(kPThreads, 1)
         float y[16];
 #pragma unroll
         for (int jj = 0; jj < 16; ++jj) y[jj] = apply_act<ACT>(__uint_as_float(r[jj]) + bias);
-        if (p.direct_store) {
-          // one warp store per token column: 32 consecutive features (64 B fp16 / 128 B fp32)
-          OutT* col = out + (long long)(n0 + c) * p.out_ld + lane;
-#pragma unroll
-          for (int jj = 0; jj < 16; ++jj) {
-            if (jj < n && n0 + c + jj < t_rows) {
-              if constexpr (OUT_F32) col[(long long)jj * p.out_ld] = y[jj];
-              else col[(long long)jj * p.out_ld] = __float2half_rn(y[jj]);
-            }
-          }
-          continue;
-        }
-#pragma unroll
-        for (int jj = 0; jj < 16; ++jj) {
-          if constexpr (OUT_F32) stage[jj * 32 + lane] = y[jj];
-          else stage[jj * 32 + lane] = __float2half_rn(y[jj]);
-        }
-        __syncwarp();
-        const int sub = lane % kLanesPerRow;
-        for (int j0 = 0; j0 < n; j0 += kRowsPerPass) {
-          const int jr = j0 + lane / kLanesPerRow;
-          const int t = n0 + c + jr;
-          if (jr < n && t < t_rows) {
-            const uint4 v = *reinterpret_cast<const uint4*>(reinterpret_cast<const uint8_t*>(stage) + jr * kRowBytes +
-                                                            sub * 16);
-            *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(out + (long long)t * p.out_ld) + sub * 16) = v;
-          }
-        }
-        __syncwarp();
+        warp_store_rows<OutT, 16>(y, n, stage, out, n0 + c, t_rows, p.out_ld, false);
+        if (!OUT_F32 && p.out_lo_off)
+          warp_store_rows<OutT, 16>(y, n, stage, out + p.out_lo_off, n0 + c, t_rows, p.out_ld, true);
       }
     }
     if (tr && warp == 2 && lane == 0) tr[7] = globaltimer();
@@ -581,8 +552,8 @@ static void launch_persistent_t(const GemmMaps& maps, const GemmParams& p, int g
   q.trace = trace_ptr_advance(grid);
   const int row_bytes = 32 * (OUT_F32 ? 4 : 2);
   const int x_rows = q.cluster == 2 ? p.bn / 2 : p.bn;
-  const size_t smem = static_cast<size_t>(q.stages) * (kATileBytes + x_rows * 128) + kPEpiWarps * 16 * row_bytes +
-                      1024 + 256;
+  const size_t smem = static_cast<size_t>(q.stages) * (kATileBytes + x_rows * 128 * (p.hilo ? 2 : 1)) +
+                      kPEpiWarps * 16 * row_bytes + 1024 + 256;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kPThreads);
@@ -597,43 +568,29 @@ static void launch_persistent_t(const GemmMaps& maps, const GemmParams& p, int g
   attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-  prefer_max_smem(q.cluster == 2 ? reinterpret_cast<const void*>(gemm_persistent_kernel<ACT, OUT_F32, true>)
-                                  : reinterpret_cast<const void*>(gemm_persistent_kernel<ACT, OUT_F32, false>));
-  if (q.cluster == 2) cudaLaunchKernelEx(&cfg, gemm_persistent_kernel<ACT, OUT_F32, true>, maps.w, maps.x64, maps.x16, q);
-  else cudaLaunchKernelEx(&cfg, gemm_persistent_kernel<ACT, OUT_F32, false>, maps.w, maps.x64, maps.x16, q);
+  if (q.cluster == 2) cudaLaunchKernelEx(&cfg, gemm_persistent_kernel<ACT, OUT_F32, true>, maps, q);
+  else cudaLaunchKernelEx(&cfg, gemm_persistent_kernel<ACT, OUT_F32, false>, maps, q);
 }
 
-// CTA pairs (cta_group::2) halve each CTA's token-tile traffic; SP_PERSIST_PAIR=0/1 forces them
-// off/on, default: from SP_PERSIST_PAIR_MIN_ROWS tokens (see DESIGN.md for the measured crossover).
+// CTA pairs (cta_group::2) halve each CTA's token-tile traffic: from 1024 tokens (batched load;
+// measured slower than single-CTA tiles below that).
 bool gemm_persistent_pair(int t_rows, int m_tiles, int groups) {
-  static const int pair_mode = [] {
-    const char* v = getenv("SP_PERSIST_PAIR");
-    return v == nullptr ? -1 : atoi(v);
-  }();
-  static const int min_rows = [] {
-    const char* v = getenv("SP_PERSIST_PAIR_MIN_ROWS");
-    return v ? atoi(v) : 1024;
-  }();
-  const bool on = pair_mode < 0 ? t_rows >= min_rows : pair_mode != 0;
-  return on && m_tiles % 2 == 0 && groups * m_tiles >= 4;
+  return t_rows >= 1024 && m_tiles % 2 == 0 && groups * m_tiles >= 4;
 }
 
 // Tile policy of the persistent path: pick the token-tile count that minimises the makespan
 // ceil(units / CTAs) x (fixed + bn) (bn <= 256), so projections with few feature tiles (O, FFN2:
 // 6 per student) still fill every SM; ring as deep as the smem left after staging.
+// Every operand is an (hi, lo) pair: two token terms per stage and two MMAs per k-slice.
 void gemm_configure_persistent(int t_rows, bool out_f32, int units_per_tile, int n_ctas, bool pair, int* bn,
                                int* n_tiles, int* stages) {
   // Cost of a tiling = rounds x per-unit time, in cycles per 64-wide k-block of one CTA:
-  //   MMA      2 * bn                          (128 x bn x 64 at 8192 flop/clk)
-  //   operands 3 * (128 + token rows staged)   (L2 -> SM at ~42 B/clk per SM, 12.4 TB/s / 148)
+  //   MMA      2 * 2 * bn                          (two 128 x bn x 64 MMAs at 8192 flop/clk)
+  //   operands 3 * (128 + 2 * token rows staged)   (L2 -> SM at ~42 B/clk per SM, 12.4 TB/s / 148)
   // plus ~200 cycles of per-unit fill / drain. Pairs stage half the token tile per CTA and run
   // units_per_tile / 2 units on n_ctas / 2 pairs.
   const int ctas = pair ? n_ctas / 2 : n_ctas;
   const int upt = pair ? units_per_tile / 2 : units_per_tile;
-  static const int force_bn = [] {  // experiment knob: fixed token-tile width
-    const char* v = getenv("SP_PERSIST_BN");
-    return v ? atoi(v) : 0;
-  }();
   int best_tiles = (t_rows + 255) / 256;
   long long best_cost = 0x7fffffffffffll;
   for (int tiles = (t_rows + 255) / 256; tiles <= (t_rows + 63) / 64; ++tiles) {
@@ -642,9 +599,8 @@ void gemm_configure_persistent(int t_rows, bool out_f32, int units_per_tile, int
     if (b > 256) continue;
     const int x = pair ? b / 2 : b;
     const long long rounds = (upt * (long long)tiles + ctas - 1) / ctas;
-    const long long unit = std::max(2LL * b, 3LL * (128 + x)) + 200;
-    long long cost = rounds * unit;
-    if (force_bn) cost = std::abs(b - force_bn);
+    const long long unit = std::max(4LL * b, 3LL * (128 + 2 * x)) + 200;
+    const long long cost = rounds * unit;
     if (cost < best_cost) {
       best_cost = cost;
       best_tiles = tiles;
@@ -656,7 +612,7 @@ void gemm_configure_persistent(int t_rows, bool out_f32, int units_per_tile, int
   *bn = b;
   *n_tiles = tiles;
   const int staging = kPEpiWarps * 16 * 32 * (out_f32 ? 4 : 2);
-  int st = (224 * 1024 - staging) / (kATileBytes + (pair ? b / 2 : b) * 128);
+  int st = (224 * 1024 - staging) / (kATileBytes + (pair ? b / 2 : b) * 128 * 2);
   if (st > 8) st = 8;
   if (st < 2) st = 2;
   *stages = st;
@@ -707,35 +663,25 @@ int gemm_trace_counts(int* out, int max) {
   return n;
 }
 
+// stage = weight tile + both token terms (the smem size does not depend on hilo being used)
 size_t gemm_smem_bytes(int bn, int stages) {
-  return static_cast<size_t>(stages) * (kATileBytes + bn * 128) + 1024 /*align*/ + 256 /*barriers*/;
+  return static_cast<size_t>(stages) * (kATileBytes + 2 * bn * 128) + 1024 /*align*/ + 256 /*barriers*/;
 }
 
-// Tile policy knobs (tuning sweeps): SP_GEMM_MAXBN (16..256; default 64 up to 128 tokens, else 128), SP_GEMM_SMEM_KB.
-static int env_int(const char* name, int dflt, int lo, int hi) {
-  const char* v = getenv(name);
-  if (!v) return dflt;
-  int x = atoi(v);
-  return x < lo ? lo : (x > hi ? hi : x);
-}
-
-void gemm_configure_tiles(int t_rows, bool cluster2, int* bn, int* n_tiles, int* stages) {
+void gemm_configure_tiles(int t_rows, int* bn, int* n_tiles, int* stages) {
   // token-tile cap: 64 up to 128 tokens (two tiles at 65-128 tokens: more CTAs stream the split-K
-  // weights, -4..-6 us at 96-128 measured in-graph), else 128; SP_GEMM_MAXBN overrides
-  static const int max_bn_env = env_int("SP_GEMM_MAXBN", 0, 0, kMaxBn);
-  const int max_bn = max_bn_env >= 16 ? max_bn_env : (t_rows <= 128 ? 64 : 128);
-  static const int smem_kb = env_int("SP_GEMM_SMEM_KB", 110, 40, 200);  // 6 stages at <= 32-token tiles
+  // weights, -4..-6 us at 96-128 measured in-graph), else 128
+  const int max_bn = t_rows <= 128 ? 64 : 128;
   int tiles = (t_rows + max_bn - 1) / max_bn;
   if (tiles < 1) tiles = 1;
   const int per = (t_rows + tiles - 1) / tiles;
-  const int gran = cluster2 ? 32 : 16;  // a pair splits the tile in halves of whole 16-row boxes
-  int b = ((per + gran - 1) / gran) * gran;
-  if (b < gran) b = gran;
+  int b = ((per + 15) / 16) * 16;
+  if (b < 16) b = 16;
   *bn = b;
   *n_tiles = tiles;
   // ~110 KiB per CTA so that two CTAs (e.g. the tail of one projection and the prefetching head
   // of the next, or two tiles of one projection) share an SM: smem 2 x <= 111 KiB, TMEM <= 2 x 128 cols.
-  int st = (smem_kb * 1024) / (kATileBytes + b * 128);
+  int st = (110 * 1024) / (kATileBytes + 2 * b * 128);
   if (st > 6) st = 6;
   if (st < 2) st = 2;
   *stages = st;
@@ -753,31 +699,23 @@ static void launch_gemm_t(const GemmMaps& maps, const GemmParams& p, int groups,
   cfg.blockDim = dim3(64 + 32 * p.epi_warps);
   cfg.dynamicSmemBytes = gemm_smem_bytes(p.bn, p.stages);
   cfg.stream = stream;
-  cudaLaunchAttribute attr[2];
+  cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
-  attr[1].id = cudaLaunchAttributeClusterDimension;
-  attr[1].val.clusterDim.x = p.cluster;
-  attr[1].val.clusterDim.y = 1;
-  attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 2;
+  cfg.numAttrs = 1;
   GemmParams q = p;
   q.trace = g_trace ? g_trace + 8 * g_trace_used : nullptr;
   if (g_trace) {
     g_trace_used += (size_t)cfg.gridDim.x * cfg.gridDim.y;
     g_trace_counts.push_back(static_cast<int>(cfg.gridDim.x * cfg.gridDim.y));
   }
-  prefer_max_smem(reinterpret_cast<const void*>(gemm_kernel<ACT, OUT_F32>));
-  cudaLaunchKernelEx(&cfg, gemm_kernel<ACT, OUT_F32>, maps.w, maps.x64, maps.x16, q);
+  cudaLaunchKernelEx(&cfg, gemm_kernel<ACT, OUT_F32>, maps, q);
 }
 
 // Epilogue warps of the small-T kernel: 4 (192 threads) unless the launch has several wide token
 // tiles (measured in-graph: 4 warps -1..-3 us at 96-192 tokens, 8 warps better at 256 = 2 x 128).
-int gemm_epi_warps(int bn, int n_tiles) {
-  static const int max_bn4 = env_int("SP_GEMM_EPI4_MAXBN", 96, 0, 256);
-  return (bn <= max_bn4 || n_tiles == 1) ? 4 : 8;
-}
+int gemm_epi_warps(int bn, int n_tiles) { return (bn <= 96 || n_tiles == 1) ? 4 : 8; }
 
 void launch_gemm(const GemmMaps& maps, const GemmParams& p, int groups, cudaStream_t stream) {
   const bool f32 = p.out_f32 || p.splits > 1;

@@ -19,6 +19,7 @@
 
 #include "sp_kernels.cuh"
 #include "sp_ptx.cuh"
+#include "sp_device.cuh"
 
 namespace sp {
 
@@ -79,7 +80,8 @@ __global__ void __launch_bounds__(kMThreads, 1)
     mlp_persistent_kernel(const __grid_constant__ MlpMaps m, const MlpParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const int stage_bytes = kMATileBytes + std::max(p.bn_a, p.bn_b) * 128;
+  // weight tile + the (hi, lo) token terms of the wider phase's tile
+  const int stage_bytes = kMATileBytes + 2 * std::max(p.bn_a, p.bn_b) * 128;
   uint8_t* staging = smem + p.stages * stage_bytes;  // 16 warps x 16 rows x 128 B
   uint64_t* full = reinterpret_cast<uint64_t*>(staging + kMEpiWarps * 16 * kMStageRowBytes);
   uint64_t* empty = full + p.stages;
@@ -148,9 +150,9 @@ __global__ void __launch_bounds__(kMThreads, 1)
       pdl_wait();  // phase A reads the LayerNorm output of the previous kernel
       for (int phase = 0; phase < 2; ++phase) {
         const MlpPhase f = mlp_phase(p, phase);
-        const CUtensorMap* m64 = phase == 0 ? &m.xa64 : &m.xb64;
-        const CUtensorMap* m16 = phase == 0 ? &m.xa16 : &m.xb16;
-        const uint32_t x_bytes = (uint32_t)f.bn * 128u;
+        const CUtensorMap* m64[2] = {phase == 0 ? &m.xa64 : &m.xb64, phase == 0 ? &m.xal64 : &m.xbl64};
+        const CUtensorMap* m16[2] = {phase == 0 ? &m.xa16 : &m.xb16, phase == 0 ? &m.xal16 : &m.xbl16};
+        const uint32_t x_bytes = (uint32_t)f.bn * 128u;  // per term
         const int a_tiles_per_student = (p.n_a / kMBlockM) * p.n_tiles_a;
         int dep_g = -1;
         for (int k = 0;; ++k) {
@@ -171,11 +173,14 @@ __global__ void __launch_bounds__(kMThreads, 1)
           const int kb0 = sp * f.nkb;
           for (int kb = kb0; kb < kb0 + f.nkb; ++kb) {
             mbar_wait(&empty[s], ph ^ 1);
-            mbar_arrive_expect_tx(&full[s], x_bytes);
+            mbar_arrive_expect_tx(&full[s], 2 * x_bytes);
             uint8_t* sb = smem + s * stage_bytes + kMATileBytes;
-            int r = 0;
-            for (; r + 64 <= f.bn; r += 64) tma_load_2d(m64, &full[s], sb + r * 128, kb * kMBlockK, xrow + r, pol);
-            for (; r < f.bn; r += 16) tma_load_2d(m16, &full[s], sb + r * 128, kb * kMBlockK, xrow + r, pol);
+            for (int term = 0; term < 2; ++term, sb += x_bytes) {
+              int r = 0;
+              for (; r + 64 <= f.bn; r += 64)
+                tma_load_2d(m64[term], &full[s], sb + r * 128, kb * kMBlockK, xrow + r, pol);
+              for (; r < f.bn; r += 16) tma_load_2d(m16[term], &full[s], sb + r * 128, kb * kMBlockK, xrow + r, pol);
+            }
             if (++s == p.stages) {
               s = 0;
               ph ^= 1;
@@ -205,9 +210,12 @@ __global__ void __launch_bounds__(kMThreads, 1)
             const uint32_t sa = smem_u32(smem + s * stage_bytes);
             const uint64_t adesc = umma_sdesc_sw128(sa);
             const uint64_t bdesc = umma_sdesc_sw128(sa + kMATileBytes);
+            const uint64_t ldesc = umma_sdesc_sw128(sa + kMATileBytes + f.bn * 128);  // lo term
 #pragma unroll
-            for (int kk = 0; kk < kMBlockK / 16; ++kk)
+            for (int kk = 0; kk < kMBlockK / 16; ++kk) {
               umma_f16_ss(acc, adesc + 2 * kk, bdesc + 2 * kk, idesc, (kb > 0 || kk > 0) ? 1u : 0u);
+              umma_f16_ss(acc, adesc + 2 * kk, ldesc + 2 * kk, idesc, 1u);
+            }
             umma_commit(&empty[s]);
             if (++s == p.stages) {
               s = 0;
@@ -253,20 +261,29 @@ __global__ void __launch_bounds__(kMThreads, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(&acc_empty[b]);
           }
-          if (phase == 0) {  // bias + erf-GELU -> fp16 ffn activations
+          if (phase == 0) {  // bias + erf-GELU -> fp16 (hi, lo) ffn activations
             constexpr int kRow = 64, kLanes = kRow / 16, kRowsPass = 32 / kLanes;
             half* st = reinterpret_cast<half*>(stage_base);
+            float y[16];
 #pragma unroll
-            for (int jj = 0; jj < 16; ++jj) st[jj * 32 + lane] = __float2half_rn(gelu_erf(__uint_as_float(r[jj]) + bias));
-            __syncwarp();
-            half* out = p.out_a + (long long)g * p.out_a_gs + m0 + q * 32;
-            const int sub = lane % kLanes;
-            for (int j0 = 0; j0 < n; j0 += kRowsPass) {
-              const int jr = j0 + lane / kLanes;
-              const int t = n0 + c + jr;
-              if (jr < n && t < t_rows) {
-                const uint4 v = *reinterpret_cast<const uint4*>(stage_base + jr * kRow + sub * 16);
-                *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(out + (long long)t * p.out_a_ld) + sub * 16) = v;
+            for (int jj = 0; jj < 16; ++jj) y[jj] = gelu_erf(__uint_as_float(r[jj]) + bias);
+            for (int term = 0; term < 2; ++term) {
+              if (term) __syncwarp();
+#pragma unroll
+              for (int jj = 0; jj < 16; ++jj) {
+                const half h = __float2half_rn(y[jj]);
+                st[jj * 32 + lane] = term ? __float2half_rn(y[jj] - __half2float(h)) : h;
+              }
+              __syncwarp();
+              half* out = p.out_a + (term ? p.out_a_lo_off : 0) + (long long)g * p.out_a_gs + m0 + q * 32;
+              const int sub = lane % kLanes;
+              for (int j0 = 0; j0 < n; j0 += kRowsPass) {
+                const int jr = j0 + lane / kLanes;
+                const int t = n0 + c + jr;
+                if (jr < n && t < t_rows) {
+                  const uint4 v = *reinterpret_cast<const uint4*>(stage_base + jr * kRow + sub * 16);
+                  *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(out + (long long)t * p.out_a_ld) + sub * 16) = v;
+                }
               }
             }
           } else {  // raw fp32 projection (bias + residual + LayerNorm in the next kernel), 8 columns at a time
@@ -311,10 +328,10 @@ __global__ void __launch_bounds__(kMThreads, 1)
   }
   if (threadIdx.x == 0) {  // the last CTA out resets the counters for the next launch
     __threadfence();
-    const int old = atomicAdd(p.done + kReqMaxStudents, 1);
+    const int old = atomicAdd(p.done + kMlpMaxStudents, 1);
     if (old == (int)gridDim.x - 1) {
       for (int i = 0; i < p.groups; ++i) p.done[i] = 0;
-      p.done[kReqMaxStudents] = 0;
+      p.done[kMlpMaxStudents] = 0;
       __threadfence();
     }
   }
@@ -324,7 +341,7 @@ __global__ void __launch_bounds__(kMThreads, 1)
 
 int mlp_smem_bytes(int bn_max, int* stages) {
   const int staging = kMEpiWarps * 16 * kMStageRowBytes;
-  const int stage = kMATileBytes + bn_max * 128;
+  const int stage = kMATileBytes + 2 * bn_max * 128;
   int st = (224 * 1024 - staging - 2048) / stage;
   if (st > 8) st = 8;
   if (stages) *stages = st;

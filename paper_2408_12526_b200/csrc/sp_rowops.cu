@@ -16,11 +16,10 @@ __global__ void __launch_bounds__(128)
                     const half* __restrict__ word, const half* __restrict__ pos, const half* __restrict__ type,
                     long long word_gs, long long pos_gs, const float* __restrict__ gamma,
                     const float* __restrict__ beta, int hidden, float eps, float* x32, half* x16, long long x_gs,
-                    const void* pf_ptr, unsigned long long pf_bytes) {
-  prefetch_share_l2(pf_ptr, pf_bytes);
-  // Everything read here is a request input (ids, cu_seqlens: copied before the first kernel) or a
-  // weight, so the gathers are issued before the dependency wait; only the stores follow it (the
-  // previous request's kernels may still read x32 / x16).
+                    long long x_lo_off) {
+  // The first kernel of a request is launched WITHOUT programmatic serialization (launch_embed_ln),
+  // so whatever the caller ran before it on the stream — a copy or its own kernel producing ids /
+  // cu_seqlens — has completed; only the next projection is released early.
   pdl_launch_dependents();
   const int t = blockIdx.x * 4 + warp_id();
   if (n_tokens < 0) n_tokens = __ldg(cu + n_seqs);  // graph replay: live count = cu_seqlens[n_seqs]
@@ -51,10 +50,9 @@ __global__ void __launch_bounds__(128)
 #pragma unroll
     for (int j = 0; j < 4; ++j) v[c][j] = a[j] + bb[j] + cc[j];
   }
-  pdl_wait();
   const long long row = (long long)g * x_gs + (long long)t * hidden;
   layer_norm_store<NC>(v, gamma + (long long)g * hidden, beta + (long long)g * hidden, eps, hidden, x32 + row,
-                       x16 + row, nullptr);
+                       x16 + row, x_lo_off, nullptr, 0);
 }
 
 // SPLITS: number of split-K partials, a template parameter so only the live ones hold registers
@@ -64,9 +62,8 @@ __global__ void __launch_bounds__(128)
     reduce_ln_kernel(const float* __restrict__ part, int splits, long long part_split_stride,
                      const float* __restrict__ bias, const float* __restrict__ gamma, const float* __restrict__ beta,
                      int hidden, float eps, float* x32, half* x16, long long x_gs, int n_tokens,
-                     const int* __restrict__ cu, int n_seqs, half* cls16, long long cls_gs, const void* pf_ptr,
-                     unsigned long long pf_bytes) {
-  prefetch_share_l2(pf_ptr, pf_bytes);
+                     const int* __restrict__ cu, int n_seqs, half* cls16, long long cls_gs, long long x_lo_off,
+                     long long cls_lo_off) {
   // request inputs (cu_seqlens) and weights (bias) are read before the dependency wait
   pdl_launch_dependents();
   const int t = blockIdx.x * 4 + warp_id();
@@ -109,7 +106,7 @@ __global__ void __launch_bounds__(128)
     }
   }
   layer_norm_store<NC>(v, gamma + (long long)g * hidden, beta + (long long)g * hidden, eps, hidden, x32 + row,
-                       x16 + row, cls_row);
+                       x16 + row, x_lo_off, cls_row, cls_lo_off);
 }
 
 // One CTA per output row b, one thread per feature j (blockDim = hidden <= 1024).
@@ -208,22 +205,22 @@ template <int NC>
 static void embed_ln_t(dim3 grid, cudaStream_t st, const int* ids, const int* cu, int n_seqs, int n_tokens,
                        const half* word, const half* pos, const half* type, long long word_gs, long long pos_gs,
                        const float* gamma, const float* beta, int hidden, float eps, float* x32, half* x16,
-                       long long x_gs, const void* pf_ptr, unsigned long long pf_bytes) {
-  launch_pdl(embed_ln_kernel<NC>, grid, dim3(128), 0, st, ids, cu, n_seqs, n_tokens, word, pos, type, word_gs,
-             pos_gs, gamma, beta, hidden, eps, x32, x16, x_gs, pf_ptr, pf_bytes);
+                       long long x_gs, long long x_lo_off) {
+  launch_plain(embed_ln_kernel<NC>, grid, dim3(128), 0, st, ids, cu, n_seqs, n_tokens, word, pos, type, word_gs,
+               pos_gs, gamma, beta, hidden, eps, x32, x16, x_gs, x_lo_off);
 }
 
 void launch_embed_ln(const int* ids, const int* cu_seqlens, int n_seqs, int n_tokens, int groups, const half* word,
                      const half* pos, const half* type, long long word_gs, long long pos_gs, const float* gamma,
                      const float* beta, int hidden, float eps, float* x32, half* x16, long long x_gs,
-                     cudaStream_t stream, const void* pf_ptr, unsigned long long pf_bytes) {
+                     long long x_lo_off, cudaStream_t stream) {
   if (n_tokens == 0 || groups <= 0) return;
   // n_tokens < 0: grid sized for -n_tokens rows, live count read from cu_seqlens (graph replay)
   dim3 grid(((n_tokens < 0 ? -n_tokens : n_tokens) + 3) / 4, groups);
   if (n_tokens < 0) n_tokens = -1;
 #define SP_EMBED(NC_)                                                                                      \
   embed_ln_t<NC_>(grid, stream, ids, cu_seqlens, n_seqs, n_tokens, word, pos, type, word_gs, pos_gs, gamma, \
-                  beta, hidden, eps, x32, x16, x_gs, pf_ptr, pf_bytes)
+                  beta, hidden, eps, x32, x16, x_gs, x_lo_off)
   switch (hidden / 128) {
     case 1: SP_EMBED(1); break;
     case 2: SP_EMBED(2); break;
@@ -237,14 +234,14 @@ void launch_embed_ln(const int* ids, const int* cu_seqlens, int n_seqs, int n_to
 
 void launch_reduce_ln(const float* part, int splits, long long part_split_stride, const float* bias,
                       const float* gamma, const float* beta, int hidden, float eps, float* x32, half* x16,
-                      long long x_gs, int n_tokens, int groups, const int* cu_seqlens, int n_seqs, half* cls16,
-                      long long cls_gs, cudaStream_t stream, const void* pf_ptr, unsigned long long pf_bytes) {
+                      long long x_gs, long long x_lo_off, int n_tokens, int groups, const int* cu_seqlens, int n_seqs,
+                      half* cls16, long long cls_gs, long long cls_lo_off, cudaStream_t stream) {
   if (n_tokens == 0 || groups <= 0) return;
   dim3 grid(((n_tokens < 0 ? -n_tokens : n_tokens) + 3) / 4, groups);
   if (n_tokens < 0) n_tokens = -1;
 #define SP_REDUCE_S(NC_, S_)                                                                                     \
   launch_pdl(reduce_ln_kernel<NC_, S_>, grid, dim3(128), 0, stream, part, splits, part_split_stride, bias, gamma, \
-             beta, hidden, eps, x32, x16, x_gs, n_tokens, cu_seqlens, n_seqs, cls16, cls_gs, pf_ptr, pf_bytes)
+             beta, hidden, eps, x32, x16, x_gs, n_tokens, cu_seqlens, n_seqs, cls16, cls_gs, x_lo_off, cls_lo_off)
 #define SP_REDUCE(NC_)                     \
   do {                                     \
     if (splits <= 1) SP_REDUCE_S(NC_, 1);  \

@@ -233,9 +233,11 @@ class StudentGroup:
 
     def forward_dense_device(self, x16: torch.Tensor, n_rows: int, k_local: int, rep: torch.Tensor | None,
                              logits: torch.Tensor, add_bias: bool = True,
-                             stream: torch.cuda.Stream | None = None) -> None:
-        _lib.check(self._lib.sp_group_forward_dense(self._handle, x16.data_ptr(), n_rows, k_local, _ptr(rep),
-                                                    logits.data_ptr(), int(add_bias),
+                             stream: torch.cuda.Stream | None = None, x16_lo: torch.Tensor | None = None) -> None:
+        """Dense kind on device buffers: x16 fp16 [n_rows, d_in] (+ optional x16_lo, the fp16 residual of
+        a wider input, read as a second operand term)."""
+        _lib.check(self._lib.sp_group_forward_dense(self._handle, x16.data_ptr(), _ptr(x16_lo), n_rows, k_local,
+                                                    _ptr(rep), logits.data_ptr(), int(add_bias),
                                                     _stream_handle(stream, self.device)))
 
     # ------------------------------------------------------------------ reference-facing API
@@ -252,20 +254,22 @@ class StudentGroup:
             n = xa.shape[0]
             if n > self.max_tokens:
                 raise ValueError(f"{n} rows exceed the group's capacity {self.max_tokens}")
-            xp = np.zeros((n, w.d_in_padded), np.float16)
-            xp[:, : w.d_in] = xa
+            # the float64 input as an fp16 (hi, lo) pair: both operand terms of input_proj
+            xp = np.zeros((2, n, w.d_in_padded), np.float16)
+            xp[0, :, : w.d_in] = xa
+            xp[1, :, : w.d_in] = xa - xp[0, :, : w.d_in].astype(np.float64)
             kl = self.local_k(k) if k_local is None else k_local
             with torch.cuda.device(dev):
                 x16 = _dev_tensor(xp, dev)
                 rep = torch.empty((n, self.hidden), dtype=torch.float32, device=dev) if want_rep else None
                 if evaluate:
                     finals, prefix = self._eval_buffers(kl, n)
-                    _lib.check(self._lib.sp_group_forward_dense_eval(self._handle, x16.data_ptr(), n, kl,
-                                                                     finals.data_ptr(), prefix.data_ptr(),
-                                                                     _stream_handle(None, dev)))
+                    _lib.check(self._lib.sp_group_forward_dense_eval(self._handle, x16[0].data_ptr(),
+                                                                     x16[1].data_ptr(), n, kl, finals.data_ptr(),
+                                                                     prefix.data_ptr(), _stream_handle(None, dev)))
                     return finals[:, :, : w.rep_dim], prefix, squeeze, w.rep_dim
                 logits = torch.empty((n, self.n_classes), dtype=torch.float32, device=dev)
-                self.forward_dense_device(x16, n, kl, rep, logits, add_bias)
+                self.forward_dense_device(x16[0], n, kl, rep, logits, add_bias, x16_lo=x16[1])
             width = w.rep_dim
         else:
             ids, cu, squeeze = pack_sequences(x)

@@ -51,15 +51,15 @@ def cuda_lib():
 
 
 def rel_err_rows(got, ref):
-    """max |got - ref| / scale, scale = max |ref| over the batch (the logit scale).
+    """max over rows of max_c |got - ref| / max_c |ref| (per-row logit scale).
 
-    This is the parity metric for "logits within 1e-3 relative" (BASELINE.json). A per-row
-    denominator is ill-posed for rows whose logits all sit near zero (the classifier is indifferent
-    there and only absolute error is meaningful); at batch-1 the two definitions coincide.
+    This is the parity metric for "logits within 1e-3 relative" (BASELINE.json): every request's
+    logits are measured against that request's own largest logit, so a batched test is held to the
+    same bar as a batch-1 one.
     """
     import numpy as np
 
-    got = np.atleast_2d(got)
-    ref = np.atleast_2d(ref)
-    scale = max(float(np.abs(ref).max()), 1e-30)
-    return float(np.abs(got - ref).max() / scale)
+    got = np.atleast_2d(np.asarray(got, np.float64))
+    ref = np.atleast_2d(np.asarray(ref, np.float64))
+    scale = np.maximum(np.abs(ref).max(axis=1), 1e-30)
+    return float((np.abs(got - ref).max(axis=1) / scale).max())

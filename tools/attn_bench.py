@@ -11,9 +11,10 @@ G, NH, D = 8, 12, 64
 H = NH * D
 for L in [int(x) for x in sys.argv[1].split(",")]:
     qkv = (torch.randn(G, L, 3 * H, device="cuda") * 0.5).half()
-    ctx = torch.empty(G, L, H, device="cuda").half()
+    ctx = torch.empty(2, G, L, H, device="cuda").half()  # (hi, lo) context planes
     cu = torch.tensor([0, L], dtype=torch.int32, device="cuda")
-    run = lambda: _lib.check(lib.sp_op_attention(qkv.data_ptr(), ctx.data_ptr(), cu.data_ptr(), 1, L, G, NH, D, L, None))
+    run = lambda: _lib.check(lib.sp_op_attention(qkv.data_ptr(), ctx[0].data_ptr(), ctx[1].data_ptr(), cu.data_ptr(), 1, L, G, NH, D, L,
+                                                         None))
     for _ in range(3): run()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
