@@ -15,7 +15,7 @@ replays each batch-1 request's bucket CUDA graph instead of launching its kernel
 p50_ms/p99_ms = nearest-rank percentiles (servesim.py:370-376) of the per-request latency.
 e2e = the same metric through the public API with host buffers (pinned ids in, logits out).
 --impl reference times the float64 CPU port of the path (oracle/, the reference is pure Python and
-has no BERT student) on the host cores, rank 0 only.
+has no BERT student) on the host cores, one whole request per step, rank 0 only.
 """
 from __future__ import annotations
 
@@ -154,33 +154,74 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- CPU port
-def cpu_port_sample(weights, reqs, seconds, max_samples=None):
-    """Time the float64 oracle port (oracle/bert.py) one (request, student) pair at a time.
-
-    Students are independent and identical in cost, so K x (mean per-student time) + the head is
-    the per-request cost; returns (req/s, samples, seconds)."""
+def cpu_port_requests(weights, reqs, n=None, seconds=None):
+    """Time the float64 oracle port (oracle/bert.py) on whole requests: every student of the group,
+    the boosting sum and the classifier, one request at a time. Stops after n requests, or once
+    `seconds` of CPU time are spent (at least one request). Returns per-request seconds."""
     from oracle.bert import OracleBertGroup  # the CPU baseline is the checker, timed, never shipped
 
     orc = OracleBertGroup(weights)
-    K = orc.n_students
-    for m in range(K):  # f64 weight copies are resident before timing (like the reference's arrays)
+    for m in range(orc.n_students):  # f64 weight copies resident before timing (like the reference's arrays)
         orc.student(m)
     times = []
     t_start = time.perf_counter()
     i = 0
     while True:
         ids = reqs[i % len(reqs)]
-        m = i % K
         t0 = time.perf_counter()
-        orc.pooled(m, [ids])
+        orc.forward([ids])
         times.append(time.perf_counter() - t0)
         i += 1
-        if max_samples is not None and i >= max_samples:
+        if n is not None and i >= n:
             break
-        if max_samples is None and time.perf_counter() - t_start >= seconds:
+        if n is None and time.perf_counter() - t_start >= seconds:
             break
-    per_req = K * float(np.mean(times))
-    return 1.0 / per_req, len(times), float(np.sum(times))
+    return np.array(times)
+
+
+_DENSE_REF_TIMING = r"""
+import json, sys, time
+import numpy as np
+sys.path.insert(0, sys.argv[1])
+from oracle.dense import ensemble_rep, dense_layer, student_forward, IDENTITY
+K, H, rows, budget = int(sys.argv[2]), int(sys.argv[3]), int(sys.argv[4]), float(sys.argv[5])
+rng = np.random.default_rng(0)
+g = lambda o, i: (rng.uniform(-1, 1, size=(o, i)) * np.sqrt(6.0 / (o + i)), np.zeros(o))
+students = [[g(H, H), g(H, H), g(H, H)] for _ in range(K)]
+alphas = [1.0] + list(rng.uniform(0.2, 1.0, size=K - 1))
+wc, bc = g(2, H)
+x = rng.normal(size=(rows, H))
+def req():
+    finals = [student_forward(s, x)[0] for s in students]
+    return dense_layer(wc, bc, ensemble_rep(finals, alphas), IDENTITY)
+req()
+ts = []
+t_end = time.perf_counter() + budget
+while len(ts) < 3 or (time.perf_counter() < t_end and len(ts) < 200):
+    t0 = time.perf_counter(); req(); ts.append(time.perf_counter() - t0)
+ts.sort()
+print(json.dumps({"p50_ms": 1e3 * ts[len(ts) // 2], "p99_ms": 1e3 * ts[min(len(ts) - 1, int(0.99 * len(ts)))], "n": len(ts)}))
+"""
+
+
+def cpu_dense_reference_timing(threads_list, budget_s=2.0):
+    """the reference's own CPU path for the group head — EnsembleState.rep over dense
+    StudentModel students + classifier (distill.py:169-178, :512; restated bit-for-bit in
+    oracle/dense.py, pinned to the reference's goldens) — at K=8, H=768 per request of 1 and 128 rows,
+    with OPENBLAS_NUM_THREADS set to the host core count and to 1 (fresh process each: the thread
+    count is fixed when numpy loads)."""
+    out = []
+    for threads in threads_list:
+        for rows in (1, 128):
+            env = {**os.environ, "OPENBLAS_NUM_THREADS": str(threads), "OMP_NUM_THREADS": str(threads)}
+            try:
+                r = subprocess.run([sys.executable, "-c", _DENSE_REF_TIMING, str(ROOT), "8", "768", str(rows),
+                                    str(budget_s)], env=env, capture_output=True, text=True, timeout=120)
+                d = json.loads(r.stdout.strip().splitlines()[-1])
+            except Exception as e:  # reported, never fatal for the GPU line
+                d = {"error": str(e)[:200]}
+            out.append({"threads": threads, "K": 8, "hidden": 768, "rows": rows, **d})
+    return out
 
 
 def host_cores():
@@ -189,6 +230,10 @@ def host_cores():
 
 # ----------------------------------------------------------------------------- reference arm
 def run_reference(args):
+    """The reference's CPU implementation of the path on the host cores: one step = one whole
+    request of the workload (all K students + boosting sum + classifier) through the float64 port
+    oracle/bert.py (the reference is pure Python and has no BERT student; its dense group head is
+    the same numpy code). Rank 0 only."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
@@ -196,19 +241,21 @@ def run_reference(args):
 
     cfg, K = PRESETS[args.config]
     weights = random_bert_group(cfg, K, seed=args.seed)
-    reqs = make_requests(max(64, args.steps + args.warmup), args.seed, args.len_min, args.len_max, cfg.vocab)
-    cpu_port_sample(weights, reqs, 0.0, max_samples=max(1, args.warmup))
+    reqs = make_requests(args.steps + args.warmup, args.seed, args.len_min, args.len_max, cfg.vocab)
+    cpu_port_requests(weights, reqs[: args.warmup], n=max(1, args.warmup))
     t0 = time.perf_counter()
-    value, n, busy = cpu_port_sample(weights, reqs[args.warmup:] + reqs[: args.warmup], 0.0, max_samples=args.steps)
+    times = cpu_port_requests(weights, reqs[args.warmup:], n=args.steps)
     wall = time.perf_counter() - t0
+    value = len(times) / float(times.sum())
     cores = host_cores()
-    sample = (f"{n} (request, student) forwards of the {args.config} group (L~U{{{args.len_min}..{args.len_max}}}), "
-              f"float64 numpy/OpenBLAS port (oracle/bert.py); req/s = 1 / (K x mean student time)")
+    sample = (f"{len(times)} whole requests of the {args.config} group (K={K}, L~U{{{args.len_min}..{args.len_max}}}), "
+              f"float64 numpy/OpenBLAS port (oracle/bert.py), {cores} host threads")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * busy / max(n, 1),
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * float(times.mean()),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": workload_config(args, cfg, K, args.gpus),
+        "p50_ms": 1e3 * nearest_rank(times, 50), "p99_ms": 1e3 * nearest_rank(times, 99),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "wall_s": wall,
@@ -359,7 +406,6 @@ def run_engine(args):
         flush()
         step(i)
     barrier()
-    launches_per_step = grp.local.last_launches
 
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -367,12 +413,14 @@ def run_engine(args):
     if clocks:
         clocks.start()
     barrier()
+    launch_counts = []
     for j in range(args.steps):
         i = args.warmup + j
         flush()
         starts[j].record()
         step(i)
         ends[j].record()
+        launch_counts.append(grp.local.last_launches)
     barrier()
     clock_info = clocks.stop() if clocks else None
     step_ms = torch.tensor([s.elapsed_time(e) for s, e in zip(starts, ends)], dtype=torch.float64, device=dev)
@@ -402,58 +450,75 @@ def run_engine(args):
             per_launch.append((r["kind"], r["ms"], r["bytes"], r["flops"]))
         step_total_ms += sum(r["ms"] for r in recs)
     grp.local.set_profiling(False)
-    peaks = {}
     try:
         peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
-        hbm_peak, peak_src = float(peaks["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (measured)"
+        hbm_peak, peak_src = float(peaks["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs / bf16_tflops (measured, burst)"
         tc_peak = float(peaks["bf16_tflops"])
     except Exception:
-        hbm_peak, peak_src, tc_peak = 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)", 1590.0
+        hbm_peak, peak_src, tc_peak = 6650.0, "fallback 6.65 TB/s / 1.59 PFLOP/s (B200_PROFILING.md)", 1590.0
     gemm_names = [LAUNCH_KINDS[k] for k in sorted(GEMM_KINDS)]
     g_ms = sum(agg[k][0] for k in gemm_names if k in agg)
     g_bytes = sum(agg[k][1] for k in gemm_names if k in agg)
     g_flops = sum(agg[k][2] for k in gemm_names if k in agg)
     g_launches = sum(agg[k][3] for k in gemm_names if k in agg)
     achieved = g_bytes / (g_ms / 1e3) / 1e9 if g_ms > 0 else 0.0
-    traffic = None
-    tfile = ROOT / "profiles" / "gemm_dram_traffic.json"
-    if tfile.exists():
-        try:
-            traffic = json.loads(tfile.read_text()).get("dram_bytes_per_launch")
-        except Exception:
-            traffic = None
     tflops = g_flops / (g_ms / 1e3) / 1e12 if g_ms > 0 else 0.0
     if B == 1:  # batch-1: weight streaming, HBM-bound
         bound, ach, peak, unit = "hbm", achieved, hbm_peak, "GB/s"
     else:  # batched: dense contraction, tensor-bound
         bound, ach, peak, unit = "tensor", tflops, tc_peak, "TFLOP/s"
     roofline = {
-        "bound": bound, "kernel": "gemm_kernel / gemm_persistent_kernel (tcgen05 grouped projections)",
+        "bound": bound, "kernel": "gemm_kernel / gemm_persistent_kernel / mlp_persistent_kernel (tcgen05 grouped "
+                                  "projections)",
         "achieved": ach, "peak": peak, "unit": unit, "frac": ach / peak,
-        "hbm_achieved_gbs": achieved, "hbm_peak_gbs": hbm_peak,
-        "traffic": traffic, "peak_source": peak_src,
+        # dram__bytes per launch is not measured inside this run (ncu replays kernels); the ncu
+        # captures of these launches are committed under profiles/ (r2_ncu_*)
+        "traffic": None,
+        "peak_source": peak_src,
+        "algorithmic_bytes": "SURVEY 8(d): weight + bias bytes of each projection launch (activations are "
+                             "L2-resident and not compulsory HBM traffic)",
         "algorithmic_bytes_per_launch": g_bytes / max(g_launches, 1),
         "avg_launch_us": 1e3 * g_ms / max(g_launches, 1),
-        "tensor_tflops": tflops, "tensor_peak_tflops": tc_peak,
+        "hbm_achieved_gbs": achieved, "hbm_peak_gbs": hbm_peak,
+        "tensor_tflops_algorithmic": tflops, "tensor_tflops_executed": 2.0 * tflops,
+        "tensor_peak_tflops": tc_peak,
+        "executed_note": "every activation is an fp16 (hi, lo) pair: the tensor pipe runs 2 MMAs per k-slice, "
+                         "2x the algorithmic flops",
         "gemm_share_of_step": g_ms / step_total_ms if step_total_ms else None,
-        "method": f"CUDA events around every launch on the launching stream, instrumented replay of {n_prof} timed requests",
+        "method": f"CUDA events around every launch on the launching stream, instrumented replay of {n_prof} "
+                  "timed requests",
         "per_kind_ms_per_request": {k: v[0] / n_prof for k, v in sorted(agg.items())},
     }
-    # Mixed-intensity workloads (batch-1 L from 16 to 512 crosses the ridge at ~254 FLOP/B): the
-    # attainable time of each GEMM launch is max(bytes / HBM peak, flops / tensor peak); report the
-    # sum of attainable times over the sum of measured times (1.0 = every launch on its roofline).
-    att = [max(b / (hbm_peak * 1e9), f / (tc_peak * 1e12)) for k, ms, b, f in per_launch if k in gemm_names]
-    meas = [ms / 1e3 for k, ms, b, f in per_launch if k in gemm_names]
-    roofline["gemm_attainable_frac"] = (sum(att) / sum(meas)) if meas else None
-    n_hbm = sum(1 for k, ms, b, f in per_launch if k in gemm_names and b / hbm_peak / 1e9 >= f / tc_peak / 1e12)
-    roofline["gemm_launches_hbm_bound"] = n_hbm
-    roofline["gemm_launches_tensor_bound"] = len(meas) - n_hbm
-    # request-level roofline: all weight bytes of a request vs its latency
-    w_bytes = grp.local.weights  # local weights (host copy)
-    req_bytes_local = sum(getattr(w_bytes, n).nbytes for n in
-                          ["w_qkv", "w_o", "w_ffn1", "w_ffn2", "w_pool", "b_qkv", "b_o", "b_ffn1", "b_ffn2", "b_pool"])
-    roofline["request_weight_bytes_per_gpu"] = req_bytes_local
-    roofline["request_hbm_frac_p50"] = (req_bytes_local / (nearest_rank(step_ms, 50) / 1e3) / 1e9) / hbm_peak
+    # Request-level roofline (SURVEY 8(d) per request): compulsory bytes = this GPU's weights of the
+    # active students + gathered embedding rows; flops = the request's algorithmic flops; attainable
+    # time = max(bytes / HBM peak, flops / tensor peak); frac = attainable / measured device latency.
+    lw = grp.local.weights
+    H, F, NL, C = cfg.hidden, cfg.ffn, cfg.n_layers, cfg.n_classes
+    k_loc = len(lw.alpha)
+    w_bytes = sum(getattr(lw, n).nbytes for n in
+                  ["w_qkv", "b_qkv", "w_o", "b_o", "ln1_gamma", "ln1_beta", "w_ffn1", "b_ffn1", "w_ffn2", "b_ffn2",
+                   "ln2_gamma", "ln2_beta", "w_pool", "b_pool", "emb_ln_gamma", "emb_ln_beta", "type_emb"])
+    w_bytes += lw.w_cls.nbytes + lw.b_cls.nbytes
+    fr, att_s, meas_s = [], 0.0, 0.0
+    for j in range(args.steps):
+        i = args.warmup + j
+        lens = np.diff(step_cu[i]).astype(np.float64)
+        T = lens.sum()
+        byt = w_bytes + k_loc * T * H * 2 * 2  # + word and position rows gathered per student
+        flo = k_loc * (NL * (2 * T * (4 * H * H + 2 * H * F) + 4 * H * float((lens ** 2).sum())) + 2 * H * H * B) \
+            + 2 * C * H * B
+        t_att = max(byt / (hbm_peak * 1e9), flo / (tc_peak * 1e12))
+        fr.append(t_att / (step_ms[j] / 1e3))
+        att_s += t_att
+        meas_s += step_ms[j] / 1e3
+    roofline["request"] = {
+        "attainable_frac_p50": float(np.median(fr)), "attainable_frac_mean": float(np.mean(fr)),
+        "attainable_frac_aggregate": att_s / meas_s,
+        "weight_bytes_per_gpu": w_bytes,
+        "hbm_frac_p50": (w_bytes / (nearest_rank(step_ms, 50) / 1e3) / 1e9) / hbm_peak,
+        "definition": "per timed request: max(compulsory bytes / HBM peak, algorithmic flops / bf16 peak) / "
+                      "device latency (L2 flushed before every request)",
+    }
     if B == 1:
         roofline["in_request"] = in_request_gemm_roofline(grp.local, args, step_eager, step_tok, flush, hbm_peak)
 
@@ -490,22 +555,24 @@ def run_engine(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, n, busy = cpu_port_sample(grp.local.weights, reqs, args.cpu_seconds)
-        cpu = {"value": v, "unit": UNIT, "cores": host_cores(), "kind": "port",
-               "sample": f"{n} (request, student) float64 forwards of this workload in {busy:.1f} s "
-                         f"(oracle/bert.py, numpy/OpenBLAS, all {host_cores()} host threads); "
-                         f"req/s = 1/(K x mean student time)"}
+        times = cpu_port_requests(grp.local.weights, reqs[args.warmup:], seconds=args.cpu_seconds)
+        cpu = {"value": len(times) / float(times.sum()), "unit": UNIT, "cores": host_cores(), "kind": "port",
+               "sample": f"{len(times)} whole requests of this workload in {times.sum():.1f} s (oracle/bert.py float64 "
+                         f"port, numpy/OpenBLAS, all {host_cores()} host threads)",
+               "p50_ms": 1e3 * float(np.median(times)),
+               "dense_reference_path": cpu_dense_reference_timing(sorted({host_cores(), 1}))}
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * total_s / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "fp16", "data": "synthetic",
+            "precision": "fp16 weights, fp16 (hi, lo) activation pairs, fp32 accumulation and residual stream",
             "config": workload_config(args, cfg, K, world),
             "p50_ms": nearest_rank(step_ms, 50), "p99_ms": nearest_rank(step_ms, 99),
             "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clock_info,
-            "gpu_launches": launches_per_step * args.steps,
-            "launches_per_request": launches_per_step,
+            "gpu_launches": int(sum(launch_counts)),
+            "launches_per_request": float(np.mean(launch_counts)),
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -183,8 +183,10 @@ enum sp_launch_kind {
 typedef struct sp_launch_record {
   int32_t kind;   /* enum sp_launch_kind */
   float ms;       /* device duration (CUDA events) */
-  double bytes;   /* algorithmic HBM bytes: compulsory reads + writes of the launch */
-  double flops;   /* algorithmic flops */
+  double bytes;   /* algorithmic HBM bytes: projections = weights + bias; row kernels and
+                     attention = their activation reads + writes */
+  double flops;   /* algorithmic flops (projections 2 N K T; the tensor pipe runs twice that: one MMA per
+                     operand term) */
 } sp_launch_record;
 
 int sp_group_set_profiling(sp_group* group, int enable);

@@ -1,0 +1,157 @@
+// sp_attn_cls.cu — attention of the CLS query only, for the last encoder layer.
+//
+// Only the CLS row of the last layer reaches the pooler (tanh(W_p h_CLS + b_p)), so
+// the last layer needs K and V of every token but the query, the context, the O projection, the
+// LayerNorms and the FFN of the CLS row alone; the engine computes exactly that (the result is the
+// same function: the other rows are dead). Per (student, sequence, head) one CTA of 4 warps:
+//   1. scores s_j = q . k_j / sqrt(d) in fp32, one thread per key (16-byte loads of the key row),
+//      kept in shared memory;
+//   2. softmax in fp32 (block max / sum);
+//   3. context c = sum_j p_j v_j: each warp a quarter of the keys, each lane 2 (d = 64) or 1 (d = 32)
+//      of the dims (one coalesced 128 / 64-byte row per key), four independent keys in flight; the
+//      warps' partial sums combined through shared memory, written as an (hi, lo) fp16 pair.
+// Unlike the tensor-core kernels, P stays fp32 (no fp16 rounding of the probabilities).
+#include "sp_kernels.cuh"
+#include "sp_ptx.cuh"
+#include "sp_device.cuh"
+
+namespace sp {
+
+namespace {
+constexpr int kClsThreads = 128;
+}
+
+template <int D>
+__global__ void __launch_bounds__(kClsThreads)
+    attn_cls_kernel(const half* __restrict__ qkv, long long qkv_gs, const half* __restrict__ qs, long long q_gs,
+                    const int* __restrict__ cu, int n_heads, int hidden, half* __restrict__ ctx, long long ctx_gs,
+                    long long lo_off, float scale) {
+  extern __shared__ float sc[];  // [L] scores -> probabilities
+  __shared__ float red[4][D];
+  __shared__ float stat[8];
+  pdl_launch_dependents();
+  const int gh = blockIdx.x;
+  const int g = gh / n_heads, h = gh % n_heads;
+  const int b = blockIdx.y;
+  const int c0 = __ldg(cu + b), c1 = __ldg(cu + b + 1);  // request input: before the dependency wait
+  const int L = c1 - c0;
+  const int tid = threadIdx.x, warp = warp_id(), lane = lane_id();
+  const long long row3 = 3LL * hidden;
+  const half* base = qkv + (long long)g * qkv_gs + (long long)c0 * row3 + h * D;
+  const half* qrow = qs ? qs + (long long)g * q_gs + (long long)b * hidden + h * D : base;
+  pdl_wait();
+  // q of the CLS row (fp32, every thread a full copy through registers)
+  float q[D];
+#pragma unroll
+  for (int v = 0; v < D / 8; ++v) {
+    const uint4 u = *reinterpret_cast<const uint4*>(qrow + v * 8);
+    const __half2* hp = reinterpret_cast<const __half2*>(&u);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float2 f = __half22float2(hp[i]);
+      q[v * 8 + 2 * i] = f.x * scale;
+      q[v * 8 + 2 * i + 1] = f.y * scale;
+    }
+  }
+  // 1. scores, one thread per key
+  float mx = -INFINITY;
+  for (int j = tid; j < L; j += kClsThreads) {
+    const half* kr = base + (long long)j * row3 + hidden;
+    float s = 0.f;
+#pragma unroll
+    for (int v = 0; v < D / 8; ++v) {
+      const uint4 u = *reinterpret_cast<const uint4*>(kr + v * 8);
+      const __half2* hp = reinterpret_cast<const __half2*>(&u);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float2 f = __half22float2(hp[i]);
+        s = fmaf(q[v * 8 + 2 * i], f.x, s);
+        s = fmaf(q[v * 8 + 2 * i + 1], f.y, s);
+      }
+    }
+    sc[j] = s;
+    mx = fmaxf(mx, s);
+  }
+  // 2. softmax statistics
+  mx = warp_max(mx);
+  if (lane == 0) stat[warp] = mx;
+  __syncthreads();
+  mx = fmaxf(fmaxf(stat[0], stat[1]), fmaxf(stat[2], stat[3]));
+  float sum = 0.f;
+  for (int j = tid; j < L; j += kClsThreads) {
+    const float p = __expf(sc[j] - mx);
+    sc[j] = p;
+    sum += p;
+  }
+  sum = warp_sum(sum);
+  __syncthreads();  // stat[] reads above are done; sc[] complete
+  if (lane == 0) stat[4 + warp] = sum;
+  __syncthreads();
+  const float inv = 1.f / ((stat[4] + stat[5]) + (stat[6] + stat[7]));
+  // 3. context: warp w takes keys w, w+4, ...; lane owns DPL consecutive dims
+  constexpr int DPL = D / 32;
+  float acc[4][DPL];
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int d = 0; d < DPL; ++d) acc[u][d] = 0.f;
+  const half* vb = base + 2 * hidden + lane * DPL;
+  int j = warp;
+  for (; j + 12 < L; j += 16) {  // four independent keys per iteration
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int jj = j + 4 * u;
+      const float p = sc[jj];
+      if constexpr (DPL == 2) {
+        const float2 f = __half22float2(*reinterpret_cast<const __half2*>(vb + (long long)jj * row3));
+        acc[u][0] = fmaf(p, f.x, acc[u][0]);
+        acc[u][1] = fmaf(p, f.y, acc[u][1]);
+      } else {
+        acc[u][0] = fmaf(p, __half2float(vb[(long long)jj * row3]), acc[u][0]);
+      }
+    }
+  }
+  for (; j < L; j += 4) {
+    const float p = sc[j];
+    if constexpr (DPL == 2) {
+      const float2 f = __half22float2(*reinterpret_cast<const __half2*>(vb + (long long)j * row3));
+      acc[0][0] = fmaf(p, f.x, acc[0][0]);
+      acc[0][1] = fmaf(p, f.y, acc[0][1]);
+    } else {
+      acc[0][0] = fmaf(p, __half2float(vb[(long long)j * row3]), acc[0][0]);
+    }
+  }
+#pragma unroll
+  for (int d = 0; d < DPL; ++d) red[warp][lane * DPL + d] = (acc[0][d] + acc[1][d]) + (acc[2][d] + acc[3][d]);
+  __syncthreads();
+  if (tid < D / 2) {
+    const int d = 2 * tid;
+    const float o0 = ((red[0][d] + red[1][d]) + (red[2][d] + red[3][d])) * inv;
+    const float o1 = ((red[0][d + 1] + red[1][d + 1]) + (red[2][d + 1] + red[3][d + 1])) * inv;
+    uint32_t hi, lo;
+    split_half2(o0, o1, hi, lo);
+    half* out = ctx + (long long)g * ctx_gs + (long long)b * hidden + h * D + d;
+    *reinterpret_cast<uint32_t*>(out) = hi;
+    *reinterpret_cast<uint32_t*>(out + lo_off) = lo;
+  }
+}
+
+void launch_attention_cls(const half* qkv, long long qkv_gs, const half* q, long long q_gs, const int* cu_seqlens,
+                          int n_seqs, int groups, int n_heads, int head_dim, int hidden, half* ctx, long long ctx_gs,
+                          long long lo_off, int max_len, cudaStream_t stream) {
+  if (n_seqs <= 0 || groups <= 0) return;
+  const float scale = 1.0f / sqrtf(static_cast<float>(head_dim));
+  const size_t smem = sizeof(float) * (size_t)max_len;
+  dim3 grid(groups * n_heads, n_seqs);
+  if (head_dim == 64) {
+    if (smem > 48 * 1024) cudaFuncSetAttribute(attn_cls_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    launch_pdl(attn_cls_kernel<64>, grid, dim3(kClsThreads), smem, stream, qkv, qkv_gs, q, q_gs, cu_seqlens, n_heads,
+               hidden, ctx, ctx_gs, lo_off, scale);
+  } else {
+    if (smem > 48 * 1024) cudaFuncSetAttribute(attn_cls_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    launch_pdl(attn_cls_kernel<32>, grid, dim3(kClsThreads), smem, stream, qkv, qkv_gs, q, q_gs, cu_seqlens, n_heads,
+               hidden, ctx, ctx_gs, lo_off, scale);
+  }
+}
+
+}  // namespace sp

@@ -124,7 +124,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     // previous kernel (weights never depend on it)
     for (int i = 0; i < n_pre; ++i) {
       mbar_arrive_expect_tx(&full[i], stage_bytes);
-      tma_load_2d(&maps.w, &full[i], smem + i * stage_bytes, (kb0 + i) * kBlockK, g * p.n_out + m0, pol_w);
+      tma_load_2d(&maps.w, &full[i], smem + i * stage_bytes, (kb0 + i) * kBlockK, g * p.w_gs + p.w_r0 + m0, pol_w);
     }
     tma_prefetch_desc(&maps.x64);
     tma_prefetch_desc(&maps.x16);
@@ -143,7 +143,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   if (warp == 0) {
     if (elect_one()) {
       const uint64_t pol_x = policy_evict_last();   // activations: re-read by every M tile
-      const int wrow = g * p.n_out + m0;
+      const int wrow = g * p.w_gs + p.w_r0 + m0;
       const int xrow = g * p.x_group_rows + n0;
       auto load_x = [&](int s, int kb) {
         uint8_t* sb = smem + s * stage_bytes + kATileBytes;
@@ -328,7 +328,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
         const int n_pre = min(p.stages, nkb);
         for (int i = 0; i < n_pre; ++i) {
           mbar_arrive_expect_tx(&full[i], full_bytes);
-          tma_load_2d(&maps.w, &full[i], smem + i * stage_bytes, i * kBlockK, g * p.n_out + mt * kBlockM, pol_w);
+          tma_load_2d(&maps.w, &full[i], smem + i * stage_bytes, i * kBlockK, g * p.w_gs + p.w_r0 + mt * kBlockM, pol_w);
         }
       }
     }
@@ -388,7 +388,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
       for (int u = u_first; u < units; u += u_stride) {
         int g, mt, nt;
         decode(u, g, mt, nt);
-        const int wrow = g * p.n_out + mt * kBlockM;
+        const int wrow = g * p.w_gs + p.w_r0 + mt * kBlockM;
         const int xrow = g * p.x_group_rows + nt * p.bn + (int)crank * x_rows;
         int kb = 0;
         if (first) {  // weight prefetch of the first stages before the dependency wait

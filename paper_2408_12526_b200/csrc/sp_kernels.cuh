@@ -54,6 +54,8 @@ enum Act : int { ACT_NONE = 0, ACT_TANH = 1, ACT_GELU = 2 };
 //    out + out_lo_off (the next GEMM's operand).
 struct GemmParams {
   int n_out;        // multiple of 128
+  int w_gs;         // weight rows per student in the map (>= n_out; the QKV slab is 3H rows)
+  int w_r0;         // first weight row of the launch within a student's slab (K|V of QKV: H)
   int k_dim;        // multiple of 64
   int t_rows;       // valid rows per student
   int x_group_rows; // X row stride between students
@@ -132,12 +134,41 @@ void launch_embed_ln(const int* ids, const int* cu_seqlens, int n_seqs, int n_to
                      const float* gamma, const float* beta, int hidden, float eps, float* x32, half* x16,
                      long long x_gs, long long x_lo_off, cudaStream_t stream);
 
-// Split-K reduce + bias + residual + LayerNorm:
-//   x = LN(x + b + sum_s part[s]); optional CLS rows copied to cls16[g][seq] (+ cls_lo_off: lo).
-void launch_reduce_ln(const float* part, int splits, long long part_split_stride, const float* bias,
-                      const float* gamma, const float* beta, int hidden, float eps, float* x32, half* x16,
-                      long long x_gs, long long x_lo_off, int n_tokens, int groups, const int* cu_seqlens, int n_seqs,
-                      half* cls16, long long cls_gs, long long cls_lo_off, cudaStream_t stream);
+// Split-K reduce + bias + residual + LayerNorm over rows t < n_rows of `groups` students:
+//   x_out[t] = LN(x_in[in_rows ? in_rows[t] : t] + b + sum_s part[s][t])  (fp32)
+//   x16[t] / x16[t] + x_lo_off = the (hi, lo) fp16 operand pair of the next projection
+//   cls16[seq] (+ cls_lo_off) = the same pair for the sequences' CLS rows, when cls16 is set.
+// Group strides (elements) per buffer; n_rows < 0: live count = cu[n_seqs] (graph replay).
+struct RowLn {
+  const float* part;
+  int splits;
+  long long part_ss, part_gs;
+  const float *bias, *gamma, *beta;  // [groups][hidden], already at the layer
+  const float* x_in;
+  long long in_gs;
+  const int* in_rows;  // residual row of output row t (the CLS rows: cu_seqlens), or null
+  float* x_out;
+  long long out_gs;
+  half* x16;
+  long long x16_gs, x_lo_off;
+  half* cls16;
+  long long cls_gs, cls_lo_off;
+  int hidden;
+  float eps;
+  int n_rows;
+  const int* cu;
+  int n_seqs;
+};
+void launch_reduce_ln(const RowLn& a, int groups, cudaStream_t stream);
+
+// Attention of the CLS query only (the last layer: only the CLS row reaches the pooler): per
+// (student, sequence, head) softmax(q_CLS K^T / sqrt(d)) V over the sequence's keys, fp32. Keys and
+// values from qkv [g][T][3H]; the query from q[g][seq] (row stride hidden, group stride q_gs), or,
+// when q is null, from the CLS row of qkv. The context row is written as an (hi, lo) pair to
+// ctx[g][seq] (row stride hidden, group stride ctx_gs).
+void launch_attention_cls(const half* qkv, long long qkv_gs, const half* q, long long q_gs, const int* cu_seqlens,
+                          int n_seqs, int groups, int n_heads, int head_dim, int hidden, half* ctx, long long ctx_gs,
+                          long long lo_off, int max_len, cudaStream_t stream);
 
 // Boosting sum + shared classifier (distill.py:169-178, :512):
 //   final[m][b] = splits ? tanh(sum_s part[s][m][b] + b_pool[m]) : final_rep[m][b]

@@ -337,11 +337,17 @@ __device__ __forceinline__ float warp_sum(float v) {
   return v;
 }
 
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
 __device__ __forceinline__ float gelu_erf_exact(float x) { return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f)); }
 
 // erf-GELU with erf from Abramowitz & Stegun 7.1.28: erf(z) ~ 1 - (1 + a1 z + ... + a6 z^6)^-16,
 // |error| <= 3e-7 (8.7e-7 measured on the GELU in fp32): one MUFU reciprocal and ~11 FMA/FMUL,
-// no exponential. The result is stored as fp16 (relative precision 4.9e-4).
+// no exponential. The result is stored as an fp16 (hi, lo) pair (~22 significant bits).
 __device__ __forceinline__ float gelu_erf(float x) {
   const float z = fabsf(x) * 0.70710678118654752f;
   float p = fmaf(4.30638e-5f, z, 2.765672e-4f);

@@ -57,38 +57,38 @@ __global__ void __launch_bounds__(128)
 
 // SPLITS: number of split-K partials, a template parameter so only the live ones hold registers
 // (4 x NC float4 partials capped occupancy at 4 blocks/SM when the persistent path writes one).
+// Row t: x_out[t] = LN(x_in[in_rows ? in_rows[t] : t] + b + sum_s part[s][t]); the (hi, lo) operand
+// to x16; the CLS rows of the sequences also to cls16 (when set).
 template <int NC, int SPLITS>
-__global__ void __launch_bounds__(128)
-    reduce_ln_kernel(const float* __restrict__ part, int splits, long long part_split_stride,
-                     const float* __restrict__ bias, const float* __restrict__ gamma, const float* __restrict__ beta,
-                     int hidden, float eps, float* x32, half* x16, long long x_gs, int n_tokens,
-                     const int* __restrict__ cu, int n_seqs, half* cls16, long long cls_gs, long long x_lo_off,
-                     long long cls_lo_off) {
+__global__ void __launch_bounds__(128) reduce_ln_kernel(const RowLn a) {
   // request inputs (cu_seqlens) and weights (bias) are read before the dependency wait
   pdl_launch_dependents();
   const int t = blockIdx.x * 4 + warp_id();
-  if (n_tokens < 0) n_tokens = __ldg(cu + n_seqs);
-  if (t >= n_tokens) return;
+  const int n_rows = a.n_rows < 0 ? __ldg(a.cu + a.n_seqs) : a.n_rows;
+  if (t >= n_rows) return;
   const int g = blockIdx.y;
   const int lane = lane_id();
-  const long long row = (long long)g * x_gs + (long long)t * hidden;
+  const int hidden = a.hidden;
   float4 r[NC], bs[NC], pv[SPLITS][NC];
 #pragma unroll
   for (int c = 0; c < NC; ++c)
-    bs[c] = __ldg(reinterpret_cast<const float4*>(bias + (long long)g * hidden + c * 128 + lane * 4));
+    bs[c] = __ldg(reinterpret_cast<const float4*>(a.bias + (long long)g * hidden + c * 128 + lane * 4));
   half* cls_row = nullptr;
-  if (cls16 != nullptr) {
-    const int b = seq_of(cu, n_seqs, t);
-    if (__ldg(cu + b) == t) cls_row = cls16 + (long long)g * cls_gs + (long long)b * hidden;
+  if (a.cls16 != nullptr) {
+    const int b = seq_of(a.cu, a.n_seqs, t);
+    if (__ldg(a.cu + b) == t) cls_row = a.cls16 + (long long)g * a.cls_gs + (long long)b * hidden;
   }
+  const int t_in = a.in_rows ? __ldg(a.in_rows + t) : t;
+  const float* x_in = a.x_in + (long long)g * a.in_gs + (long long)t_in * hidden;
+  const float* part = a.part + (long long)g * a.part_gs + (long long)t * hidden;
   pdl_wait();
   // then every load of the row at once: residual and up to kMaxSplitsRow partial sums
 #pragma unroll
   for (int c = 0; c < NC; ++c) {
     const int f = c * 128 + lane * 4;
-    r[c] = *reinterpret_cast<const float4*>(x32 + row + f);
+    r[c] = *reinterpret_cast<const float4*>(x_in + f);
 #pragma unroll
-    for (int s = 0; s < SPLITS; ++s) pv[s][c] = *reinterpret_cast<const float4*>(part + s * part_split_stride + row + f);
+    for (int s = 0; s < SPLITS; ++s) pv[s][c] = *reinterpret_cast<const float4*>(part + s * a.part_ss + f);
   }
   float v[NC][4];
 #pragma unroll
@@ -105,8 +105,9 @@ __global__ void __launch_bounds__(128)
       v[c][3] += pv[s][c].w;
     }
   }
-  layer_norm_store<NC>(v, gamma + (long long)g * hidden, beta + (long long)g * hidden, eps, hidden, x32 + row,
-                       x16 + row, x_lo_off, cls_row, cls_lo_off);
+  layer_norm_store<NC>(v, a.gamma + (long long)g * hidden, a.beta + (long long)g * hidden, a.eps, hidden,
+                       a.x_out + (long long)g * a.out_gs + (long long)t * hidden,
+                       a.x16 + (long long)g * a.x16_gs + (long long)t * hidden, a.x_lo_off, cls_row, a.cls_lo_off);
 }
 
 // One CTA per output row b, one thread per feature j (blockDim = hidden <= 1024).
@@ -232,24 +233,19 @@ void launch_embed_ln(const int* ids, const int* cu_seqlens, int n_seqs, int n_to
 #undef SP_EMBED
 }
 
-void launch_reduce_ln(const float* part, int splits, long long part_split_stride, const float* bias,
-                      const float* gamma, const float* beta, int hidden, float eps, float* x32, half* x16,
-                      long long x_gs, long long x_lo_off, int n_tokens, int groups, const int* cu_seqlens, int n_seqs,
-                      half* cls16, long long cls_gs, long long cls_lo_off, cudaStream_t stream) {
-  if (n_tokens == 0 || groups <= 0) return;
-  dim3 grid(((n_tokens < 0 ? -n_tokens : n_tokens) + 3) / 4, groups);
-  if (n_tokens < 0) n_tokens = -1;
-#define SP_REDUCE_S(NC_, S_)                                                                                     \
-  launch_pdl(reduce_ln_kernel<NC_, S_>, grid, dim3(128), 0, stream, part, splits, part_split_stride, bias, gamma, \
-             beta, hidden, eps, x32, x16, x_gs, n_tokens, cu_seqlens, n_seqs, cls16, cls_gs, x_lo_off, cls_lo_off)
+void launch_reduce_ln(const RowLn& a, int groups, cudaStream_t stream) {
+  if (a.n_rows == 0 || groups <= 0) return;
+  // n_rows < 0: grid sized for -n_rows rows, live count read from cu_seqlens (graph replay)
+  dim3 grid(((a.n_rows < 0 ? -a.n_rows : a.n_rows) + 3) / 4, groups);
+#define SP_REDUCE_S(NC_, S_) launch_pdl(reduce_ln_kernel<NC_, S_>, grid, dim3(128), 0, stream, a)
 #define SP_REDUCE(NC_)                     \
   do {                                     \
-    if (splits <= 1) SP_REDUCE_S(NC_, 1);  \
-    else if (splits == 2) SP_REDUCE_S(NC_, 2); \
-    else if (splits == 3) SP_REDUCE_S(NC_, 3); \
+    if (a.splits <= 1) SP_REDUCE_S(NC_, 1);  \
+    else if (a.splits == 2) SP_REDUCE_S(NC_, 2); \
+    else if (a.splits == 3) SP_REDUCE_S(NC_, 3); \
     else SP_REDUCE_S(NC_, 4);              \
   } while (0)
-  switch (hidden / 128) {
+  switch (a.hidden / 128) {
     case 1: SP_REDUCE(1); break;
     case 2: SP_REDUCE(2); break;
     case 4: SP_REDUCE(4); break;

@@ -125,7 +125,14 @@ struct sp_group {
   half* ffn = nullptr;     // [2][S][max_tokens][F] GELU output (FFN2 operand)
   float* part = nullptr;   // [kMaxSplits][S][max_tokens][H] split-K partials
   half* cls16 = nullptr;   // [2][S][max_seqs][H] CLS rows (pooler operand)
-  long long x_lo = 0, ctx_lo = 0, ffn_lo = 0, cls_lo = 0;
+  // the last layer on the CLS rows only (B = max_seqs rows per student)
+  float* xc32 = nullptr;   // [S][B][H] residual stream of the CLS rows
+  half* cln = nullptr;     // [2][S][B][H] LayerNorm-1 output of the CLS rows (FFN1 operand)
+  half* ctxc = nullptr;    // [2][S][B][H] CLS-query attention context (O operand)
+  half* ffnc = nullptr;    // [2][S][B][F] GELU output of the CLS rows (FFN2 operand)
+  float* partc = nullptr;  // [kMaxSplits][S][B][H] split-K partials of the CLS-row projections
+  half* qc = nullptr;      // [S][B][H] last-layer query of the CLS rows
+  long long x_lo = 0, ctx_lo = 0, ffn_lo = 0, cls_lo = 0, cf_lo = 0;  // cf_lo: lo offset of ffnc
   float* final32 = nullptr;  // [kMaxSplits][S][rows_cap][H] per-student final representation / pooler partials
   int32_t* d_ids = nullptr;  // staging block [cu_pad | ids]: d_cu = block, d_ids = block + cu_pad
   int32_t* d_cu = nullptr;
@@ -149,7 +156,7 @@ struct sp_group {
   CUtensorMap m_pool, m_in;
   CUtensorMap m_qkv_attn;  // qkv buffer viewed with a {64, 128} box (tensor-core attention)
   CUtensorMap m_qkv_kv64;  // the same with a {64, 64} box (64-key chunks of the three-CTA kernel)
-  XMaps xm_x16, xm_ctx, xm_ffn, xm_cls, xm_ha, xm_hb;
+  XMaps xm_x16, xm_ctx, xm_ffn, xm_cls, xm_ha, xm_hb, xm_cln, xm_ctxc, xm_ffnc;
   half* ha = nullptr;  // dense kind: hidden-state ping-pong [2][S][T][H] each
   half* hb = nullptr;
   long long h_lo = 0;
@@ -327,6 +334,13 @@ int sp_group_create(const sp_config* cfg, const sp_weights* weights, int device,
     if ((rc = dev_alloc(g, &g->ffn, 2 * S * T * F))) return bail(rc);
     if ((rc = dev_alloc(g, &g->part, (size_t)kMaxSplits * S * T * H))) return bail(rc);
     if ((rc = dev_alloc(g, &g->cls16, 2 * S * B * H))) return bail(rc);
+    g->cf_lo = (long long)(S * B * F);
+    if ((rc = dev_alloc(g, &g->xc32, S * B * H))) return bail(rc);
+    if ((rc = dev_alloc(g, &g->cln, 2 * S * B * H))) return bail(rc);
+    if ((rc = dev_alloc(g, &g->ctxc, 2 * S * B * H))) return bail(rc);
+    if ((rc = dev_alloc(g, &g->ffnc, 2 * S * B * F))) return bail(rc);
+    if ((rc = dev_alloc(g, &g->partc, (size_t)kMaxSplits * S * B * H))) return bail(rc);
+    if ((rc = dev_alloc(g, &g->qc, S * B * H))) return bail(rc);
     const auto* wq = static_cast<const half*>(w.w_qkv);
     const auto* wo = static_cast<const half*>(w.w_o);
     const auto* w1 = static_cast<const half*>(w.w_ffn1);
@@ -347,6 +361,9 @@ int sp_group_create(const sp_config* cfg, const sp_weights* weights, int device,
     ok &= make_xmaps(&g->xm_ctx, g->ctx, g->ctx + g->ctx_lo, S * T, H);
     ok &= make_xmaps(&g->xm_ffn, g->ffn, g->ffn + g->ffn_lo, S * T, F);
     ok &= make_xmaps(&g->xm_cls, g->cls16, g->cls16 + g->cls_lo, S * B, H);
+    ok &= make_xmaps(&g->xm_cln, g->cln, g->cln + g->cls_lo, S * B, H);
+    ok &= make_xmaps(&g->xm_ctxc, g->ctxc, g->ctxc + g->cls_lo, S * B, H);
+    ok &= make_xmaps(&g->xm_ffnc, g->ffnc, g->ffnc + g->cf_lo, S * B, F);
     ok &= make_map(&g->m_qkv_attn, g->qkv, S * T, 3 * H, 128);
     ok &= make_map(&g->m_qkv_kv64, g->qkv, S * T, 3 * H, 64);
     // rows past a request's tokens are read (masked) by the attention tiles: keep them finite
@@ -444,10 +461,12 @@ void launch_attention_any(int kind, const CUtensorMap& map_qkv, const CUtensorMa
 void run_gemm(sp_group* grp, int kind, const CUtensorMap& wmap, const XMaps& xm, int groups, int n_out, int k_dim,
               int t_rows, int x_group_rows, const float* bias, int bias_gs, int act, void* out, long long out_gs,
               long long out_lo_off, int out_f32, int splits, long long split_stride, cudaStream_t st,
-              const int* t_dev = nullptr) {
+              const int* t_dev = nullptr, int out_ld = 0, int w_gs = 0, int w_r0 = 0) {
   sp::GemmParams p{};
   p.t_dev = t_dev;
   p.n_out = n_out;
+  p.w_gs = w_gs ? w_gs : n_out;
+  p.w_r0 = w_r0;
   p.k_dim = k_dim;
   p.t_rows = t_rows;
   p.x_group_rows = x_group_rows;
@@ -456,7 +475,7 @@ void run_gemm(sp_group* grp, int kind, const CUtensorMap& wmap, const XMaps& xm,
   p.out = out;
   p.out_group_stride = out_gs;
   p.out_lo_off = out_f32 ? 0 : out_lo_off;
-  p.out_ld = n_out;
+  p.out_ld = out_ld ? out_ld : n_out;
   p.bias = bias;
   p.bias_group_stride = bias_gs;
   p.act = act;
@@ -467,8 +486,10 @@ void run_gemm(sp_group* grp, int kind, const CUtensorMap& wmap, const XMaps& xm,
   maps.x16 = xm.x16;
   maps.xl64 = xm.xl64;
   maps.xl16 = xm.xl16;
-  const double G = groups, N = n_out, K = k_dim, T = t_rows, terms = xm.hilo ? 2.0 : 1.0;
-  const double xin = (x_group_rows == 0 ? 1.0 : G) * T * K * 2.0 * terms;
+  // profiling: algorithmic bytes of a projection = its weights + bias (the activations
+  // are L2-resident at batch-1 and not part of the request's compulsory HBM traffic)
+  const double G = groups, N = n_out, K = k_dim, T = t_rows;
+  const double wbytes = G * N * K * 2.0 + (bias ? G * N * 4.0 : 0.0);
   // one-split projections from 17 tokens on: the persistent kernel (measured equal or 2-4 us faster)
   if (splits == 1 && t_rows >= 17) {
     p.splits = 1;
@@ -478,10 +499,7 @@ void run_gemm(sp_group* grp, int kind, const CUtensorMap& wmap, const XMaps& xm,
     // weights re-read by many token tiles stay in L2 (evict_last); streamed once or twice (batch-1)
     // they must not push the residual stream out (evict_first: -2% at L=512)
     p.w_keep = p.n_tiles > 2 ? 2 : 0;
-    if (grp)
-      grp->rec_begin(kind, G * N * K * 2.0 + xin + G * T * N * (out_f32 ? 4.0 : 2.0 * (out_lo_off ? 2 : 1)) +
-                               (bias ? G * N * 4.0 : 0.0),
-                     2.0 * G * N * K * T * terms);
+    if (grp) grp->rec_begin(kind, wbytes, 2.0 * G * N * K * T);
     sp::launch_gemm_persistent(maps, p, groups, st);
     if (grp) grp->rec_end();
     return;
@@ -493,10 +511,7 @@ void run_gemm(sp_group* grp, int kind, const CUtensorMap& wmap, const XMaps& xm,
   p.splits = splits;
   p.kb_per_split = (k_dim / 64) / splits;
   p.out_split_stride = split_stride;
-  if (grp) {
-    const double outb = G * T * N * (splits > 1 ? 4.0 * splits : (out_f32 ? 4.0 : 2.0 * (out_lo_off ? 2 : 1)));
-    grp->rec_begin(kind, G * N * K * 2.0 + xin + outb + (bias ? G * N * 4.0 : 0.0), 2.0 * G * N * K * T * terms);
-  }
+  if (grp) grp->rec_begin(kind, wbytes, 2.0 * G * N * K * T);
   sp::launch_gemm(maps, p, groups, st);
   if (grp) grp->rec_end();
 }
@@ -547,8 +562,7 @@ int run_mlp(sp_group* g, int l, int k, int n_tokens, const int* t_dev, cudaStrea
   m.xbl64 = g->xm_ffn.xl64;
   m.xbl16 = g->xm_ffn.xl16;
   const double G = k, Tt = n_tokens;
-  g->rec_begin(SP_LAUNCH_GEMM_FFN1, G * 2.0 * F * H * 2.0 + G * Tt * (H * 4.0 + F * 4.0 * 2.0 + H * 4.0),
-               2.0 * 2.0 * 2.0 * G * F * H * Tt);
+  g->rec_begin(SP_LAUNCH_GEMM_FFN1, G * 2.0 * F * H * 2.0 + G * F * 4.0, 2.0 * 2.0 * G * F * H * Tt);
   sp::launch_mlp(m, p, st);
   g->rec_end();
   return p.splits_b;
@@ -582,11 +596,85 @@ int bert_forward(sp_group* g, const int32_t* ids, const int32_t* cu, int n_seqs,
     const int s_o = choose_splits(k * (H / 128) * n_tiles, H / 64, kMaxSplits);
     const int s_f = choose_splits(k * (H / 128) * n_tiles, F / 64, kMaxSplits);
     const int akind = attn_kind(H / c.n_heads, max_len);
+    // CLS-row projections of the last layer: n_seqs rows per student
+    const long long bgs = (long long)B * H, partc_ss = (long long)S * bgs;
+    int bn_c, n_tiles_c;
+    sp::gemm_configure_tiles(n_seqs, &bn_c, &n_tiles_c, &stages);
+    const int s_oc = choose_splits(k * (H / 128) * n_tiles_c, H / 64, kMaxSplits);
+    const int s_fc = choose_splits(k * (H / 128) * n_tiles_c, F / 64, kMaxSplits);
+    const double GBH = (double)k * n_seqs * H;
+    // one LayerNorm launch (rows of k students)
+    auto layer_norm = [&](const float* part, int splits, long long pss, long long pgs, const float* b_, const float* g_,
+                          const float* be_, const float* x_in, long long in_gs, const int* in_rows, float* x_out,
+                          long long out_gs, half* x16, long long x16_gs, long long lo, int n_rows, double rows,
+                          half* cls_copy = nullptr) {
+      sp::RowLn a{};
+      a.cls16 = cls_copy;  // CLS rows also to cls_copy (the last layer's query operand)
+      a.cls_gs = bgs;
+      a.cls_lo_off = g->cls_lo;
+      a.part = part;
+      a.splits = splits;
+      a.part_ss = pss;
+      a.part_gs = pgs;
+      a.bias = b_;
+      a.gamma = g_;
+      a.beta = be_;
+      a.x_in = x_in;
+      a.in_gs = in_gs;
+      a.in_rows = in_rows;
+      a.x_out = x_out;
+      a.out_gs = out_gs;
+      a.x16 = x16;
+      a.x16_gs = x16_gs;
+      a.x_lo_off = lo;
+      a.hidden = H;
+      a.eps = c.ln_eps;
+      a.n_rows = n_rows;
+      a.cu = cu;
+      a.n_seqs = n_seqs;
+      g->rec_begin(SP_LAUNCH_REDUCE_LN, rows * H * (4.0 * splits + 12.0), 0.0);
+      sp::launch_reduce_ln(a, k, st);
+      g->rec_end();
+      ++launches;
+    };
     for (int l = 0; l < c.n_layers; ++l) {
       const size_t lS = (size_t)l * S;
       const bool last = (l == c.n_layers - 1);
-      run_gemm(g, SP_LAUNCH_GEMM_QKV, g->m_qkv[l], g->xm_x16, k, 3 * H, H, n_tokens, T, w.b_qkv + lS * 3 * H, 3 * H,
-               sp::ACT_NONE, g->qkv, (long long)T * 3 * H, 0, 0, 1, 0, st, t_dev);
+      if (last && l > 0) {
+        // last layer: K and V of every token (weight rows [H, 3H) of each student's QKV slab), the
+        // query of the CLS rows only (rows [0, H) on the CLS copies the previous LayerNorm wrote)
+        run_gemm(g, SP_LAUNCH_GEMM_QKV, g->m_qkv[l], g->xm_x16, k, 2 * H, H, n_tokens, T, w.b_qkv + lS * 3 * H + H,
+                 3 * H, sp::ACT_NONE, g->qkv + H, (long long)T * 3 * H, 0, 0, 1, 0, st, t_dev, 3 * H, 3 * H, H);
+        run_gemm(g, SP_LAUNCH_GEMM_QKV, g->m_qkv[l], g->xm_cls, k, H, H, n_seqs, B, w.b_qkv + lS * 3 * H, 3 * H,
+                 sp::ACT_NONE, g->qc, bgs, 0, 0, 1, 0, st, nullptr, H, 3 * H, 0);
+        launches += 2;
+      } else {
+        run_gemm(g, SP_LAUNCH_GEMM_QKV, g->m_qkv[l], g->xm_x16, k, 3 * H, H, n_tokens, T, w.b_qkv + lS * 3 * H,
+                 3 * H, sp::ACT_NONE, g->qkv, (long long)T * 3 * H, 0, 0, 1, 0, st, t_dev);
+        ++launches;
+      }
+      if (last) {
+        // Only the CLS row of the last layer reaches the pooler: attention of the CLS query over
+        // the sequence's keys, then O, LayerNorm-1, FFN and LayerNorm-2 on the CLS rows alone
+        // (n_seqs rows per student; the residual input is gathered at cu_seqlens[b]).
+        g->rec_begin(SP_LAUNCH_ATTENTION, GTH * 4.0, 4.0 * k * H * (double)n_tokens);
+        sp::launch_attention_cls(g->qkv, (long long)T * 3 * H, l > 0 ? g->qc : nullptr, bgs, cu, n_seqs, k,
+                                 c.n_heads, H / c.n_heads, H, g->ctxc, bgs, g->cls_lo, max_len, st);
+        g->rec_end();
+        run_gemm(g, SP_LAUNCH_GEMM_O, g->m_o[l], g->xm_ctxc, k, H, H, n_seqs, B, nullptr, H, sp::ACT_NONE, g->partc,
+                 bgs, 0, 1, s_oc, partc_ss, st);
+        ++launches;
+        layer_norm(g->partc, s_oc, partc_ss, bgs, w.b_o + lS * H, w.ln1_gamma + lS * H, w.ln1_beta + lS * H, g->x32,
+                   xgs, cu, g->xc32, bgs, g->cln, bgs, g->cls_lo, n_seqs, GBH);
+        run_gemm(g, SP_LAUNCH_GEMM_FFN1, g->m_f1[l], g->xm_cln, k, F, H, n_seqs, B, w.b_ffn1 + lS * F, F,
+                 sp::ACT_GELU, g->ffnc, (long long)B * F, g->cf_lo, 0, 1, 0, st);
+        run_gemm(g, SP_LAUNCH_GEMM_FFN2, g->m_f2[l], g->xm_ffnc, k, H, F, n_seqs, B, nullptr, H, sp::ACT_NONE,
+                 g->partc, bgs, 0, 1, s_fc, partc_ss, st);
+        launches += 2;
+        layer_norm(g->partc, s_fc, partc_ss, bgs, w.b_ffn2 + lS * H, w.ln2_gamma + lS * H, w.ln2_beta + lS * H,
+                   g->xc32, bgs, nullptr, g->xc32, bgs, g->cls16, bgs, g->cls_lo, n_seqs, GBH);
+        break;
+      }
       g->rec_begin(SP_LAUNCH_ATTENTION, GTH * 10.0, 4.0 * k * H * g->sum_len_sq);
       launch_attention_any(akind, g->m_qkv_attn, g->m_qkv_kv64, g->qkv, g->ctx, g->ctx_lo, cu, n_seqs, max_len, k,
                            c.n_heads, H / c.n_heads, H, T, st);
@@ -594,11 +682,9 @@ int bert_forward(sp_group* g, const int32_t* ids, const int32_t* cu, int n_seqs,
       // O and FFN2 write raw partial sums; the reduce+LN kernel owns bias, residual and LayerNorm
       run_gemm(g, SP_LAUNCH_GEMM_O, g->m_o[l], g->xm_ctx, k, H, H, n_tokens, T, nullptr, H, sp::ACT_NONE, g->part, xgs,
                0, 1, s_o, part_ss, st, t_dev);
-      g->rec_begin(SP_LAUNCH_REDUCE_LN, GTH * (4.0 * s_o + 12.0), 0.0);
-      sp::launch_reduce_ln(g->part, s_o, part_ss, w.b_o + lS * H, w.ln1_gamma + lS * H, w.ln1_beta + lS * H, H,
-                           c.ln_eps, g->x32, g->x16, xgs, g->x_lo, n_rows_arg, k, cu, n_seqs, nullptr, 0, 0, st);
-      g->rec_end();
-      launches += 4;
+      launches += 2;
+      layer_norm(g->part, s_o, part_ss, xgs, w.b_o + lS * H, w.ln1_gamma + lS * H, w.ln1_beta + lS * H, g->x32, xgs,
+                 nullptr, g->x32, xgs, g->x16, xgs, g->x_lo, n_rows_arg, GTH);
       // FFN1 + FFN2 as one persistent kernel where both would take the single-CTA persistent path
       // (only where FFN2 itself would be a one-split persistent GEMM: measured -2% at L=512, but
       // +3% at L=256 where FFN2's split-K tiles beat the fused kernel's 96-token phase-B tiles)
@@ -616,12 +702,9 @@ int bert_forward(sp_group* g, const int32_t* ids, const int32_t* cu, int n_seqs,
                  g->part, xgs, 0, 1, s_f, part_ss, st, t_dev);
         launches += 2;
       }
-      g->rec_begin(SP_LAUNCH_REDUCE_LN, GTH * (4.0 * s_ln2 + 12.0), 0.0);
-      sp::launch_reduce_ln(g->part, s_ln2, part_ss, w.b_ffn2 + lS * H, w.ln2_gamma + lS * H, w.ln2_beta + lS * H, H,
-                           c.ln_eps, g->x32, g->x16, xgs, g->x_lo, n_rows_arg, k, cu, n_seqs,
-                           last ? g->cls16 : nullptr, (long long)B * H, g->cls_lo, st);
-      g->rec_end();
-      ++launches;
+      layer_norm(g->part, s_ln2, part_ss, xgs, w.b_ffn2 + lS * H, w.ln2_gamma + lS * H, w.ln2_beta + lS * H, g->x32,
+                 xgs, nullptr, g->x32, xgs, g->x16, xgs, g->x_lo, n_rows_arg, GTH,
+                 l == c.n_layers - 2 ? g->cls16 : nullptr);
     }
     // pooler on the CLS rows: tanh(W_p h_CLS + b_p). Few rows: split-K partials (more CTAs stream the
     // pooler weights), finished by the head kernel; many rows: one pass with the tanh epilogue.

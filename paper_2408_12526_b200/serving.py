@@ -7,9 +7,12 @@ real engine can replace its analytic ``service_time`` (servesim.py:287-307):
   and multi-phase bursts (cli.py:191-202); deterministic per seed (seeding.py:19-21).
 * ``decide_controller_action`` — DROP_ONE / ADD_ONE / HOLD (servesim.py:317-342).
 * ``nearest_rank_percentile`` — the p50/p99 definition of the metric (servesim.py:370-376).
-* ``AdaptiveServer`` — a live serving loop: requests are dispatched immediately on arrival
-  (no batching wait, no padding), the active prefix k is snapshotted per request
-  (servesim.py:486) and adapted by the controller rule from the observed backlog.
+* ``AdaptiveServer`` — the serving loop on the real engine: the simulator's event loop
+  (servesim.py:430-549: arrivals, completions, 100 ms heartbeats; retries, controller tick and
+  dispatch at every boundary) with the analytic service time replaced by the measured execution of
+  a launch. Queued requests are packed into ONE unpadded launch (cu_seqlens) up to a token budget
+  the moment an engine slot is free — no batching wait, no padding; ``max_batch_seqs=1`` is the
+  single-request-in-flight server. k is snapshotted per launch (servesim.py:486).
 """
 from __future__ import annotations
 
@@ -135,72 +138,135 @@ class ServeMetrics:
     records: list[ServeRecord] = field(default_factory=list, repr=False)
 
 
+HEARTBEAT_MS = 100.0  # servesim.py:411
+
+
+def group_count(group_size: int, gpus: int, replicas_per_gpu: int) -> int:
+    """Replica groups a node hosts: floor(replicas x G / S), at least 1 (servesim.py:220-222)."""
+    return max(1, (replicas_per_gpu * gpus) // group_size)
+
+
 class AdaptiveServer:
     """Open-loop serving of an arrival trace on a real engine with the adaptive student count.
 
-    ``execute(req, k) -> service_ms`` runs one request on the engine (batch-1, unpadded) and
-    returns its measured service time; it replaces the simulator's analytic service_time
-    (servesim.py:486-487). The server keeps one in-flight request per group (a FIFO of arrivals
-    is the buffer); at each dispatch boundary the controller compares the backlog against
-    ``buffer_capacity`` (DROP_ONE when full) and the time the queue has been empty (ADD_ONE
-    after ``idle_window_ms``), exactly the rule of decide_controller_action. Time is virtual:
-    it advances by the measured service times, so the trace is replayed faithfully without
-    sleeping.
+    ``execute(reqs, k, active) -> service_ms`` runs ONE launch on the engine: the requests ``reqs``
+    packed unpadded (cu_seqlens), the first ``k`` students, while ``active`` launches are in flight
+    (including this one), and returns its measured service time — it replaces the simulator's
+    analytic service_time (servesim.py:486-487). Time is virtual: it advances by the measured
+    service times, so the trace is replayed faithfully without sleeping.
+
+    Event semantics follow Simulation (servesim.py:430-549): arrivals push into a bounded FIFO (a
+    push into a full buffer is deferred to a retry queue, :519-523, :539-542); every event boundary
+    first retries deferred pushes, then runs the controller (decide_controller_action with the
+    real inputs: any buffer full, the time every buffer has been empty — None while a request is
+    queued —, idle and occupied student slots, :497-517), then dispatches while a slot is free
+    (:481-487), packing queued requests FIFO up to ``max_batch_seqs`` / ``max_batch_tokens``.
+    Heartbeats every 100 ms let ADD_ONE fire during idle periods. ``slots(k)`` (default 1: one
+    launch in flight per GPU) and ``capacity(k)`` (buffer capacity in requests) may depend on k like
+    the reference's group_count (:220-222, :465-471).
     """
 
     def __init__(self, execute, max_students: int, min_students: int = 1, start_k: int | None = None,
-                 buffer_capacity: int = 8, idle_window_ms: float = 50.0):
+                 buffer_capacity=8, idle_window_ms: float = 50.0, max_batch_seqs: int = 1,
+                 max_batch_tokens: int = 1 << 30, slots=1):
         if not 1 <= min_students <= max_students:
             raise ValueError("need 1 <= min_students <= max_students")
+        if max_batch_seqs < 1 or max_batch_tokens < 1:
+            raise ValueError("batch limits must be >= 1")
         self.execute = execute
         self.max_students, self.min_students = max_students, min_students
         self.k = max_students if start_k is None else start_k
         if not min_students <= self.k <= max_students:
             raise ValueError("start_k outside [min_students, max_students]")
-        self.capacity = buffer_capacity
+        self.capacity = buffer_capacity if callable(buffer_capacity) else (lambda k, c=buffer_capacity: c)
+        self.slots = slots if callable(slots) else (lambda k, n=slots: n)
         self.idle_window_ms = idle_window_ms
+        self.max_batch_seqs, self.max_batch_tokens = max_batch_seqs, max_batch_tokens
+        self.actions: list[tuple[float, str]] = []
+        self.batches: list[int] = []
+        self.rejected_pushes = 0
 
     def run(self, requests: list[Request]) -> ServeMetrics:
-        now = 0.0
-        queue: list[Request] = []
-        i = 0
-        idle_since: float | None = 0.0
+        import heapq
+        from collections import deque
+
+        events: list = []
+        seq = 0
+
+        def push_event(t, kind, payload):
+            nonlocal seq
+            heapq.heappush(events, (t, seq, kind, payload))
+            seq += 1
+
+        for r in requests:
+            push_event(r.arrival_ms, "arrival", r)
+        horizon = max((r.arrival_ms for r in requests), default=0.0) + self.idle_window_ms + 5 * HEARTBEAT_MS
+        t = 0.0
+        while t <= horizon:
+            push_event(t, "heartbeat", None)
+            t += HEARTBEAT_MS
+        queue: deque[Request] = deque()
+        retry: deque[Request] = deque()
+        busy = 0
+        empty_since: float | None = 0.0
         timeline = [(0.0, self.k)]
         records: list[ServeRecord] = []
-        n = len(requests)
-        while i < n or queue:
-            while i < n and requests[i].arrival_ms <= now:
-                queue.append(requests[i])
-                i += 1
-            if not queue:
-                now = requests[i].arrival_ms
-                continue
-            # controller boundary (servesim.py:497-531): buffer full -> drop; long idle -> add
-            idle_ms = None if idle_since is None else now - idle_since
+
+        def try_push(req) -> bool:
+            if len(queue) >= self.capacity(self.k):
+                return False
+            queue.append(req)
+            return True
+
+        while events:
+            now, _, kind, payload = heapq.heappop(events)
+            if kind == "arrival":
+                if retry or not try_push(payload):
+                    self.rejected_pushes += 1
+                    retry.append(payload)
+            elif kind == "completion":
+                start, k_b, batch = payload
+                busy -= 1
+                for req in batch:
+                    records.append(ServeRecord(req.id, req.arrival_ms, start, now, k_b, req.length_tokens))
+            # ---- event boundary (servesim.py:525-531)
+            while retry and try_push(retry[0]):
+                retry.popleft()
+            idle_ms = (now - empty_since) if (not queue and empty_since is not None) else None
+            slots = self.slots(self.k)
             action = decide_controller_action(self.k, self.min_students, self.max_students,
-                                              len(queue) >= self.capacity, idle_ms,
-                                              idle_students=self.k, occupied_students=0,  # the group is idle here
+                                              len(queue) >= self.capacity(self.k), idle_ms,
+                                              idle_students=max(0, slots - busy) * self.k,
+                                              occupied_students=busy * self.k,
                                               idle_window_ms=self.idle_window_ms)
             if action == DROP_ONE:
                 self.k -= 1
                 timeline.append((now, self.k))
+                self.actions.append((now, action))
             elif action == ADD_ONE:
                 self.k += 1
-                idle_since = now
                 timeline.append((now, self.k))
-            req = queue.pop(0)
-            k_req = self.k  # snapshotted per dispatched request (servesim.py:486)
-            service = float(self.execute(req, k_req))
-            start = now
-            now = now + service
-            records.append(ServeRecord(req.id, req.arrival_ms, start, now, k_req, req.length_tokens))
-            while i < n and requests[i].arrival_ms <= now:
-                queue.append(requests[i])
-                i += 1
-            if queue:
-                idle_since = None
-            elif idle_since is None:
-                idle_since = now
+                self.actions.append((now, action))
+                if empty_since is not None:  # a fresh idle window must elapse before the next add
+                    empty_since = now
+            while busy < self.slots(self.k) and queue:
+                batch = [queue.popleft()]
+                tokens = batch[0].length_tokens
+                while (queue and len(batch) < self.max_batch_seqs
+                       and tokens + queue[0].length_tokens <= self.max_batch_tokens):
+                    tokens += queue[0].length_tokens
+                    batch.append(queue.popleft())
+                busy += 1
+                k_b = self.k  # snapshotted per dispatched launch (servesim.py:486)
+                dt = float(self.execute(batch, k_b, busy))
+                self.batches.append(len(batch))
+                push_event(now + dt, "completion", (now, k_b, batch))
+            if not queue:
+                if empty_since is None:
+                    empty_since = now
+            else:
+                empty_since = None
+        records.sort(key=lambda r: (r.arrival_ms, r.request_id))
         lat = [r.latency_ms for r in records]
         return ServeMetrics(nearest_rank_percentile(lat, 50), nearest_rank_percentile(lat, 99),
                             float(np.mean(lat)), len(records), timeline, records)

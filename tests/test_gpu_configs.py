@@ -79,7 +79,7 @@ def test_base_bert_full_group_16_ragged_requests():
 
     cfg, K = PRESETS["base"]
     w = random_bert_group(cfg, K, seed=41)
-    grp = StudentGroup(w, max_tokens=4096, max_seqs=16)
+    grp = StudentGroup(w, max_tokens=8192, max_seqs=16)
     rng = np.random.default_rng(41)
     seqs = _seqs(rng, rng.integers(16, 513, size=16))
     _, z_ref = OracleBertGroup(w).forward(seqs)
@@ -102,30 +102,44 @@ def test_k32_group_batch1_every_adaptive_prefix():
         _check(grp.logits(ids, k), z_ref)
 
 
-def test_adaptive_server_runs_on_engine():
+def test_adaptive_server_on_engine_single_and_batched():
+    """The serving loop drives the real engine through forward_host on a bursty trace (B8 group,
+    k in [2, 8]): single request in flight (bucket graphs) and continuous batching (queued requests
+    packed into one unpadded launch). Every launch's logits equal the same requests run one by one
+    at the launch's k."""
     import time
 
     from paper_2408_12526_b200 import PRESETS, StudentGroup, random_bert_group
     from paper_2408_12526_b200.serving import AdaptiveServer, generate_phases, synth_tokens
 
-    cfg, _ = PRESETS["tiny"]
-    group = StudentGroup(random_bert_group(cfg, 4, seed=1), max_tokens=128, max_seqs=1)
-    group.prepare_graphs(128, 4)
-    seen_k = []
+    cfg, K = PRESETS["base"]
+    group = StudentGroup(random_bert_group(cfg, K, seed=1), max_tokens=4096, max_seqs=32)
+    trace = generate_phases([(2000.0, 20.0), (40000.0, 5.0), (1000.0, 40.0)], seed=0, max_len=512, bin_width=32)
+    tokens = {r.id: synth_tokens(r, 0, cfg.vocab) for r in trace}
+    checked = []
 
-    def execute(req, k):
-        ids = synth_tokens(req, seed=0, vocab=cfg.vocab)
+    def execute(batch, k, active):
+        ids = np.concatenate([tokens[r.id] for r in batch])
+        cu = np.concatenate([[0], np.cumsum([len(tokens[r.id]) for r in batch])]).astype(np.int32)
         t0 = time.perf_counter()
-        z = group.forward_host(ids, np.array([0, len(ids)], np.int32), k)
-        assert z.shape == (1, 2) and np.all(np.isfinite(z))
-        seen_k.append(k)
-        return 1e3 * (time.perf_counter() - t0)
+        z = group.forward_host(ids, cu, k)
+        ms = 1e3 * (time.perf_counter() - t0)
+        assert z.shape == (len(batch), 2) and np.all(np.isfinite(z))
+        if len(batch) > 1 and len(checked) < 3:
+            one = np.stack([group.forward_host(tokens[r.id], np.array([0, len(tokens[r.id])], np.int32), k)[0]
+                            for r in batch])
+            np.testing.assert_allclose(z, one, rtol=0, atol=2e-5)
+            checked.append(len(batch))
+        return ms
 
-    trace = generate_phases([(2000.0, 40.0), (50000.0, 10.0), (2000.0, 60.0)], seed=0, max_len=128, bin_width=8)
-    metrics = AdaptiveServer(execute, max_students=4, min_students=2, buffer_capacity=4).run(trace)
-    assert len(seen_k) == len(trace)
-    assert min(seen_k) >= 2 and max(seen_k) <= 4
-    assert metrics.completed == len(trace)
+    single = AdaptiveServer(execute, max_students=K, min_students=2, buffer_capacity=16, idle_window_ms=5.0)
+    m1 = single.run(trace)
+    assert m1.completed == len(trace) and max(single.batches) == 1
+    batched = AdaptiveServer(execute, max_students=K, min_students=2, buffer_capacity=256, idle_window_ms=5.0,
+                             max_batch_seqs=32, max_batch_tokens=4096)
+    m2 = batched.run(trace)
+    assert m2.completed == len(trace) and max(batched.batches) > 1 and checked
+    assert all(2 <= r.k <= K for r in m1.records + m2.records)
 
 
 def test_sharded_host_path_matches_group_host_path():

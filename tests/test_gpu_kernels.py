@@ -57,8 +57,9 @@ def test_gemm_matches_torch(cuda_lib, T, act):
 
 @pytest.mark.parametrize("T", [16, 200])
 def test_gemm_hilo_operand_removes_fp16_rounding(cuda_lib, T):
-    """The lo term is what carries the precision: hi only is off by ~1e-3 relative (fp16 rounding of
-    the activation), hi + lo by ~1e-6, on both the small-T and the persistent kernel."""
+    """The lo term is what carries the precision: hi only is off by ~2e-4 of max|y| (fp16 rounding of
+    the activation), hi + lo by ~3e-6 (fp32 accumulation over K = 768), on both the small-T and the
+    persistent kernel."""
     from paper_2408_12526_b200 import _lib
 
     torch.manual_seed(T)
@@ -74,7 +75,7 @@ def test_gemm_hilo_operand_removes_fp16_rounding(cuda_lib, T):
                                        T, G * T, None, 0, out.data_ptr(), None, 1, 1, None))
         torch.cuda.synchronize()
         errs.append(float((out.double() - ref).abs().max() / ref.abs().max()))
-    assert errs[0] > 1e-4 and errs[1] < 2e-6, errs
+    assert errs[0] > 1e-4 and errs[1] < 1e-5 and errs[0] > 30 * errs[1], errs
 
 
 @pytest.mark.parametrize("T", [5, 48, 130])

@@ -151,8 +151,8 @@ def test_adaptive_server_drops_under_burst_and_recovers():
     full and adds them back after the idle window; k is snapshotted per request."""
     reqs = serving.generate_phases([(2000.0, 100.0), (20000.0, 20.0), (500.0, 400.0)], seed=0)
 
-    def execute(req, k):  # synthetic service time: 0.1 ms per active student
-        return 0.1 * k
+    def execute(batch, k, active):  # synthetic service time: 0.1 ms per active student per request
+        return 0.1 * k * len(batch)
 
     srv = serving.AdaptiveServer(execute, max_students=8, min_students=2, buffer_capacity=4, idle_window_ms=5.0)
     m = srv.run(reqs)
@@ -162,3 +162,109 @@ def test_adaptive_server_drops_under_burst_and_recovers():
     assert ks[-1] == 8, "idle tail should restore the full group"
     assert all(2 <= r.k <= 8 for r in m.records)
     assert m.p99_ms >= m.p50_ms > 0
+
+
+def test_adaptive_server_continuous_batching_packs_the_backlog():
+    """With max_batch_seqs > 1 every launch takes the whole FIFO backlog (up to the token budget) the
+    moment the engine is free: no batching wait (a lone request runs alone), no padding."""
+    reqs = serving.generate_phases([(2000.0, 50.0), (50000.0, 10.0), (500.0, 200.0)], seed=1, max_len=128)
+    seen = []
+
+    def execute(batch, k, active):
+        assert active == 1  # one launch in flight per GPU
+        seen.append(batch)
+        return 0.05 + 0.002 * sum(r.length_tokens for r in batch)
+
+    srv = serving.AdaptiveServer(execute, max_students=8, min_students=2, buffer_capacity=256,
+                                 max_batch_seqs=64, max_batch_tokens=2048)
+    m = srv.run(reqs)
+    assert m.completed == len(reqs)
+    assert max(len(b) for b in seen) > 1 and min(len(b) for b in seen) == 1
+    assert all(len(b) <= 64 and (len(b) == 1 or sum(r.length_tokens for r in b) <= 2048) for b in seen)
+    order = [r.id for b in seen for r in b]
+    assert order == sorted(order)  # FIFO
+
+
+def test_adaptive_server_reproduces_reference_simulation(ref):
+    """The serving loop is the reference's event loop: driven by the reference's own analytic
+    service_time (servesim.py:287-307) with one request per element (max_merge=1) and the
+    reference's slots / buffer capacity (group_count, :220-222), it reproduces Simulation's
+    student-number timeline and every request's completion time exactly, through a burst that
+    drops students and an idle tail that adds them back."""
+    import studentpar.perfmodel as pm
+
+    sim = ref.servesim
+    model = pm.PerfModel()
+    model.calibrate(pm.baseline_reference(), 11.6)
+    factors = sim.ServiceFactors(model=model, depth=2, width_per_student=256, capacity=pm.DEFAULT_CAPACITY,
+                                 pcie_tokens_per_ms=pm.DEFAULT_PCIE_TOKENS_PER_MS, gather_ms=pm.DEFAULT_GATHER_MS)
+    table = ref.distill.AccuracyTable([(k, 0.9 + 0.01 * k, 0.9 + 0.01 * k) for k in range(1, 4)])
+    ctl = sim.ControllerConfig(max_students=3, accuracy_table=table, min_students=1, idle_window_ms=300.0)
+    G, R = 4, 3
+    cluster = sim.ClusterConfig(controller=ctl, nodes=1, gpus_per_node=G, group_size=3, replicas_per_gpu=R,
+                                max_merge=1)
+    reqs = serving.generate_phases([(2000.0, 200.0), (30000.0, 60.0), (300.0, 900.0)], seed=3)
+    ref_reqs = [sim.Request(r.id, r.arrival_ms, r.length_tokens) for r in reqs]
+    want = sim.run_simulation(cluster, ref_reqs, factors)
+
+    def execute(batch, k, active):
+        (r,) = batch
+        b = sim.bin_of(r.length_tokens, cluster)
+        el = sim.BufferElement(bin=b, padded_len=(b + 1) * cluster.bin_width, requests=[ref_reqs[r.id]])
+        return sim.service_time(el, k, cluster, factors, active_groups=active)
+
+    cap = lambda k: sim.group_count(k, G, R)  # noqa: E731
+    srv = serving.AdaptiveServer(execute, max_students=3, min_students=1, start_k=3, buffer_capacity=cap,
+                                 idle_window_ms=300.0, max_batch_seqs=1, slots=cap)
+    got = srv.run(reqs)
+    assert [k for _, k in got.k_timeline] == [k for _, k in want.student_number_timeline]
+    assert [t for t, _ in got.k_timeline] == pytest.approx([t for t, _ in want.student_number_timeline], abs=1e-9)
+    assert min(k for _, k in got.k_timeline) < 3 and got.k_timeline[-1][1] == 3
+    assert srv.rejected_pushes == want.rejected_pushes
+    assert [(r.request_id, r.completion_ms) for r in got.records] == \
+        pytest.approx([(r.request_id, r.completion_ms) for r in want.per_request], abs=1e-9)
+
+
+@pytest.mark.parametrize("mode", ["binary", "json"])
+def test_bert_student_checkpoint_round_trip_bit_exact(tmp_path, mode):
+    """bert-student entries in ensemble-checkpoint-v1 (checkpoint.py): save -> load reproduces every
+    array bit for bit (float64 base64 / decimal lists of fp16 / fp32 values)."""
+    from paper_2408_12526_b200.checkpoint import load_ensemble_weights, save_bert_ensemble
+
+    cfg = BertConfig(hidden=128, n_heads=4, n_layers=2, vocab=300, max_pos=40, n_classes=3)
+    w = random_bert_group(cfg, 3, seed=5)
+    path = tmp_path / f"bert_{mode}.json"
+    save_bert_ensemble(w, path, mode)
+    back = load_ensemble_weights(path)
+    assert back.cfg == w.cfg and back.kind == "bert"
+    for name in ["word_emb", "pos_emb", "type_emb", "emb_ln_gamma", "emb_ln_beta", "w_qkv", "b_qkv", "w_o", "b_o",
+                 "ln1_gamma", "ln1_beta", "w_ffn1", "b_ffn1", "w_ffn2", "b_ffn2", "ln2_gamma", "ln2_beta", "w_pool",
+                 "b_pool", "alpha", "w_cls", "b_cls"]:
+        a, b = getattr(w, name), getattr(back, name)
+        assert a.dtype == b.dtype and a.shape == b.shape and a.tobytes() == b.tobytes(), name
+
+
+def test_bert_student_checkpoint_rejects_malformed(tmp_path):
+    import copy
+
+    from paper_2408_12526_b200.checkpoint import bert_group_from_dict, bert_group_to_dict
+
+    cfg = BertConfig(hidden=128, n_heads=4, n_layers=1, vocab=64, max_pos=16)
+    d = bert_group_to_dict(random_bert_group(cfg, 2, seed=1), "json")
+    bert_group_from_dict(d)
+    bad = copy.deepcopy(d)
+    bad["students"][1]["layers"][0]["ffn1"]["activation"] = "tanh"
+    with pytest.raises(ValueError):
+        bert_group_from_dict(bad)
+    bad = copy.deepcopy(d)
+    bad["multipliers"][0] = 0.5  # alpha_0 must be 1 (distill.py:152-153)
+    with pytest.raises(ValueError):
+        bert_group_from_dict(bad)
+    bad = copy.deepcopy(d)
+    bad["students"][0]["pooler"]["bias"][3] = float("nan")  # nnkernel.py:486-487
+    with pytest.raises(ValueError):
+        bert_group_from_dict(bad)
+    bad = copy.deepcopy(d)
+    bad["students"][0]["layers"][0]["o"]["out_dim"] = 64
+    with pytest.raises(ValueError):
+        bert_group_from_dict(bad)
