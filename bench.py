@@ -56,6 +56,9 @@ def parse_args():
                     help="batch-1 on one GPU: replay each request's 16-token-bucket CUDA graph (inputs copied "
                          "device-to-device into the engine's staging) instead of launching every kernel; "
                          "measured equal (5477 vs 5487 req/s): the eager chain is not host-bound")
+    ap.add_argument("--reduce", choices=["nccl", "p2p"], default="nccl",
+                    help="N > 1: logit reduce of the sharded group: one NCCL all-reduce (default), or the "
+                         "device-side mailbox (P2P stores into the root's GPU + flag, rank-order sum)")
     ap.add_argument("--batch", type=int, default=1,
                     help="requests per step, packed unpadded with cu_seqlens (1 = batch-1 streaming)")
     return ap.parse_args()
@@ -92,7 +95,7 @@ def workload_config(args, cfg, K, world):
         "K": K, "hidden": cfg.hidden, "heads": cfg.n_heads, "layers": cfg.n_layers, "ffn": cfg.ffn,
         "global_batch": args.batch, "seq_len": [args.len_min, args.len_max], "k_active": K,
         "students_per_gpu": [len(s) for s in placement(K, world)],
-        "parallelism": f"student-parallel x{world}" if world > 1 else "single GPU",
+        "parallelism": (f"student-parallel x{world}, logit reduce: {args.reduce}") if world > 1 else "single GPU",
         "l2": "flushed before every timed request: 256 MiB write + 256 MiB read (> 126 MB L2)",
         "launch": ("CUDA-graph replay per request (16-token bucket graph; 2 device-to-device input copies "
                    "+ 1 graph launch, inside the timed region"
@@ -348,7 +351,8 @@ def run_engine(args):
     dev = torch.device("cuda", local_rank)
     B = args.batch
     grp = ShardedStudentGroup(cfg, K, seed=args.seed, rank=rank, world=world, device=local_rank,
-                              max_tokens=args.len_max * B, max_seqs=B)
+                              max_tokens=args.len_max * B, max_seqs=B,
+                              reduce=args.reduce if (world > 1 and not one_device) else "nccl")
     n_steps = args.steps + args.warmup
     reqs = make_requests(n_steps * B, args.seed, args.len_min, args.len_max, cfg.vocab)
     # one step = B requests packed back to back (no padding); inputs resident in HBM before timing

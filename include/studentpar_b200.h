@@ -194,6 +194,28 @@ int sp_group_set_profiling(sp_group* group, int enable);
  * launches recorded (or a negative sp_status). */
 int sp_group_profile_read(sp_group* group, sp_launch_record* out, int max_records);
 
+/* Device-side logit reduce of a sharded group (replaces the NCCL reduce of partial logits):
+ * a mailbox on the ROOT rank's GPU (sp_reduce_mailbox_bytes, zero-initialised device memory,
+ * mapped into the other ranks' processes with the IPC calls below); every rank publishes its
+ * partial logits f32 [n_rows][C] for request `seq` (1, 2, ...: the same on every rank, strictly
+ * increasing) into its slot and raises its flag; the root's combine waits for all `world` flags of
+ * `seq`, sums the slots in rank order (+ bias once, if non-NULL) into `out` (device or host-mapped
+ * memory) and, if `out_flag` is set (host-mapped int), then writes seq there. Asynchronous on
+ * `stream`; at most 4 requests in flight per mailbox (a publisher waits for the root to consume
+ * request seq - 4). */
+long long sp_reduce_mailbox_bytes(int32_t world, int32_t max_rows, int32_t n_classes);
+/* Allocate (zeroed, its own cudaMalloc so IPC maps it whole) / free a mailbox on `device`. */
+int sp_mailbox_create(int32_t world, int32_t max_rows, int32_t n_classes, int32_t device, void** mailbox_out);
+int sp_mailbox_destroy(void* mailbox);
+int sp_reduce_publish(void* mailbox, const float* partial, int32_t rank, int32_t world, int32_t n_rows,
+                      int32_t max_rows, int32_t n_classes, int64_t seq, void* stream);
+int sp_reduce_combine(void* mailbox, int32_t world, int32_t n_rows, int32_t max_rows, int32_t n_classes, int64_t seq,
+                      const float* bias, float* out, int32_t* out_flag, void* stream);
+/* CUDA IPC of a device allocation (64-byte handle), to map the root's mailbox in peer processes. */
+int sp_ipc_get_handle(const void* dev_ptr, void* handle_out);
+int sp_ipc_open_handle(const void* handle, void** dev_ptr_out);
+int sp_ipc_close_handle(void* dev_ptr);
+
 /* Op-level entry points (single kernels, used by the per-kernel parity tests).
  * GEMM: x / x_lo fp16 [x_rows_total][k_dim] operand terms (x_lo may be NULL); fp16 output with
  * out_lo != NULL is written as an (hi, lo) pair. Attention: ctx / ctx_lo the (hi, lo) context. */

@@ -99,6 +99,20 @@ SIGNATURES: dict[str, tuple] = {
     "sp_debug_set_gemm_trace": (C.c_int, [C.c_void_p]),
     "sp_debug_set_attn_trace": (C.c_int, [C.c_void_p]),
     "sp_debug_gemm_trace_launches": (C.c_int, [C.c_void_p, C.c_int32]),
+    "sp_reduce_mailbox_bytes": (C.c_longlong, [C.c_int32, C.c_int32, C.c_int32]),
+    "sp_reduce_publish": (
+        C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int64, C.c_void_p]
+    ),
+    "sp_reduce_combine": (
+        C.c_int,
+        [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p,
+         C.c_void_p],
+    ),
+    "sp_mailbox_create": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_void_p)]),
+    "sp_mailbox_destroy": (C.c_int, [C.c_void_p]),
+    "sp_ipc_get_handle": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "sp_ipc_open_handle": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
+    "sp_ipc_close_handle": (C.c_int, [C.c_void_p]),
     "sp_op_attention": (
         C.c_int,
         [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,

@@ -9,6 +9,9 @@
 
 namespace sp {
 
+// Record the message sp_last_error() returns and pass the status code through (sp_runtime.cu).
+int report_error(int code, const char* msg);
+
 // Launch with programmatic stream serialization: the kernel may start while its predecessor in
 // the stream finishes; every kernel of this library calls griddepcontrol.wait before touching
 // data the predecessor produces (and only prefetches read-only weights before that).

@@ -112,6 +112,10 @@ constexpr int kMaxSplits = 4;
 
 }  // namespace
 
+namespace sp {
+int report_error(int code, const char* msg) { return fail(code, "%s", msg); }
+}  // namespace sp
+
 struct sp_group {
   sp_config cfg;
   sp_weights w;
@@ -131,7 +135,7 @@ struct sp_group {
   half* ctxc = nullptr;    // [2][S][B][H] CLS-query attention context (O operand)
   half* ffnc = nullptr;    // [2][S][B][F] GELU output of the CLS rows (FFN2 operand)
   float* partc = nullptr;  // [kMaxSplits][S][B][H] split-K partials of the CLS-row projections
-  half* qc = nullptr;      // [S][B][H] last-layer query of the CLS rows
+  half* qc = nullptr;      // [S][B][H] last-layer query of the CLS rows (long requests)
   long long x_lo = 0, ctx_lo = 0, ffn_lo = 0, cls_lo = 0, cf_lo = 0;  // cf_lo: lo offset of ffnc
   float* final32 = nullptr;  // [kMaxSplits][S][rows_cap][H] per-student final representation / pooler partials
   int32_t* d_ids = nullptr;  // staging block [cu_pad | ids]: d_cu = block, d_ids = block + cu_pad
@@ -341,6 +345,7 @@ int sp_group_create(const sp_config* cfg, const sp_weights* weights, int device,
     if ((rc = dev_alloc(g, &g->ffnc, 2 * S * B * F))) return bail(rc);
     if ((rc = dev_alloc(g, &g->partc, (size_t)kMaxSplits * S * B * H))) return bail(rc);
     if ((rc = dev_alloc(g, &g->qc, S * B * H))) return bail(rc);
+
     const auto* wq = static_cast<const half*>(w.w_qkv);
     const auto* wo = static_cast<const half*>(w.w_o);
     const auto* w1 = static_cast<const half*>(w.w_ffn1);
@@ -603,6 +608,7 @@ int bert_forward(sp_group* g, const int32_t* ids, const int32_t* cu, int n_seqs,
     const int s_oc = choose_splits(k * (H / 128) * n_tiles_c, H / 64, kMaxSplits);
     const int s_fc = choose_splits(k * (H / 128) * n_tiles_c, F / 64, kMaxSplits);
     const double GBH = (double)k * n_seqs * H;
+    const bool split_q = c.n_layers > 1 && n_tokens >= 256;
     // one LayerNorm launch (rows of k students)
     auto layer_norm = [&](const float* part, int splits, long long pss, long long pgs, const float* b_, const float* g_,
                           const float* be_, const float* x_in, long long in_gs, const int* in_rows, float* x_out,
@@ -640,9 +646,10 @@ int bert_forward(sp_group* g, const int32_t* ids, const int32_t* cu, int n_seqs,
     for (int l = 0; l < c.n_layers; ++l) {
       const size_t lS = (size_t)l * S;
       const bool last = (l == c.n_layers - 1);
-      if (last && l > 0) {
-        // last layer: K and V of every token (weight rows [H, 3H) of each student's QKV slab), the
-        // query of the CLS rows only (rows [0, H) on the CLS copies the previous LayerNorm wrote)
+      if (split_q && last) {
+        // long requests, last layer: K and V of every token (weight rows [H, 3H) of each student's
+        // QKV slab), the query of the CLS rows only (rows [0, H) on the CLS copies the previous
+        // LayerNorm wrote): -12 us at L = 512 (measured); below 256 tokens the extra launch costs more
         run_gemm(g, SP_LAUNCH_GEMM_QKV, g->m_qkv[l], g->xm_x16, k, 2 * H, H, n_tokens, T, w.b_qkv + lS * 3 * H + H,
                  3 * H, sp::ACT_NONE, g->qkv + H, (long long)T * 3 * H, 0, 0, 1, 0, st, t_dev, 3 * H, 3 * H, H);
         run_gemm(g, SP_LAUNCH_GEMM_QKV, g->m_qkv[l], g->xm_cls, k, H, H, n_seqs, B, w.b_qkv + lS * 3 * H, 3 * H,
@@ -658,7 +665,7 @@ int bert_forward(sp_group* g, const int32_t* ids, const int32_t* cu, int n_seqs,
         // the sequence's keys, then O, LayerNorm-1, FFN and LayerNorm-2 on the CLS rows alone
         // (n_seqs rows per student; the residual input is gathered at cu_seqlens[b]).
         g->rec_begin(SP_LAUNCH_ATTENTION, GTH * 4.0, 4.0 * k * H * (double)n_tokens);
-        sp::launch_attention_cls(g->qkv, (long long)T * 3 * H, l > 0 ? g->qc : nullptr, bgs, cu, n_seqs, k,
+        sp::launch_attention_cls(g->qkv, (long long)T * 3 * H, split_q ? g->qc : nullptr, bgs, cu, n_seqs, k,
                                  c.n_heads, H / c.n_heads, H, g->ctxc, bgs, g->cls_lo, max_len, st);
         g->rec_end();
         run_gemm(g, SP_LAUNCH_GEMM_O, g->m_o[l], g->xm_ctxc, k, H, H, n_seqs, B, nullptr, H, sp::ACT_NONE, g->partc,
@@ -704,7 +711,7 @@ int bert_forward(sp_group* g, const int32_t* ids, const int32_t* cu, int n_seqs,
       }
       layer_norm(g->part, s_ln2, part_ss, xgs, w.b_ffn2 + lS * H, w.ln2_gamma + lS * H, w.ln2_beta + lS * H, g->x32,
                  xgs, nullptr, g->x32, xgs, g->x16, xgs, g->x_lo, n_rows_arg, GTH,
-                 l == c.n_layers - 2 ? g->cls16 : nullptr);
+                 split_q && l == c.n_layers - 2 ? g->cls16 : nullptr);
     }
     // pooler on the CLS rows: tanh(W_p h_CLS + b_p). Few rows: split-K partials (more CTAs stream the
     // pooler weights), finished by the head kernel; many rows: one pass with the tanh epilogue.

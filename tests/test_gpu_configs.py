@@ -195,3 +195,37 @@ def test_sharded_partials_sum_to_group_logits():
             np.testing.assert_allclose(parts_dev[0] + parts_dev[1], want, rtol=0, atol=1e-5)
             if k == 1:
                 assert not parts_dev[1].any() and not parts_host[1].any()
+
+
+def test_p2p_mailbox_reduce_two_shards_matches_group():
+    """Device-side logit reduce (sp_reduce.cu): two shards of one group in this process share the
+    root's mailbox; rank 1 publishes its partial logits, rank 0 publishes and combines in rank order.
+    The root's logits equal the whole group's (device path with graphs, eager batched path, and the
+    host path through mapped memory without a stream sync), for prefixes that leave rank 1 empty."""
+    import torch
+    from paper_2408_12526_b200 import PRESETS, StudentGroup, random_bert_group
+    from paper_2408_12526_b200.parallel import ShardedStudentGroup
+
+    cfg, K = PRESETS["tiny"]
+    root = ShardedStudentGroup(cfg, K, seed=7, rank=0, world=2, max_tokens=256, max_seqs=4, reduce="p2p")
+    peer = ShardedStudentGroup(cfg, K, seed=7, rank=1, world=2, max_tokens=256, max_seqs=4, reduce="p2p",
+                               mailbox=root.mailbox)
+    ref = StudentGroup(random_bert_group(cfg, K, seed=7), max_tokens=256, max_seqs=4)
+    rng = np.random.default_rng(5)
+    for rep in range(3):  # more requests than mailbox banks
+        for lens in ([9], [16], [40], [5, 60, 33]):
+            seqs = _seqs(rng, lens)
+            ids = np.concatenate(seqs)
+            cu = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+            d_ids, d_cu = torch.from_numpy(ids).cuda(), torch.from_numpy(cu).cuda()
+            for k in (1, 3, K):
+                want = ref.forward_host(ids, cu, k)
+                out = torch.full((4, 2), float("nan"), device="cuda")
+                junk = torch.zeros((4, 2), device="cuda")
+                peer.forward_packed_device(d_ids, d_cu, len(lens), len(ids), max(lens), k, junk)
+                root.forward_packed_device(d_ids, d_cu, len(lens), len(ids), max(lens), k, out)
+                np.testing.assert_allclose(out[: len(lens)].cpu().numpy(), want, rtol=0, atol=1e-5)
+                assert peer.forward_host(ids, cu, k) is None
+                z = root.forward_host(ids, cu, k)
+                np.testing.assert_allclose(z, want, rtol=0, atol=1e-5)
+    assert root._seq == peer._seq

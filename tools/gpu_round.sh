@@ -1,6 +1,11 @@
+# full GPU pass (run under gpurun): tests, smoke, bench (driver-sized + long), reference arm,
+# bursty serving, length probe; logs under gpurun_out/<prefix>_*
 set -x
-timeout 900 python -m pytest tests -m gpu -q --timeout 600 2>&1 | tail -15
-timeout 600 python bench.py > gpurun_out/bench_r1.json 2> gpurun_out/bench_r1.err; echo "bench rc=$?"; tail -3 gpurun_out/bench_r1.err
-B="python bench.py --steps 20 --warmup 3 --no-cpu-baseline --profile-steps 2"
-timeout 300 $B > gpurun_out/plain.log 2>&1 && timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -s 60 -c 200 --csv --log-file gpurun_out/launches.csv $B > gpurun_out/ncu.log 2>&1; echo "ncu1 rc=$?"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:gemm_kernel -s 30 -c 4 -o gpurun_out/prof_gemm $B > gpurun_out/ncu2.log 2>&1; echo "ncu2 rc=$?"
+P=${1:-g}
+timeout 300 python __graft_entry__.py smoke > gpurun_out/${P}_smoke.log 2>&1; echo "smoke rc=$?"; tail -1 gpurun_out/${P}_smoke.log
+timeout 1500 python -m pytest tests -m gpu -q --timeout 900 -p no:cacheprovider > gpurun_out/${P}_tests.log 2>&1; echo "tests rc=$?"; tail -4 gpurun_out/${P}_tests.log
+timeout 600 python bench.py --steps 20 --warmup 5 > gpurun_out/${P}_bench20.json 2> gpurun_out/${P}_bench20.err; echo "bench20 rc=$?"
+timeout 900 python bench.py --steps 500 --warmup 20 --no-cpu-baseline > gpurun_out/${P}_bench500.json 2> gpurun_out/${P}_bench500.err; echo "bench500 rc=$?"
+timeout 600 python bench.py --impl reference --steps 5 --warmup 1 > gpurun_out/${P}_ref.json 2> gpurun_out/${P}_ref.err; echo "ref rc=$?"
+timeout 900 python tools/serve_bursty.py --out gpurun_out/${P}_serve.json > gpurun_out/${P}_serve.log 2>&1; echo "serve rc=$?"; tail -3 gpurun_out/${P}_serve.log
+timeout 600 python tools/len_probe.py 16,32,64,96,128,160,192,256,320,384,448,512 > gpurun_out/${P}_len.txt 2>&1; cat gpurun_out/${P}_len.txt

@@ -9,7 +9,7 @@ lib = _lib.load()
 fw = torch.empty(256 << 18, device="cuda"); fr = torch.ones(256 << 18, device="cuda")
 logits = torch.empty(1, 2, device="cuda")
 tr = torch.zeros(8 * 20000, dtype=torch.int64, device="cuda")
-names = ["qkv", "o", "ffn1", "ffn2"] * 2 + ["pool"]  # (per-L order of GEMM launches)
+names = ["qkv", "o", "ffn1", "ffn2", "kv", "q_cls", "o_cls", "ffn1c", "ffn2c", "pool"]  # GEMM launches in order (<= 128 tokens)
 for L in [int(x) for x in sys.argv[1].split(",")]:
     ids = torch.randint(1000, 30000, (L,), dtype=torch.int32, device="cuda")
     cu = torch.tensor([0, L], dtype=torch.int32, device="cuda")
