@@ -572,10 +572,11 @@ static void launch_persistent_t(const GemmMaps& maps, const GemmParams& p, int g
   else cudaLaunchKernelEx(&cfg, gemm_persistent_kernel<ACT, OUT_F32, false>, maps, q);
 }
 
-// CTA pairs (cta_group::2) halve each CTA's token-tile traffic: from 1024 tokens (batched load;
-// measured slower than single-CTA tiles below that).
+// CTA pairs (cta_group::2) halve each CTA's token-tile traffic (both (hi, lo) terms): from 256 tokens
+// (batch-1 L = 448 / 512: 227 / 237 us against 249 / 258 with single-CTA tiles and the fused MLP;
+// equal at 256-384; mixed below: profiles/r2_pair_threshold.txt).
 bool gemm_persistent_pair(int t_rows, int m_tiles, int groups) {
-  return t_rows >= 1024 && m_tiles % 2 == 0 && groups * m_tiles >= 4;
+  return t_rows >= 256 && m_tiles % 2 == 0 && groups * m_tiles >= 4;
 }
 
 // Tile policy of the persistent path: pick the token-tile count that minimises the makespan
