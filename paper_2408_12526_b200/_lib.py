@@ -9,7 +9,7 @@ import ctypes as C
 import threading
 from pathlib import Path
 
-from .build import LIB_PATH
+from .build import LIB_PATH, TORCH_LIB_PATH
 
 SP_OK, SP_EINVAL, SP_ECUDA, SP_ENOMEM = 0, 1, 2, 3
 SP_KIND_DENSE, SP_KIND_BERT = 0, 1

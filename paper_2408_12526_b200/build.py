@@ -21,6 +21,7 @@ OUT_DIR = PKG / "_lib"
 OBJ_DIR = OUT_DIR / "obj"
 LIB_NAME = "libstudentpar_b200.so"
 LIB_PATH = OUT_DIR / LIB_NAME
+TORCH_LIB_PATH = OUT_DIR / "libstudentpar_torch.so"  # torch.ops.studentpar (sp_torch.cpp)
 
 ARCH_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr"]
@@ -46,6 +47,35 @@ def _stale(target: Path, deps: list[Path]) -> bool:
         return True
     t = target.stat().st_mtime
     return any(d.stat().st_mtime > t for d in deps)
+
+
+def _torch_flags() -> tuple[list[str], list[str]]:
+    import torch
+    from torch.utils import cpp_extension as ce
+
+    abi = int(torch._C._GLIBCXX_USE_CXX11_ABI)
+    cuda_inc = str(Path(_nvcc()).resolve().parent.parent / "include")
+    cflags = [f"-D_GLIBCXX_USE_CXX11_ABI={abi}", "-I", cuda_inc] + [f for p in ce.include_paths() for f in ("-I", p)]
+    libdir = ce.library_paths()[0]
+    ldflags = ["-L", libdir, "-Wl,-rpath," + libdir, "-lc10", "-lc10_cuda", "-ltorch_cpu", "-ltorch_cuda",
+               "-L", str(OUT_DIR), "-Wl,-rpath,$ORIGIN", "-lstudentpar_b200"]
+    return cflags, ldflags
+
+
+def build_torch_ops(force: bool = False) -> Path:
+    """The thin PyTorch C++ extension (csrc/sp_torch.cpp) over the C ABI -> _lib/libstudentpar_torch.so."""
+    src = CSRC / "sp_torch.cpp"
+    if not force and not _stale(TORCH_LIB_PATH, [src, LIB_PATH] + sorted(INCLUDE.glob("*.h"))):
+        return TORCH_LIB_PATH
+    cflags, ldflags = _torch_flags()
+    tmp = TORCH_LIB_PATH.with_suffix(".so.tmp")
+    cmd = [shutil.which("g++") or "g++", "-O2", "-std=c++17", "-shared", "-fPIC", *cflags, str(src), "-o", str(tmp),
+           *ldflags]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"g++ failed:\n{' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
+    os.replace(tmp, TORCH_LIB_PATH)
+    return TORCH_LIB_PATH
 
 
 def build(force: bool = False, verbose: bool = False) -> Path:
@@ -77,6 +107,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         cmd = [nvcc, *ARCH_FLAGS, "-shared", "-o", str(tmp), *map(str, objs)]
         run(cmd)
         os.replace(tmp, LIB_PATH)
+    build_torch_ops(force)
     return LIB_PATH
 
 

@@ -21,14 +21,21 @@ namespace {
 constexpr int kClsThreads = 128;
 }
 
-template <int D>
+// Keys and values of the (student, sequence, head) staged in shared memory with one burst of
+// 16-byte cp.async copies right after the dependency wait (one global round trip instead of one per
+// phase); up to kClsSmemRows keys (longer sequences stream K / V from global memory).
+constexpr int kClsSmemRows = 512;
+
+template <int D, bool SMEM>
 __global__ void __launch_bounds__(kClsThreads)
     attn_cls_kernel(const half* __restrict__ qkv, long long qkv_gs, const half* __restrict__ qs, long long q_gs,
                     const int* __restrict__ cu, int n_heads, int hidden, half* __restrict__ ctx, long long ctx_gs,
                     long long lo_off, float scale) {
-  extern __shared__ float sc[];  // [L] scores -> probabilities
+  extern __shared__ __align__(16) uint8_t cls_smem[];
   __shared__ float red[4][D];
   __shared__ float stat[8];
+  __shared__ __align__(16) half qsm[D];
+  __shared__ __align__(16) float qf[D];
   pdl_launch_dependents();
   const int gh = blockIdx.x;
   const int g = gh / n_heads, h = gh % n_heads;
@@ -39,35 +46,47 @@ __global__ void __launch_bounds__(kClsThreads)
   const long long row3 = 3LL * hidden;
   const half* base = qkv + (long long)g * qkv_gs + (long long)c0 * row3 + h * D;
   const half* qrow = qs ? qs + (long long)g * q_gs + (long long)b * hidden + h * D : base;
+  constexpr int CH = D / 8;  // 16-byte chunks per row
+  half* Ks = reinterpret_cast<half*>(cls_smem);                    // [L][D]
+  half* Vs = Ks + (SMEM ? (size_t)kClsSmemRows * D : 0);           // [L][D]
+  float* sc = reinterpret_cast<float*>(Vs + (SMEM ? (size_t)kClsSmemRows * D : 0));  // [L] scores
   pdl_wait();
-  // q of the CLS row (fp32, every thread a full copy through registers)
-  float q[D];
-#pragma unroll
-  for (int v = 0; v < D / 8; ++v) {
-    const uint4 u = *reinterpret_cast<const uint4*>(qrow + v * 8);
-    const __half2* hp = reinterpret_cast<const __half2*>(&u);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const float2 f = __half22float2(hp[i]);
-      q[v * 8 + 2 * i] = f.x * scale;
-      q[v * 8 + 2 * i + 1] = f.y * scale;
+  if (tid < CH) cp_async16(qsm + tid * 8, qrow + tid * 8, 16);
+  if constexpr (SMEM) {
+    for (int i = tid; i < L * CH; i += kClsThreads) {
+      const int r = i / CH, c = i - r * CH;
+      cp_async16(Ks + r * D + c * 8, base + (long long)r * row3 + hidden + c * 8, 16);
+      cp_async16(Vs + r * D + c * 8, base + (long long)r * row3 + 2 * hidden + c * 8, 16);
     }
   }
-  // 1. scores, one thread per key
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+  // q of the CLS row (fp32, scaled) in shared memory: lanes read it at their key's chunk
+  if (tid < D) qf[tid] = __half2float(qsm[tid]) * scale;
+  __syncthreads();
+  // 1. scores, one thread per key (chunks read in a rotated order: no shared-memory bank conflicts)
   float mx = -INFINITY;
   for (int j = tid; j < L; j += kClsThreads) {
-    const half* kr = base + (long long)j * row3 + hidden;
     float s = 0.f;
 #pragma unroll
-    for (int v = 0; v < D / 8; ++v) {
-      const uint4 u = *reinterpret_cast<const uint4*>(kr + v * 8);
+    for (int cc = 0; cc < CH; ++cc) {
+      const int c = (cc + j) & (CH - 1);
+      const uint4 u = SMEM ? *reinterpret_cast<const uint4*>(Ks + j * D + c * 8)
+                           : *reinterpret_cast<const uint4*>(base + (long long)j * row3 + hidden + c * 8);
       const __half2* hp = reinterpret_cast<const __half2*>(&u);
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const float2 f = __half22float2(hp[i]);
-        s = fmaf(q[v * 8 + 2 * i], f.x, s);
-        s = fmaf(q[v * 8 + 2 * i + 1], f.y, s);
-      }
+      const float4 qa = *reinterpret_cast<const float4*>(qf + c * 8);
+      const float4 qb = *reinterpret_cast<const float4*>(qf + c * 8 + 4);
+      const float2 f0 = __half22float2(hp[0]), f1 = __half22float2(hp[1]);
+      const float2 f2 = __half22float2(hp[2]), f3 = __half22float2(hp[3]);
+      s = fmaf(qa.x, f0.x, s);
+      s = fmaf(qa.y, f0.y, s);
+      s = fmaf(qa.z, f1.x, s);
+      s = fmaf(qa.w, f1.y, s);
+      s = fmaf(qb.x, f2.x, s);
+      s = fmaf(qb.y, f2.y, s);
+      s = fmaf(qb.z, f3.x, s);
+      s = fmaf(qb.w, f3.y, s);
     }
     sc[j] = s;
     mx = fmaxf(mx, s);
@@ -95,7 +114,9 @@ __global__ void __launch_bounds__(kClsThreads)
   for (int u = 0; u < 4; ++u)
 #pragma unroll
     for (int d = 0; d < DPL; ++d) acc[u][d] = 0.f;
-  const half* vb = base + 2 * hidden + lane * DPL;
+  auto vrow = [&](int jj) -> const half* {
+    return SMEM ? Vs + jj * D + lane * DPL : base + (long long)jj * row3 + 2 * hidden + lane * DPL;
+  };
   int j = warp;
   for (; j + 12 < L; j += 16) {  // four independent keys per iteration
 #pragma unroll
@@ -103,22 +124,22 @@ __global__ void __launch_bounds__(kClsThreads)
       const int jj = j + 4 * u;
       const float p = sc[jj];
       if constexpr (DPL == 2) {
-        const float2 f = __half22float2(*reinterpret_cast<const __half2*>(vb + (long long)jj * row3));
+        const float2 f = __half22float2(*reinterpret_cast<const __half2*>(vrow(jj)));
         acc[u][0] = fmaf(p, f.x, acc[u][0]);
         acc[u][1] = fmaf(p, f.y, acc[u][1]);
       } else {
-        acc[u][0] = fmaf(p, __half2float(vb[(long long)jj * row3]), acc[u][0]);
+        acc[u][0] = fmaf(p, __half2float(*vrow(jj)), acc[u][0]);
       }
     }
   }
   for (; j < L; j += 4) {
     const float p = sc[j];
     if constexpr (DPL == 2) {
-      const float2 f = __half22float2(*reinterpret_cast<const __half2*>(vb + (long long)j * row3));
+      const float2 f = __half22float2(*reinterpret_cast<const __half2*>(vrow(j)));
       acc[0][0] = fmaf(p, f.x, acc[0][0]);
       acc[0][1] = fmaf(p, f.y, acc[0][1]);
     } else {
-      acc[0][0] = fmaf(p, __half2float(vb[(long long)j * row3]), acc[0][0]);
+      acc[0][0] = fmaf(p, __half2float(*vrow(j)), acc[0][0]);
     }
   }
 #pragma unroll
@@ -136,21 +157,43 @@ __global__ void __launch_bounds__(kClsThreads)
   }
 }
 
+template <int D, bool SMEM>
+static void launch_cls_t(dim3 grid, size_t smem, cudaStream_t stream, const half* qkv, long long qkv_gs, const half* q,
+                         long long q_gs, const int* cu, int n_heads, int hidden, half* ctx, long long ctx_gs,
+                         long long lo_off, float scale) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(attn_cls_kernel<D, SMEM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(2 * (size_t)kClsSmemRows * 64 * 2 + 4 * 8192));
+    attr = true;
+  }
+  launch_pdl(attn_cls_kernel<D, SMEM>, grid, dim3(kClsThreads), smem, stream, qkv, qkv_gs, q, q_gs, cu, n_heads, hidden,
+             ctx, ctx_gs, lo_off, scale);
+}
+
 void launch_attention_cls(const half* qkv, long long qkv_gs, const half* q, long long q_gs, const int* cu_seqlens,
                           int n_seqs, int groups, int n_heads, int head_dim, int hidden, half* ctx, long long ctx_gs,
                           long long lo_off, int max_len, cudaStream_t stream) {
   if (n_seqs <= 0 || groups <= 0) return;
   const float scale = 1.0f / sqrtf(static_cast<float>(head_dim));
-  const size_t smem = sizeof(float) * (size_t)max_len;
+  const bool in_smem = max_len <= kClsSmemRows;
+  const size_t smem = in_smem ? 2 * (size_t)kClsSmemRows * head_dim * 2 + sizeof(float) * kClsSmemRows
+                              : sizeof(float) * (size_t)max_len;
   dim3 grid(groups * n_heads, n_seqs);
   if (head_dim == 64) {
-    if (smem > 48 * 1024) cudaFuncSetAttribute(attn_cls_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    launch_pdl(attn_cls_kernel<64>, grid, dim3(kClsThreads), smem, stream, qkv, qkv_gs, q, q_gs, cu_seqlens, n_heads,
-               hidden, ctx, ctx_gs, lo_off, scale);
+    if (in_smem)
+      launch_cls_t<64, true>(grid, smem, stream, qkv, qkv_gs, q, q_gs, cu_seqlens, n_heads, hidden, ctx, ctx_gs, lo_off,
+                             scale);
+    else
+      launch_cls_t<64, false>(grid, smem, stream, qkv, qkv_gs, q, q_gs, cu_seqlens, n_heads, hidden, ctx, ctx_gs,
+                              lo_off, scale);
   } else {
-    if (smem > 48 * 1024) cudaFuncSetAttribute(attn_cls_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    launch_pdl(attn_cls_kernel<32>, grid, dim3(kClsThreads), smem, stream, qkv, qkv_gs, q, q_gs, cu_seqlens, n_heads,
-               hidden, ctx, ctx_gs, lo_off, scale);
+    if (in_smem)
+      launch_cls_t<32, true>(grid, smem, stream, qkv, qkv_gs, q, q_gs, cu_seqlens, n_heads, hidden, ctx, ctx_gs, lo_off,
+                             scale);
+    else
+      launch_cls_t<32, false>(grid, smem, stream, qkv, qkv_gs, q, q_gs, cu_seqlens, n_heads, hidden, ctx, ctx_gs,
+                              lo_off, scale);
   }
 }
 

@@ -29,6 +29,22 @@ from . import _lib
 from .weights import BertGroupWeights, DenseGroupWeights, dense_group_from_ensemble
 
 
+_TORCH_OPS = None
+
+
+def torch_ops():
+    """torch.ops.studentpar — the thin PyTorch C++ extension over the C ABI (csrc/sp_torch.cpp), or
+    None if its library was not built (the ctypes binding of the same entry points is used then)."""
+    global _TORCH_OPS
+    if _TORCH_OPS is None:
+        try:
+            torch.ops.load_library(str(_lib.TORCH_LIB_PATH))
+            _TORCH_OPS = torch.ops.studentpar
+        except (OSError, RuntimeError):
+            _TORCH_OPS = False
+    return _TORCH_OPS or None
+
+
 def _dev_tensor(a: np.ndarray, device: torch.device) -> torch.Tensor:
     return torch.from_numpy(np.ascontiguousarray(a)).to(device)
 
@@ -219,6 +235,10 @@ class StudentGroup:
                               k_local: int, rep: torch.Tensor | None, logits: torch.Tensor, add_bias: bool = True,
                               stream: torch.cuda.Stream | None = None) -> None:
         """BERT kind on device buffers (no host sync). ``logits`` f32 [n_seqs, C] is written."""
+        ops = torch_ops()
+        if ops is not None and rep is None and stream is None:  # torch's current stream, checked tensors
+            ops.group_forward(self._handle.value, ids, cu, n_seqs, n_tokens, max_len, k_local, logits, add_bias)
+            return
         _lib.check(self._lib.sp_group_forward(self._handle, ids.data_ptr(), cu.data_ptr(), n_seqs, n_tokens, max_len,
                                               k_local, _ptr(rep), logits.data_ptr(), int(add_bias),
                                               _stream_handle(stream, self.device)))
@@ -227,6 +247,10 @@ class StudentGroup:
                              logits: torch.Tensor, add_bias: bool = True,
                              stream: torch.cuda.Stream | None = None) -> None:
         """One sequence on device buffers, replayed as its 16-token bucket's CUDA graph (no host sync)."""
+        ops = torch_ops()
+        if ops is not None and stream is None:
+            ops.group_forward_graph(self._handle.value, ids, cu, n_tokens, k_local, logits, add_bias)
+            return
         _lib.check(self._lib.sp_group_forward_graph(self._handle, ids.data_ptr(), cu.data_ptr(), n_tokens, k_local,
                                                     logits.data_ptr(), int(add_bias),
                                                     _stream_handle(stream, self.device)))
@@ -343,9 +367,19 @@ class StudentGroup:
         ids = np.ascontiguousarray(ids, dtype=np.int32)
         cu = np.ascontiguousarray(cu, dtype=np.int32)
         n = len(cu) - 1
+        if n < 1:
+            raise ValueError("cu_seqlens must describe at least one sequence")
         if out is None:
             out = np.empty((n, self.n_classes), np.float32)
+        elif (out.dtype != np.float32 or not out.flags.c_contiguous or out.ndim != 2
+              or out.shape[0] < n or out.shape[1] != self.n_classes):
+            raise ValueError(f"out must be a C-contiguous float32 array of shape (>= {n}, {self.n_classes})")
         kl = self.local_k(k)
+        ops = torch_ops()
+        if ops is not None and stream is None:  # the PyTorch C++ extension: torch's current stream
+            ops.group_forward_host(self._handle.value, torch.from_numpy(ids), torch.from_numpy(cu), kl,
+                                   torch.from_numpy(out), add_bias, self.device.index)
+            return out
         _lib.check(self._lib.sp_group_forward_host(self._handle, ids.ctypes.data, cu.ctypes.data, n, len(ids), kl,
                                                    out.ctypes.data, int(add_bias),
                                                    _stream_handle(stream, self.device)))

@@ -58,3 +58,23 @@ def test_engine_refuses_cpu_fallback():
 
     with pytest.raises(RuntimeError, match="no CPU fallback"):
         StudentGroup(random_dense_group(8, 16, 2, 2))
+
+
+def test_torch_extension_registers_the_ops():
+    """The thin PyTorch C++ extension (csrc/sp_torch.cpp) loads without a GPU and registers
+    torch.ops.studentpar.{group_forward, group_forward_graph, group_forward_host}; a null handle is
+    rejected before any CUDA call."""
+    import torch
+
+    from paper_2408_12526_b200.build import TORCH_LIB_PATH, build
+    from paper_2408_12526_b200.group import torch_ops
+
+    if not TORCH_LIB_PATH.exists():
+        build()
+    ops = torch_ops()
+    assert ops is not None
+    for name in ("group_forward", "group_forward_graph", "group_forward_host"):
+        assert hasattr(ops, name)
+    with pytest.raises(RuntimeError, match="null group handle"):
+        ops.group_forward_host(0, torch.zeros(1, dtype=torch.int32), torch.tensor([0, 1], dtype=torch.int32), 1,
+                               torch.zeros(1, 2), True, 0)

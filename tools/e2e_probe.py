@@ -39,3 +39,10 @@ print(f"raw sp_group_forward_host {timeit(lambda: lib.sp_group_forward_host(*arg
 print(f"local_k                   {timeit(lambda: g.local_k(K)):7.1f} us")
 print(f"stream handle             {timeit(lambda: torch.cuda.current_stream().cuda_stream):7.1f} us")
 print(f"torch sync (idle)         {timeit(lambda: torch.cuda.synchronize()):7.1f} us")
+# the same call through the PyTorch C++ extension (torch.ops.studentpar.group_forward_host)
+from paper_2408_12526_b200 import _lib as _L2
+torch.ops.load_library(str(_L2.TORCH_LIB_PATH))
+ids_t, cu_t, out_t = torch.from_numpy(ids), torch.from_numpy(cu), torch.from_numpy(out)
+op = torch.ops.studentpar.group_forward_host
+print(f"torch op forward_host     {timeit(lambda: op(h.value, ids_t, cu_t, K, out_t, True, 0)):7.1f} us")
+print(f"torch op (from numpy)     {timeit(lambda: op(h.value, torch.from_numpy(ids), torch.from_numpy(cu), K, torch.from_numpy(out), True, 0)):7.1f} us")
