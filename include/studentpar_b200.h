@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define SP_ABI_VERSION 2
+#define SP_ABI_VERSION 3
 
 enum sp_status {
   SP_OK = 0,
@@ -100,6 +100,12 @@ typedef struct sp_weights {
   const float* alpha;         /* f32 [S]     boosting multipliers of the local students */
   const float* w_cls;         /* f32 [C][H]  shared classifier (identity activation, distill.py:535) */
   const float* b_cls;         /* f32 [C] */
+  /* dense kind, optional (ABI v3): the fp16 lo terms W - fp16(W) of weights whose source is wider
+   * than fp16 (the reference trains in float64). With them every dense projection runs as
+   * (W_hi + W_lo)(x_hi + x_lo) minus the lo x lo term — ~22-bit operands on the tensor cores.
+   * NULL = the fp16 weights are exact. Same shapes as w_in / w_layers. */
+  const void* w_in_lo;
+  const void* w_layers_lo;
 } sp_weights;
 
 typedef struct sp_group sp_group;

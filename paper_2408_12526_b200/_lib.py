@@ -13,7 +13,7 @@ from .build import LIB_PATH, TORCH_LIB_PATH
 
 SP_OK, SP_EINVAL, SP_ECUDA, SP_ENOMEM = 0, 1, 2, 3
 SP_KIND_DENSE, SP_KIND_BERT = 0, 1
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 
 class SpConfig(C.Structure):
@@ -41,6 +41,7 @@ _WEIGHT_FIELDS = [
     "w_pool", "b_pool",
     "w_in", "b_in", "w_layers", "b_layers",
     "alpha", "w_cls", "b_cls",
+    "w_in_lo", "w_layers_lo",  # ABI v3: dense weight lo terms (optional)
 ]
 
 

@@ -87,7 +87,8 @@ __global__ void __launch_bounds__(kThreads, 2)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int x_bytes = p.bn * 128;                            // one term of the token tile
-  const int stage_bytes = kATileBytes + x_bytes * (p.hilo ? 2 : 1);
+  const int a_bytes = kATileBytes * (p.whilo ? 2 : 1);       // weight tile (+ its lo term)
+  const int stage_bytes = a_bytes + x_bytes * (p.hilo ? 2 : 1);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.stages * stage_bytes);
   uint64_t* empty = full + p.stages;
   uint64_t* tmem_full = empty + p.stages;
@@ -125,6 +126,9 @@ __global__ void __launch_bounds__(kThreads, 2)
     for (int i = 0; i < n_pre; ++i) {
       mbar_arrive_expect_tx(&full[i], stage_bytes);
       tma_load_2d(&maps.w, &full[i], smem + i * stage_bytes, (kb0 + i) * kBlockK, g * p.w_gs + p.w_r0 + m0, pol_w);
+      if (p.whilo)
+        tma_load_2d(&maps.wl, &full[i], smem + i * stage_bytes + kATileBytes, (kb0 + i) * kBlockK,
+                    g * p.w_gs + p.w_r0 + m0, pol_w);
     }
     tma_prefetch_desc(&maps.x64);
     tma_prefetch_desc(&maps.x16);
@@ -146,7 +150,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       const int wrow = g * p.w_gs + p.w_r0 + m0;
       const int xrow = g * p.x_group_rows + n0;
       auto load_x = [&](int s, int kb) {
-        uint8_t* sb = smem + s * stage_bytes + kATileBytes;
+        uint8_t* sb = smem + s * stage_bytes + a_bytes;
         const int kc = kb * kBlockK;
         for (int term = 0; term < (p.hilo ? 2 : 1); ++term, sb += x_bytes) {
           const CUtensorMap* m64 = term ? &maps.xl64 : &maps.x64;
@@ -166,6 +170,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         mbar_wait(&empty[s], ph ^ 1);
         mbar_arrive_expect_tx(&full[s], stage_bytes);
         tma_load_2d(&maps.w, &full[s], smem + s * stage_bytes, kb * kBlockK, wrow, pol_w);
+        if (p.whilo) tma_load_2d(&maps.wl, &full[s], smem + s * stage_bytes + kATileBytes, kb * kBlockK, wrow, pol_w);
         load_x(s, kb);
         if (++s == p.stages) {
           s = 0;
@@ -185,13 +190,15 @@ __global__ void __launch_bounds__(kThreads, 2)
         if (tr && kb == kb0) tr[4] = globaltimer();
         const uint32_t sa = smem_u32(smem + s * stage_bytes);
         const uint64_t adesc = umma_sdesc_sw128(sa);
-        const uint64_t bdesc = umma_sdesc_sw128(sa + kATileBytes);
-        const uint64_t ldesc = umma_sdesc_sw128(sa + kATileBytes + x_bytes);
+        const uint64_t aldesc = umma_sdesc_sw128(sa + kATileBytes);  // weight lo term (whilo)
+        const uint64_t bdesc = umma_sdesc_sw128(sa + a_bytes);
+        const uint64_t ldesc = umma_sdesc_sw128(sa + a_bytes + x_bytes);
 #pragma unroll
         for (int k = 0; k < kBlockK / 16; ++k) {
           // +32 bytes per K=16 slice inside the 128-byte swizzle row (address field in 16-byte units)
           umma_f16_ss(tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
           if (p.hilo) umma_f16_ss(tmem, adesc + 2 * k, ldesc + 2 * k, idesc, 1u);
+          if (p.whilo) umma_f16_ss(tmem, aldesc + 2 * k, bdesc + 2 * k, idesc, 1u);
         }
         umma_commit(&empty[s]);
         if (++s == p.stages) {
@@ -287,7 +294,8 @@ __global__ void __launch_bounds__(kPThreads, 1)
   const bool leader = crank == 0;
   const int x_rows = pair ? (p.bn >> 1) : p.bn;  // token rows staged by this CTA (per term)
   const int x_bytes = x_rows * 128;
-  const int stage_bytes = kATileBytes + x_bytes * (p.hilo ? 2 : 1);
+  const int a_bytes = kATileBytes * (p.whilo ? 2 : 1);  // weight tile (+ its lo term)
+  const int stage_bytes = a_bytes + x_bytes * (p.hilo ? 2 : 1);
   uint8_t* staging = smem + p.stages * stage_bytes;  // 16 warps x 16 rows x kRowBytes
   uint64_t* full = reinterpret_cast<uint64_t*>(staging + kPEpiWarps * 16 * kRowBytes);
   uint64_t* empty = full + p.stages;
@@ -329,6 +337,9 @@ __global__ void __launch_bounds__(kPThreads, 1)
         for (int i = 0; i < n_pre; ++i) {
           mbar_arrive_expect_tx(&full[i], full_bytes);
           tma_load_2d(&maps.w, &full[i], smem + i * stage_bytes, i * kBlockK, g * p.w_gs + p.w_r0 + mt * kBlockM, pol_w);
+          if (p.whilo)
+            tma_load_2d(&maps.wl, &full[i], smem + i * stage_bytes + kATileBytes, i * kBlockK,
+                        g * p.w_gs + p.w_r0 + mt * kBlockM, pol_w);
         }
       }
     }
@@ -364,11 +375,17 @@ __global__ void __launch_bounds__(kPThreads, 1)
                                                                                      : policy_evict_first());
       const uint64_t pol_x = policy_evict_last();
       auto load_w = [&](int s, int kb, int wrow) {
-        if constexpr (PAIR) tma_load_2d_2sm(&maps.w, &full[s], smem + s * stage_bytes, kb * kBlockK, wrow, pol_w);
-        else tma_load_2d(&maps.w, &full[s], smem + s * stage_bytes, kb * kBlockK, wrow, pol_w);
+        uint8_t* sa = smem + s * stage_bytes;
+        if constexpr (PAIR) {
+          tma_load_2d_2sm(&maps.w, &full[s], sa, kb * kBlockK, wrow, pol_w);
+          if (p.whilo) tma_load_2d_2sm(&maps.wl, &full[s], sa + kATileBytes, kb * kBlockK, wrow, pol_w);
+        } else {
+          tma_load_2d(&maps.w, &full[s], sa, kb * kBlockK, wrow, pol_w);
+          if (p.whilo) tma_load_2d(&maps.wl, &full[s], sa + kATileBytes, kb * kBlockK, wrow, pol_w);
+        }
       };
       auto load_x = [&](int s, int kb, int xrow) {
-        uint8_t* sb = smem + s * stage_bytes + kATileBytes;
+        uint8_t* sb = smem + s * stage_bytes + a_bytes;
         for (int term = 0; term < (p.hilo ? 2 : 1); ++term, sb += x_bytes) {
           const CUtensorMap* m64 = term ? &maps.xl64 : &maps.x64;
           const CUtensorMap* m16 = term ? &maps.xl16 : &maps.x16;
@@ -441,13 +458,15 @@ __global__ void __launch_bounds__(kPThreads, 1)
           if (tr && j == 0 && kb == 0) tr[4] = globaltimer();
           const uint32_t sa = smem_u32(smem + s * stage_bytes);
           const uint64_t adesc = umma_sdesc_sw128(sa);
-          const uint64_t bdesc = umma_sdesc_sw128(sa + kATileBytes);
-          const uint64_t ldesc = umma_sdesc_sw128(sa + kATileBytes + x_bytes);  // lo term (hilo)
+          const uint64_t aldesc = umma_sdesc_sw128(sa + kATileBytes);      // weight lo term (whilo)
+          const uint64_t bdesc = umma_sdesc_sw128(sa + a_bytes);
+          const uint64_t ldesc = umma_sdesc_sw128(sa + a_bytes + x_bytes);  // token lo term (hilo)
           if constexpr (PAIR) {
 #pragma unroll
             for (int k = 0; k < kBlockK / 16; ++k) {
               umma_f16_ss_2sm(acc, adesc + 2 * k, bdesc + 2 * k, idesc, (kb > 0 || k > 0) ? 1u : 0u);
               if (p.hilo) umma_f16_ss_2sm(acc, adesc + 2 * k, ldesc + 2 * k, idesc, 1u);
+              if (p.whilo) umma_f16_ss_2sm(acc, aldesc + 2 * k, bdesc + 2 * k, idesc, 1u);
             }
             umma_commit_2sm_mc(&empty[s], 0x3);
           } else {
@@ -455,6 +474,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
             for (int k = 0; k < kBlockK / 16; ++k) {
               umma_f16_ss(acc, adesc + 2 * k, bdesc + 2 * k, idesc, (kb > 0 || k > 0) ? 1u : 0u);
               if (p.hilo) umma_f16_ss(acc, adesc + 2 * k, ldesc + 2 * k, idesc, 1u);
+              if (p.whilo) umma_f16_ss(acc, aldesc + 2 * k, bdesc + 2 * k, idesc, 1u);
             }
             umma_commit(&empty[s]);
           }
@@ -552,7 +572,8 @@ static void launch_persistent_t(const GemmMaps& maps, const GemmParams& p, int g
   q.trace = trace_ptr_advance(grid);
   const int row_bytes = 32 * (OUT_F32 ? 4 : 2);
   const int x_rows = q.cluster == 2 ? p.bn / 2 : p.bn;
-  const size_t smem = static_cast<size_t>(q.stages) * (kATileBytes + x_rows * 128 * (p.hilo ? 2 : 1)) +
+  const size_t smem = static_cast<size_t>(q.stages) *
+                          (kATileBytes * (p.whilo ? 2 : 1) + x_rows * 128 * (p.hilo ? 2 : 1)) +
                       kPEpiWarps * 16 * row_bytes + 1024 + 256;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
@@ -665,8 +686,18 @@ int gemm_trace_counts(int* out, int max) {
 }
 
 // stage = weight tile + both token terms (the smem size does not depend on hilo being used)
-size_t gemm_smem_bytes(int bn, int stages) {
-  return static_cast<size_t>(stages) * (kATileBytes + 2 * bn * 128) + 1024 /*align*/ + 256 /*barriers*/;
+size_t gemm_smem_bytes(int bn, int stages, int whilo) {
+  return static_cast<size_t>(stages) * (kATileBytes * (whilo ? 2 : 1) + 2 * bn * 128) + 1024 /*align*/ +
+         256 /*barriers*/;
+}
+
+int gemm_whilo_stages(int x_rows, bool persistent, bool out_f32) {
+  const int stage = 2 * kATileBytes + 2 * x_rows * 128;
+  if (persistent) {
+    const int staging = kPEpiWarps * 16 * 32 * (out_f32 ? 4 : 2);
+    return std::max(2, std::min(8, (224 * 1024 - staging) / stage));
+  }
+  return std::max(2, std::min(6, (110 * 1024) / stage));
 }
 
 void gemm_configure_tiles(int t_rows, int* bn, int* n_tiles, int* stages) {
@@ -698,7 +729,7 @@ static void launch_gemm_t(const GemmMaps& maps, const GemmParams& p, int groups,
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(p.m_tiles * p.n_tiles * p.splits, groups);
   cfg.blockDim = dim3(64 + 32 * p.epi_warps);
-  cfg.dynamicSmemBytes = gemm_smem_bytes(p.bn, p.stages);
+  cfg.dynamicSmemBytes = gemm_smem_bytes(p.bn, p.stages, p.whilo);
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;

@@ -69,6 +69,7 @@ struct GemmParams {
   int kb_per_split;
   int stages;
   int hilo;         // X operand is an (hi, lo) pair (maps xl64 / xl16)
+  int whilo;        // W operand is an (hi, lo) pair too (map wl): weights of a float64 source (dense kind)
   void* out;
   long long out_group_stride;  // elements
   long long out_split_stride;  // elements
@@ -92,6 +93,7 @@ int gemm_trace_counts(int* out, int max);
 
 struct GemmMaps {
   CUtensorMap w;      // box {64, 128}
+  CUtensorMap wl;     // box {64, 128}   the weights' lo term (whilo)
   CUtensorMap x64;    // box {64, 64}   hi term
   CUtensorMap x16;    // box {64, 16}
   CUtensorMap xl64;   // box {64, 64}   lo term (hilo)
@@ -105,7 +107,9 @@ bool gemm_persistent_pair(int t_rows, int m_tiles, int groups);
 void gemm_configure_persistent(int t_rows, bool out_f32, int units_per_tile, int n_ctas, bool pair, int* bn,
                                int* n_tiles, int* stages);
 int sm_count();
-size_t gemm_smem_bytes(int bn, int stages);
+size_t gemm_smem_bytes(int bn, int stages, int whilo = 0);
+// ring depth when every stage also holds the weights' lo tile (x_rows = token rows staged per CTA)
+int gemm_whilo_stages(int x_rows, bool persistent, bool out_f32);
 void gemm_configure_tiles(int t_rows, int* bn, int* n_tiles, int* stages);
 int gemm_epi_warps(int bn, int n_tiles);
 

@@ -156,8 +156,9 @@ struct sp_group {
   int* mlp_done = nullptr;    // fused FFN kernel: FFN1 tiles finished per student + exit counter
   std::vector<void*> allocs;
   // tensor maps
-  std::vector<CUtensorMap> m_qkv, m_o, m_f1, m_f2, m_layers;
-  CUtensorMap m_pool, m_in;
+  std::vector<CUtensorMap> m_qkv, m_o, m_f1, m_f2, m_layers, m_layers_lo;
+  CUtensorMap m_pool, m_in, m_in_lo;
+  bool dense_whilo = false;  // dense weights carry their lo terms (w_in_lo / w_layers_lo)
   CUtensorMap m_qkv_attn;  // qkv buffer viewed with a {64, 128} box (tensor-core attention)
   CUtensorMap m_qkv_kv64;  // the same with a {64, 64} box (64-key chunks of the three-CTA kernel)
   XMaps xm_x16, xm_ctx, xm_ffn, xm_cls, xm_ha, xm_hb, xm_cln, xm_ctxc, xm_ffnc;
@@ -384,6 +385,16 @@ int sp_group_create(const sp_config* cfg, const sp_weights* weights, int device,
     g->m_layers.resize(c.n_layers);
     bool ok = make_map(&g->m_in, w.w_in, S * H, c.d_in, 128);
     for (int l = 0; l < c.n_layers; ++l) ok &= make_map(&g->m_layers[l], wl + (size_t)l * S * H * H, S * H, H, 128);
+    if ((w.w_in_lo == nullptr) != (w.w_layers_lo == nullptr))
+      return bail(fail(SP_EINVAL, "w_in_lo and w_layers_lo must be given together"));
+    g->dense_whilo = w.w_in_lo != nullptr;
+    if (g->dense_whilo) {
+      const auto* wll = static_cast<const half*>(w.w_layers_lo);
+      g->m_layers_lo.resize(c.n_layers);
+      ok &= make_map(&g->m_in_lo, w.w_in_lo, S * H, c.d_in, 128);
+      for (int l = 0; l < c.n_layers; ++l)
+        ok &= make_map(&g->m_layers_lo[l], wll + (size_t)l * S * H * H, S * H, H, 128);
+    }
     ok &= make_xmaps(&g->xm_ha, g->ha, g->ha + g->h_lo, S * T, H);
     ok &= make_xmaps(&g->xm_hb, g->hb, g->hb + g->h_lo, S * T, H);
     if (!ok) return bail(fail(SP_EINVAL, "tensor-map creation failed (pointer alignment / shape)"));
@@ -466,7 +477,8 @@ void launch_attention_any(int kind, const CUtensorMap& map_qkv, const CUtensorMa
 void run_gemm(sp_group* grp, int kind, const CUtensorMap& wmap, const XMaps& xm, int groups, int n_out, int k_dim,
               int t_rows, int x_group_rows, const float* bias, int bias_gs, int act, void* out, long long out_gs,
               long long out_lo_off, int out_f32, int splits, long long split_stride, cudaStream_t st,
-              const int* t_dev = nullptr, int out_ld = 0, int w_gs = 0, int w_r0 = 0) {
+              const int* t_dev = nullptr, int out_ld = 0, int w_gs = 0, int w_r0 = 0,
+              const CUtensorMap* wlo = nullptr) {
   sp::GemmParams p{};
   p.t_dev = t_dev;
   p.n_out = n_out;
@@ -487,6 +499,8 @@ void run_gemm(sp_group* grp, int kind, const CUtensorMap& wmap, const XMaps& xm,
   p.out_f32 = out_f32;
   sp::GemmMaps maps;
   maps.w = wmap;
+  p.whilo = wlo ? 1 : 0;
+  if (wlo) maps.wl = *wlo;
   maps.x64 = xm.x64;
   maps.x16 = xm.x16;
   maps.xl64 = xm.xl64;
@@ -494,13 +508,16 @@ void run_gemm(sp_group* grp, int kind, const CUtensorMap& wmap, const XMaps& xm,
   // profiling: algorithmic bytes of a projection = its weights + bias (the activations
   // are L2-resident at batch-1 and not part of the request's compulsory HBM traffic)
   const double G = groups, N = n_out, K = k_dim, T = t_rows;
-  const double wbytes = G * N * K * 2.0 + (bias ? G * N * 4.0 : 0.0);
+  const double wbytes = G * N * K * 2.0 * (wlo ? 2 : 1) + (bias ? G * N * 4.0 : 0.0);
   // one-split projections from 17 tokens on: the persistent kernel (measured equal or 2-4 us faster)
   if (splits == 1 && t_rows >= 17) {
     p.splits = 1;
     p.kb_per_split = k_dim / 64;
     sp::gemm_configure_persistent(t_rows, out_f32 != 0, groups * p.m_tiles, sp::sm_count(),
                                   sp::gemm_persistent_pair(t_rows, p.m_tiles, groups), &p.bn, &p.n_tiles, &p.stages);
+    if (wlo)  // a second weight tile per stage: re-derive the ring depth (same smem budget)
+      p.stages = sp::gemm_whilo_stages(sp::gemm_persistent_pair(t_rows, p.m_tiles, groups) ? p.bn / 2 : p.bn, true,
+                                       out_f32 != 0);
     // weights re-read by many token tiles stay in L2 (evict_last); streamed once or twice (batch-1)
     // they must not push the residual stream out (evict_first: -2% at L=512)
     p.w_keep = p.n_tiles > 2 ? 2 : 0;
@@ -512,6 +529,7 @@ void run_gemm(sp_group* grp, int kind, const CUtensorMap& wmap, const XMaps& xm,
   p.cluster = 1;
   p.w_keep = 0;  // evict_last for re-read weights measured 1-4 us slower at 160-256 tokens
   sp::gemm_configure_tiles(t_rows, &p.bn, &p.n_tiles, &p.stages);
+  if (wlo) p.stages = sp::gemm_whilo_stages(p.bn, false, out_f32 != 0);
   p.epi_warps = sp::gemm_epi_warps(p.bn, p.n_tiles);
   p.splits = splits;
   p.kb_per_split = (k_dim / 64) / splits;
@@ -803,7 +821,7 @@ void dense_forward(sp_group* g, const XMaps& xin_maps, int n_rows, int k, float*
     half* bufs[2] = {g->ha, g->hb};
     const XMaps* maps[2] = {&g->xm_ha, &g->xm_hb};
     run_gemm(g, SP_LAUNCH_GEMM_DENSE, g->m_in, xin_maps, k, H, c.d_in, n_rows, 0, w.b_in, H, sp::ACT_TANH, bufs[0],
-             hgs, g->h_lo, 0, 1, 0, st);
+             hgs, g->h_lo, 0, 1, 0, st, nullptr, 0, 0, 0, g->dense_whilo ? &g->m_in_lo : nullptr);
     ++launches;
     int cur = 0;
     for (int l = 0; l < c.n_layers; ++l) {
@@ -811,7 +829,8 @@ void dense_forward(sp_group* g, const XMaps& xin_maps, int n_rows, int k, float*
       const size_t lS = (size_t)l * S;
       void* out = last ? static_cast<void*>(g->final32) : static_cast<void*>(bufs[cur ^ 1]);
       run_gemm(g, SP_LAUNCH_GEMM_DENSE, g->m_layers[l], *maps[cur], k, H, H, n_rows, T, w.b_layers + lS * H, H,
-               sp::ACT_TANH, out, last ? fgs : hgs, last ? 0 : g->h_lo, last ? 1 : 0, 1, 0, st);
+               sp::ACT_TANH, out, last ? fgs : hgs, last ? 0 : g->h_lo, last ? 1 : 0, 1, 0, st, nullptr, 0, 0, 0,
+               g->dense_whilo ? &g->m_layers_lo[l] : nullptr);
       ++launches;
       cur ^= 1;
     }

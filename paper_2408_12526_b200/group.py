@@ -141,6 +141,8 @@ class StudentGroup:
                 cfg.hidden, cfg.n_layers, cfg.d_in = weights.hidden_padded, weights.depth, weights.d_in_padded
                 cfg.n_classes = weights.n_classes
                 names = ["w_in", "b_in", "w_layers", "b_layers"]
+                if weights.exact_weights:
+                    names += ["w_in_lo", "w_layers_lo"]
                 self.hidden, self.n_classes = weights.hidden_padded, weights.n_classes
             else:
                 raise TypeError(f"unsupported weights {type(weights).__name__}")

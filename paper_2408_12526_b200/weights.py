@@ -210,6 +210,11 @@ class DenseGroupWeights:
     alpha: np.ndarray     # f32 [K]
     w_cls: np.ndarray     # f32 [C, Hp]
     b_cls: np.ndarray     # f32 [C]
+    # fp16 lo terms W - fp16(W) of float64 source weights (None: the fp16 weights are exact). The
+    # engine then multiplies (W_hi + W_lo)(x_hi + x_lo) - W_lo x_lo: ~22-bit operands, so a
+    # reference-trained float64 checkpoint reproduces the reference's own logits (ABI v3).
+    w_in_lo: np.ndarray | None = None      # f16 [K, Hp, Dp]
+    w_layers_lo: np.ndarray | None = None  # f16 [depth, K, Hp, Hp]
     kind: str = field(default="dense", init=False)
 
     @property
@@ -224,27 +229,49 @@ class DenseGroupWeights:
     def d_in_padded(self) -> int:
         return int(self.w_in.shape[2])
 
+    @property
+    def exact_weights(self) -> bool:
+        """True when the lo terms are carried (the engine runs the 3-product hi/lo projections)."""
+        return self.w_in_lo is not None
+
     def subset(self, idx) -> "DenseGroupWeights":
         idx = np.asarray(idx, dtype=np.int64)
+        lo = {}
+        if self.exact_weights:
+            lo = dict(w_in_lo=np.ascontiguousarray(self.w_in_lo[idx]),
+                      w_layers_lo=np.ascontiguousarray(self.w_layers_lo[:, idx]))
         return replace(self, w_in=np.ascontiguousarray(self.w_in[idx]), b_in=np.ascontiguousarray(self.b_in[idx]),
                        w_layers=np.ascontiguousarray(self.w_layers[:, idx]),
                        b_layers=np.ascontiguousarray(self.b_layers[:, idx]),
-                       alpha=np.ascontiguousarray(self.alpha[idx]))
+                       alpha=np.ascontiguousarray(self.alpha[idx]), **lo)
 
-    # Unpadded, rounded per-student arrays in float64 — what the reference/oracle is fed.
+    # Unpadded per-student arrays in float64 exactly as the engine represents them (hi + lo when
+    # the lo terms are carried) — what the oracle is fed for "identical weights" parity.
     def student_layers(self, m: int) -> list[tuple[np.ndarray, np.ndarray]]:
         H, D = self.rep_dim, self.d_in
-        out = [(self.w_in[m, :H, :D].astype(np.float64), self.b_in[m, :H].astype(np.float64))]
+
+        def mat(hi, lo):
+            v = hi.astype(np.float64)
+            return v if lo is None else v + lo.astype(np.float64)
+
+        out = [(mat(self.w_in[m, :H, :D], None if self.w_in_lo is None else self.w_in_lo[m, :H, :D]),
+                self.b_in[m, :H].astype(np.float64))]
         for l in range(self.depth):
-            out.append((self.w_layers[l, m, :H, :H].astype(np.float64), self.b_layers[l, m, :H].astype(np.float64)))
+            lo = None if self.w_layers_lo is None else self.w_layers_lo[l, m, :H, :H]
+            out.append((mat(self.w_layers[l, m, :H, :H], lo), self.b_layers[l, m, :H].astype(np.float64)))
         return out
 
     def classifier(self) -> tuple[np.ndarray, np.ndarray]:
         return self.w_cls[:, : self.rep_dim].astype(np.float64), self.b_cls.astype(np.float64)
 
 
-def dense_group_from_arrays(students: list[list[tuple[np.ndarray, np.ndarray]]], multipliers, classifier) -> DenseGroupWeights:
-    """Build from per-student [(W_in, b_in), (W_1, b_1), ...] lists and classifier (W_c, b_c)."""
+def dense_group_from_arrays(students: list[list[tuple[np.ndarray, np.ndarray]]], multipliers, classifier,
+                            exact: bool = True) -> DenseGroupWeights:
+    """Build from per-student [(W_in, b_in), (W_1, b_1), ...] lists and classifier (W_c, b_c).
+
+    exact: keep the fp16 lo terms of weights that fp16 does not represent (float64 sources such as
+    the reference's trained checkpoints); with exact=False, or when every weight is already an fp16
+    value, the group carries fp16 weights only (one weight operand per projection)."""
     K = len(students)
     if K == 0:
         raise ValueError("empty ensemble")
@@ -283,8 +310,20 @@ def dense_group_from_arrays(students: list[list[tuple[np.ndarray, np.ndarray]]],
         raise ValueError(f"classifier in_dim {Wc.shape[1]} does not match rep_dim {rep_dim}")
     w_cls = np.zeros((Wc.shape[0], Hp), np.float32)
     w_cls[:, :rep_dim] = Wc
+    lo = {}
+    if exact:
+        w_in_lo = np.zeros_like(w_in)
+        w_l_lo = np.zeros_like(w_l)
+        for m, layers in enumerate(students):
+            W = np.asarray(layers[0][0], dtype=np.float64)
+            w_in_lo[m, :rep_dim, :d_in] = W - w_in[m, :rep_dim, :d_in].astype(np.float64)
+            for l, (W, _) in enumerate(layers[1:]):
+                W = np.asarray(W, dtype=np.float64)
+                w_l_lo[l, m, :rep_dim, :rep_dim] = W - w_l[l, m, :rep_dim, :rep_dim].astype(np.float64)
+        if w_in_lo.any() or w_l_lo.any():
+            lo = dict(w_in_lo=w_in_lo, w_layers_lo=w_l_lo)
     return DenseGroupWeights(d_in, rep_dim, depth, int(Wc.shape[0]), w_in, b_in, w_l, b_l,
-                             _f32(np.asarray(multipliers, dtype=np.float64)), w_cls, _f32(bc))
+                             _f32(np.asarray(multipliers, dtype=np.float64)), w_cls, _f32(bc), **lo)
 
 
 def dense_group_from_ensemble(state) -> DenseGroupWeights:
@@ -304,7 +343,7 @@ def dense_group_from_ensemble(state) -> DenseGroupWeights:
 
 
 def random_dense_group(d_in: int, rep_dim: int, depth: int, n_students: int, n_classes: int = 2,
-                       seed: int = 0) -> DenseGroupWeights:
+                       seed: int = 0, exact: bool = True) -> DenseGroupWeights:
     """Glorot-uniform students as ``StudentModel.build`` draws them (nnkernel.py:24-26, :270-274),
     with small random biases so the bias path is exercised."""
     students = []
@@ -319,4 +358,4 @@ def random_dense_group(d_in: int, rep_dim: int, depth: int, n_students: int, n_c
     crng = rng_for(seed, "classifier")
     limit = math.sqrt(6.0 / (rep_dim + n_classes))
     clf = (crng.uniform(-limit, limit, size=(n_classes, rep_dim)), crng.normal(0, 0.05, size=n_classes))
-    return dense_group_from_arrays(students, [float(a) for a in _alpha_draw(seed, n_students)], clf)
+    return dense_group_from_arrays(students, [float(a) for a in _alpha_draw(seed, n_students)], clf, exact=exact)

@@ -147,3 +147,33 @@ def test_weights_container_roundtrip_matches_golden():
     for k in range(1, case["K"] + 1):
         rep, logits = od.group_forward_weights(w, case["x"], k)
         np.testing.assert_allclose(logits, case["logits"][k], rtol=1e-12, atol=1e-14)
+
+
+def test_weight_lo_terms_carry_float64_checkpoints():
+    """Float64 reference weights travel as fp16 (hi, lo) pairs (ABI v3): the group's represented
+    weights reproduce the reference's own logits to ~1e-6 on the reference-trained checkpoint and
+    the 'tiny' golden, where fp16 weights alone are 1e-3..3e-2 off. fp16-exact sources and
+    exact=False carry no lo terms; subset() keeps them aligned with the students."""
+    from conftest import rel_err_rows
+    from goldens import GOLDEN, load_trained_task
+    from paper_2408_12526_b200.checkpoint import load_ensemble_weights
+    from paper_2408_12526_b200.weights import dense_group_from_arrays
+
+    task = load_trained_task()
+    w = load_ensemble_weights(GOLDEN / "ensemble_trained.json")
+    assert w.exact_weights and w.w_in_lo.dtype == np.float16 and w.w_layers_lo.shape == w.w_layers.shape
+    for k in range(1, len(w.alpha) + 1):
+        _, z = od.group_forward_weights(w, task["x_val"], k)
+        assert rel_err_rows(z, task[f"logits_val_k{k}"]) <= 1e-5
+    case = load_dense("tiny")
+    for exact, bound in ((True, 1e-5), (False, 1e-2)):
+        wt = dense_group_from_arrays(case["students"], case["alphas"], case["classifier"], exact=exact)
+        assert wt.exact_weights == exact
+        err = max(rel_err_rows(od.group_forward_weights(wt, case["x"], k)[1], case["logits"][k])
+                  for k in range(1, case["K"] + 1))
+        assert err <= bound
+    pad = load_dense("pad")  # engine-precision fixture: weights already fp16 values
+    assert not dense_group_from_arrays(pad["students"], pad["alphas"], pad["classifier"]).exact_weights
+    sub = w.subset([2, 0])
+    np.testing.assert_array_equal(sub.w_layers_lo[:, 0], w.w_layers_lo[:, 2])
+    np.testing.assert_array_equal(sub.w_in_lo[1], w.w_in_lo[0])
