@@ -81,13 +81,16 @@ __device__ __forceinline__ void warp_store_rows(const float (&y)[NR], int n, Out
   __syncwarp();
 }
 
-template <int ACT, bool OUT_F32>
+template <bool WHILO>
+using MapsOf = typename std::conditional<WHILO, GemmMapsW, GemmMaps>::type;
+
+template <int ACT, bool OUT_F32, bool WHILO>
 __global__ void __launch_bounds__(kThreads, 2)
-    gemm_kernel(const __grid_constant__ GemmMaps maps, const GemmParams p) {
+    gemm_kernel(const __grid_constant__ MapsOf<WHILO> maps, const GemmParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int x_bytes = p.bn * 128;                            // one term of the token tile
-  const int a_bytes = kATileBytes * (p.whilo ? 2 : 1);       // weight tile (+ its lo term)
+  constexpr int a_bytes = kATileBytes * (WHILO ? 2 : 1);     // weight tile (+ its lo term)
   const int stage_bytes = a_bytes + x_bytes * (p.hilo ? 2 : 1);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.stages * stage_bytes);
   uint64_t* empty = full + p.stages;
@@ -126,7 +129,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     for (int i = 0; i < n_pre; ++i) {
       mbar_arrive_expect_tx(&full[i], stage_bytes);
       tma_load_2d(&maps.w, &full[i], smem + i * stage_bytes, (kb0 + i) * kBlockK, g * p.w_gs + p.w_r0 + m0, pol_w);
-      if (p.whilo)
+      if constexpr (WHILO)
         tma_load_2d(&maps.wl, &full[i], smem + i * stage_bytes + kATileBytes, (kb0 + i) * kBlockK,
                     g * p.w_gs + p.w_r0 + m0, pol_w);
     }
@@ -170,7 +173,8 @@ __global__ void __launch_bounds__(kThreads, 2)
         mbar_wait(&empty[s], ph ^ 1);
         mbar_arrive_expect_tx(&full[s], stage_bytes);
         tma_load_2d(&maps.w, &full[s], smem + s * stage_bytes, kb * kBlockK, wrow, pol_w);
-        if (p.whilo) tma_load_2d(&maps.wl, &full[s], smem + s * stage_bytes + kATileBytes, kb * kBlockK, wrow, pol_w);
+        if constexpr (WHILO)
+          tma_load_2d(&maps.wl, &full[s], smem + s * stage_bytes + kATileBytes, kb * kBlockK, wrow, pol_w);
         load_x(s, kb);
         if (++s == p.stages) {
           s = 0;
@@ -198,7 +202,7 @@ __global__ void __launch_bounds__(kThreads, 2)
           // +32 bytes per K=16 slice inside the 128-byte swizzle row (address field in 16-byte units)
           umma_f16_ss(tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
           if (p.hilo) umma_f16_ss(tmem, adesc + 2 * k, ldesc + 2 * k, idesc, 1u);
-          if (p.whilo) umma_f16_ss(tmem, aldesc + 2 * k, bdesc + 2 * k, idesc, 1u);
+          if constexpr (WHILO) umma_f16_ss(tmem, aldesc + 2 * k, bdesc + 2 * k, idesc, 1u);
         }
         umma_commit(&empty[s]);
         if (++s == p.stages) {
@@ -276,9 +280,9 @@ static constexpr int kPersistTmemCols = 512;  // 2 accumulators x 256 columns
 static constexpr int kPEpiWarps = 16;          // 4 warps per TMEM lane quadrant, a quarter of the columns each
 static constexpr int kPThreads = 64 + 32 * kPEpiWarps;
 
-template <int ACT, bool OUT_F32, bool PAIR>
+template <int ACT, bool OUT_F32, bool PAIR, bool WHILO>
 __global__ void __launch_bounds__(kPThreads, 1)
-    gemm_persistent_kernel(const __grid_constant__ GemmMaps maps, const GemmParams p) {
+    gemm_persistent_kernel(const __grid_constant__ MapsOf<WHILO> maps, const GemmParams p) {
   using OutT = typename std::conditional<OUT_F32, float, half>::type;
   constexpr int kRowBytes = 32 * static_cast<int>(sizeof(OutT));
   extern __shared__ uint8_t smem_raw[];
@@ -294,7 +298,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
   const bool leader = crank == 0;
   const int x_rows = pair ? (p.bn >> 1) : p.bn;  // token rows staged by this CTA (per term)
   const int x_bytes = x_rows * 128;
-  const int a_bytes = kATileBytes * (p.whilo ? 2 : 1);  // weight tile (+ its lo term)
+  constexpr int a_bytes = kATileBytes * (WHILO ? 2 : 1);  // weight tile (+ its lo term)
   const int stage_bytes = a_bytes + x_bytes * (p.hilo ? 2 : 1);
   uint8_t* staging = smem + p.stages * stage_bytes;  // 16 warps x 16 rows x kRowBytes
   uint64_t* full = reinterpret_cast<uint64_t*>(staging + kPEpiWarps * 16 * kRowBytes);
@@ -337,7 +341,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
         for (int i = 0; i < n_pre; ++i) {
           mbar_arrive_expect_tx(&full[i], full_bytes);
           tma_load_2d(&maps.w, &full[i], smem + i * stage_bytes, i * kBlockK, g * p.w_gs + p.w_r0 + mt * kBlockM, pol_w);
-          if (p.whilo)
+          if constexpr (WHILO)
             tma_load_2d(&maps.wl, &full[i], smem + i * stage_bytes + kATileBytes, i * kBlockK,
                         g * p.w_gs + p.w_r0 + mt * kBlockM, pol_w);
         }
@@ -378,10 +382,10 @@ __global__ void __launch_bounds__(kPThreads, 1)
         uint8_t* sa = smem + s * stage_bytes;
         if constexpr (PAIR) {
           tma_load_2d_2sm(&maps.w, &full[s], sa, kb * kBlockK, wrow, pol_w);
-          if (p.whilo) tma_load_2d_2sm(&maps.wl, &full[s], sa + kATileBytes, kb * kBlockK, wrow, pol_w);
+          if constexpr (WHILO) tma_load_2d_2sm(&maps.wl, &full[s], sa + kATileBytes, kb * kBlockK, wrow, pol_w);
         } else {
           tma_load_2d(&maps.w, &full[s], sa, kb * kBlockK, wrow, pol_w);
-          if (p.whilo) tma_load_2d(&maps.wl, &full[s], sa + kATileBytes, kb * kBlockK, wrow, pol_w);
+          if constexpr (WHILO) tma_load_2d(&maps.wl, &full[s], sa + kATileBytes, kb * kBlockK, wrow, pol_w);
         }
       };
       auto load_x = [&](int s, int kb, int xrow) {
@@ -466,7 +470,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
             for (int k = 0; k < kBlockK / 16; ++k) {
               umma_f16_ss_2sm(acc, adesc + 2 * k, bdesc + 2 * k, idesc, (kb > 0 || k > 0) ? 1u : 0u);
               if (p.hilo) umma_f16_ss_2sm(acc, adesc + 2 * k, ldesc + 2 * k, idesc, 1u);
-              if (p.whilo) umma_f16_ss_2sm(acc, aldesc + 2 * k, bdesc + 2 * k, idesc, 1u);
+              if constexpr (WHILO) umma_f16_ss_2sm(acc, aldesc + 2 * k, bdesc + 2 * k, idesc, 1u);
             }
             umma_commit_2sm_mc(&empty[s], 0x3);
           } else {
@@ -474,7 +478,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
             for (int k = 0; k < kBlockK / 16; ++k) {
               umma_f16_ss(acc, adesc + 2 * k, bdesc + 2 * k, idesc, (kb > 0 || k > 0) ? 1u : 0u);
               if (p.hilo) umma_f16_ss(acc, adesc + 2 * k, ldesc + 2 * k, idesc, 1u);
-              if (p.whilo) umma_f16_ss(acc, aldesc + 2 * k, bdesc + 2 * k, idesc, 1u);
+              if constexpr (WHILO) umma_f16_ss(acc, aldesc + 2 * k, bdesc + 2 * k, idesc, 1u);
             }
             umma_commit(&empty[s]);
           }
@@ -551,17 +555,17 @@ __global__ void __launch_bounds__(kPThreads, 1)
   }
 }
 
-template <int ACT, bool OUT_F32>
-static void launch_persistent_t(const GemmMaps& maps, const GemmParams& p, int groups, cudaStream_t stream) {
+template <int ACT, bool OUT_F32, bool WHILO>
+static void launch_persistent_t(const GemmMapsW& maps, const GemmParams& p, int groups, cudaStream_t stream) {
   static int n_sm = 0;
   if (n_sm == 0) {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncSetAttribute(gemm_persistent_kernel<ACT, OUT_F32, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         227 * 1024);
-    cudaFuncSetAttribute(gemm_persistent_kernel<ACT, OUT_F32, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         227 * 1024);
+    cudaFuncSetAttribute(gemm_persistent_kernel<ACT, OUT_F32, false, WHILO>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(gemm_persistent_kernel<ACT, OUT_F32, true, WHILO>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
   }
   GemmParams q = p;
   q.groups = groups;
@@ -573,7 +577,7 @@ static void launch_persistent_t(const GemmMaps& maps, const GemmParams& p, int g
   const int row_bytes = 32 * (OUT_F32 ? 4 : 2);
   const int x_rows = q.cluster == 2 ? p.bn / 2 : p.bn;
   const size_t smem = static_cast<size_t>(q.stages) *
-                          (kATileBytes * (p.whilo ? 2 : 1) + x_rows * 128 * (p.hilo ? 2 : 1)) +
+                          (kATileBytes * (WHILO ? 2 : 1) + x_rows * 128 * (p.hilo ? 2 : 1)) +
                       kPEpiWarps * 16 * row_bytes + 1024 + 256;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
@@ -589,8 +593,9 @@ static void launch_persistent_t(const GemmMaps& maps, const GemmParams& p, int g
   attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-  if (q.cluster == 2) cudaLaunchKernelEx(&cfg, gemm_persistent_kernel<ACT, OUT_F32, true>, maps, q);
-  else cudaLaunchKernelEx(&cfg, gemm_persistent_kernel<ACT, OUT_F32, false>, maps, q);
+  const MapsOf<WHILO>& m = maps;  // the BERT instantiations get the plain maps (no weight-lo map)
+  if (q.cluster == 2) cudaLaunchKernelEx(&cfg, gemm_persistent_kernel<ACT, OUT_F32, true, WHILO>, m, q);
+  else cudaLaunchKernelEx(&cfg, gemm_persistent_kernel<ACT, OUT_F32, false, WHILO>, m, q);
 }
 
 // CTA pairs (cta_group::2) halve each CTA's token-tile traffic (both (hi, lo) terms): from 256 tokens
@@ -640,17 +645,21 @@ void gemm_configure_persistent(int t_rows, bool out_f32, int units_per_tile, int
   *stages = st;
 }
 
-void launch_gemm_persistent(const GemmMaps& maps, const GemmParams& p, int groups, cudaStream_t stream) {
+// (the weight-lo operand is instantiated for the dense kind's tanh projections only)
+void launch_gemm_persistent(const GemmMapsW& maps, const GemmParams& p, int groups, cudaStream_t stream) {
   const bool f32 = p.out_f32 != 0;
-  if (p.act == ACT_GELU) {
-    if (f32) launch_persistent_t<ACT_GELU, true>(maps, p, groups, stream);
-    else launch_persistent_t<ACT_GELU, false>(maps, p, groups, stream);
+  if (p.whilo) {
+    if (f32) launch_persistent_t<ACT_TANH, true, true>(maps, p, groups, stream);
+    else launch_persistent_t<ACT_TANH, false, true>(maps, p, groups, stream);
+  } else if (p.act == ACT_GELU) {
+    if (f32) launch_persistent_t<ACT_GELU, true, false>(maps, p, groups, stream);
+    else launch_persistent_t<ACT_GELU, false, false>(maps, p, groups, stream);
   } else if (p.act == ACT_TANH) {
-    if (f32) launch_persistent_t<ACT_TANH, true>(maps, p, groups, stream);
-    else launch_persistent_t<ACT_TANH, false>(maps, p, groups, stream);
+    if (f32) launch_persistent_t<ACT_TANH, true, false>(maps, p, groups, stream);
+    else launch_persistent_t<ACT_TANH, false, false>(maps, p, groups, stream);
   } else {
-    if (f32) launch_persistent_t<ACT_NONE, true>(maps, p, groups, stream);
-    else launch_persistent_t<ACT_NONE, false>(maps, p, groups, stream);
+    if (f32) launch_persistent_t<ACT_NONE, true, false>(maps, p, groups, stream);
+    else launch_persistent_t<ACT_NONE, false, false>(maps, p, groups, stream);
   }
 }
 
@@ -719,17 +728,17 @@ void gemm_configure_tiles(int t_rows, int* bn, int* n_tiles, int* stages) {
   *stages = st;
 }
 
-template <int ACT, bool OUT_F32>
-static void launch_gemm_t(const GemmMaps& maps, const GemmParams& p, int groups, cudaStream_t stream) {
+template <int ACT, bool OUT_F32, bool WHILO>
+static void launch_gemm_t(const GemmMapsW& maps, const GemmParams& p, int groups, cudaStream_t stream) {
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(gemm_kernel<ACT, OUT_F32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(gemm_kernel<ACT, OUT_F32, WHILO>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr_set = true;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(p.m_tiles * p.n_tiles * p.splits, groups);
   cfg.blockDim = dim3(64 + 32 * p.epi_warps);
-  cfg.dynamicSmemBytes = gemm_smem_bytes(p.bn, p.stages, p.whilo);
+  cfg.dynamicSmemBytes = gemm_smem_bytes(p.bn, p.stages, WHILO);
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -742,25 +751,29 @@ static void launch_gemm_t(const GemmMaps& maps, const GemmParams& p, int groups,
     g_trace_used += (size_t)cfg.gridDim.x * cfg.gridDim.y;
     g_trace_counts.push_back(static_cast<int>(cfg.gridDim.x * cfg.gridDim.y));
   }
-  cudaLaunchKernelEx(&cfg, gemm_kernel<ACT, OUT_F32>, maps, q);
+  const MapsOf<WHILO>& m = maps;
+  cudaLaunchKernelEx(&cfg, gemm_kernel<ACT, OUT_F32, WHILO>, m, q);
 }
 
 // Epilogue warps of the small-T kernel: 4 (192 threads) unless the launch has several wide token
 // tiles (measured in-graph: 4 warps -1..-3 us at 96-192 tokens, 8 warps better at 256 = 2 x 128).
 int gemm_epi_warps(int bn, int n_tiles) { return (bn <= 96 || n_tiles == 1) ? 4 : 8; }
 
-void launch_gemm(const GemmMaps& maps, const GemmParams& p, int groups, cudaStream_t stream) {
+void launch_gemm(const GemmMapsW& maps, const GemmParams& p, int groups, cudaStream_t stream) {
   const bool f32 = p.out_f32 || p.splits > 1;
   const int act = p.splits > 1 ? ACT_NONE : p.act;
-  if (act == ACT_GELU) {
-    if (f32) launch_gemm_t<ACT_GELU, true>(maps, p, groups, stream);
-    else launch_gemm_t<ACT_GELU, false>(maps, p, groups, stream);
+  if (p.whilo) {  // dense kind: tanh projections, one split
+    if (f32) launch_gemm_t<ACT_TANH, true, true>(maps, p, groups, stream);
+    else launch_gemm_t<ACT_TANH, false, true>(maps, p, groups, stream);
+  } else if (act == ACT_GELU) {
+    if (f32) launch_gemm_t<ACT_GELU, true, false>(maps, p, groups, stream);
+    else launch_gemm_t<ACT_GELU, false, false>(maps, p, groups, stream);
   } else if (act == ACT_TANH) {
-    if (f32) launch_gemm_t<ACT_TANH, true>(maps, p, groups, stream);
-    else launch_gemm_t<ACT_TANH, false>(maps, p, groups, stream);
+    if (f32) launch_gemm_t<ACT_TANH, true, false>(maps, p, groups, stream);
+    else launch_gemm_t<ACT_TANH, false, false>(maps, p, groups, stream);
   } else {
-    if (f32) launch_gemm_t<ACT_NONE, true>(maps, p, groups, stream);
-    else launch_gemm_t<ACT_NONE, false>(maps, p, groups, stream);
+    if (f32) launch_gemm_t<ACT_NONE, true, false>(maps, p, groups, stream);
+    else launch_gemm_t<ACT_NONE, false, false>(maps, p, groups, stream);
   }
 }
 

@@ -93,16 +93,20 @@ int gemm_trace_counts(int* out, int max);
 
 struct GemmMaps {
   CUtensorMap w;      // box {64, 128}
-  CUtensorMap wl;     // box {64, 128}   the weights' lo term (whilo)
   CUtensorMap x64;    // box {64, 64}   hi term
   CUtensorMap x16;    // box {64, 16}
   CUtensorMap xl64;   // box {64, 64}   lo term (hilo)
   CUtensorMap xl16;   // box {64, 16}
 };
+// + the weights' lo term (dense kind, whilo): only the WHILO kernel instantiations take this one,
+// so the BERT kernels' parameters and loops carry nothing for it
+struct GemmMapsW : GemmMaps {
+  CUtensorMap wl;     // box {64, 128}
+};
 
-void launch_gemm(const GemmMaps& maps, const GemmParams& p, int groups, cudaStream_t stream);
+void launch_gemm(const GemmMapsW& maps, const GemmParams& p, int groups, cudaStream_t stream);
 // Persistent variant for large token counts (splits must be 1).
-void launch_gemm_persistent(const GemmMaps& maps, const GemmParams& p, int groups, cudaStream_t stream);
+void launch_gemm_persistent(const GemmMapsW& maps, const GemmParams& p, int groups, cudaStream_t stream);
 bool gemm_persistent_pair(int t_rows, int m_tiles, int groups);
 void gemm_configure_persistent(int t_rows, bool out_f32, int units_per_tile, int n_ctas, bool pair, int* bn,
                                int* n_tiles, int* stages);

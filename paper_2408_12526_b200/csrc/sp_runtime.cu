@@ -497,7 +497,7 @@ void run_gemm(sp_group* grp, int kind, const CUtensorMap& wmap, const XMaps& xm,
   p.bias_group_stride = bias_gs;
   p.act = act;
   p.out_f32 = out_f32;
-  sp::GemmMaps maps;
+  sp::GemmMapsW maps;
   maps.w = wmap;
   p.whilo = wlo ? 1 : 0;
   if (wlo) maps.wl = *wlo;
