@@ -84,14 +84,14 @@ __device__ __forceinline__ void warp_store_rows(const float (&y)[NR], int n, Out
 template <bool WHILO>
 using MapsOf = typename std::conditional<WHILO, GemmMapsW, GemmMaps>::type;
 
-template <int ACT, bool OUT_F32, bool WHILO>
+template <int ACT, bool OUT_F32, bool HILO, bool WHILO>
 __global__ void __launch_bounds__(kThreads, 2)
     gemm_kernel(const __grid_constant__ MapsOf<WHILO> maps, const GemmParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int x_bytes = p.bn * 128;                            // one term of the token tile
   constexpr int a_bytes = kATileBytes * (WHILO ? 2 : 1);     // weight tile (+ its lo term)
-  const int stage_bytes = a_bytes + x_bytes * (p.hilo ? 2 : 1);
+  const int stage_bytes = a_bytes + x_bytes * (HILO ? 2 : 1);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.stages * stage_bytes);
   uint64_t* empty = full + p.stages;
   uint64_t* tmem_full = empty + p.stages;
@@ -155,7 +155,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       auto load_x = [&](int s, int kb) {
         uint8_t* sb = smem + s * stage_bytes + a_bytes;
         const int kc = kb * kBlockK;
-        for (int term = 0; term < (p.hilo ? 2 : 1); ++term, sb += x_bytes) {
+        for (int term = 0; term < (HILO ? 2 : 1); ++term, sb += x_bytes) {
           const CUtensorMap* m64 = term ? &maps.xl64 : &maps.x64;
           const CUtensorMap* m16 = term ? &maps.xl16 : &maps.x16;
           int r = 0;
@@ -201,7 +201,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         for (int k = 0; k < kBlockK / 16; ++k) {
           // +32 bytes per K=16 slice inside the 128-byte swizzle row (address field in 16-byte units)
           umma_f16_ss(tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
-          if (p.hilo) umma_f16_ss(tmem, adesc + 2 * k, ldesc + 2 * k, idesc, 1u);
+          if constexpr (HILO) umma_f16_ss(tmem, adesc + 2 * k, ldesc + 2 * k, idesc, 1u);
           if constexpr (WHILO) umma_f16_ss(tmem, aldesc + 2 * k, bdesc + 2 * k, idesc, 1u);
         }
         umma_commit(&empty[s]);
@@ -280,7 +280,7 @@ static constexpr int kPersistTmemCols = 512;  // 2 accumulators x 256 columns
 static constexpr int kPEpiWarps = 16;          // 4 warps per TMEM lane quadrant, a quarter of the columns each
 static constexpr int kPThreads = 64 + 32 * kPEpiWarps;
 
-template <int ACT, bool OUT_F32, bool PAIR, bool WHILO>
+template <int ACT, bool OUT_F32, bool PAIR, bool HILO, bool WHILO>
 __global__ void __launch_bounds__(kPThreads, 1)
     gemm_persistent_kernel(const __grid_constant__ MapsOf<WHILO> maps, const GemmParams p) {
   using OutT = typename std::conditional<OUT_F32, float, half>::type;
@@ -299,7 +299,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
   const int x_rows = pair ? (p.bn >> 1) : p.bn;  // token rows staged by this CTA (per term)
   const int x_bytes = x_rows * 128;
   constexpr int a_bytes = kATileBytes * (WHILO ? 2 : 1);  // weight tile (+ its lo term)
-  const int stage_bytes = a_bytes + x_bytes * (p.hilo ? 2 : 1);
+  const int stage_bytes = a_bytes + x_bytes * (HILO ? 2 : 1);
   uint8_t* staging = smem + p.stages * stage_bytes;  // 16 warps x 16 rows x kRowBytes
   uint64_t* full = reinterpret_cast<uint64_t*>(staging + kPEpiWarps * 16 * kRowBytes);
   uint64_t* empty = full + p.stages;
@@ -390,7 +390,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
       };
       auto load_x = [&](int s, int kb, int xrow) {
         uint8_t* sb = smem + s * stage_bytes + a_bytes;
-        for (int term = 0; term < (p.hilo ? 2 : 1); ++term, sb += x_bytes) {
+        for (int term = 0; term < (HILO ? 2 : 1); ++term, sb += x_bytes) {
           const CUtensorMap* m64 = term ? &maps.xl64 : &maps.x64;
           const CUtensorMap* m16 = term ? &maps.xl16 : &maps.x16;
           int r = 0;
@@ -469,7 +469,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
 #pragma unroll
             for (int k = 0; k < kBlockK / 16; ++k) {
               umma_f16_ss_2sm(acc, adesc + 2 * k, bdesc + 2 * k, idesc, (kb > 0 || k > 0) ? 1u : 0u);
-              if (p.hilo) umma_f16_ss_2sm(acc, adesc + 2 * k, ldesc + 2 * k, idesc, 1u);
+              if constexpr (HILO) umma_f16_ss_2sm(acc, adesc + 2 * k, ldesc + 2 * k, idesc, 1u);
               if constexpr (WHILO) umma_f16_ss_2sm(acc, aldesc + 2 * k, bdesc + 2 * k, idesc, 1u);
             }
             umma_commit_2sm_mc(&empty[s], 0x3);
@@ -477,7 +477,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
 #pragma unroll
             for (int k = 0; k < kBlockK / 16; ++k) {
               umma_f16_ss(acc, adesc + 2 * k, bdesc + 2 * k, idesc, (kb > 0 || k > 0) ? 1u : 0u);
-              if (p.hilo) umma_f16_ss(acc, adesc + 2 * k, ldesc + 2 * k, idesc, 1u);
+              if constexpr (HILO) umma_f16_ss(acc, adesc + 2 * k, ldesc + 2 * k, idesc, 1u);
               if constexpr (WHILO) umma_f16_ss(acc, aldesc + 2 * k, bdesc + 2 * k, idesc, 1u);
             }
             umma_commit(&empty[s]);
@@ -555,16 +555,16 @@ __global__ void __launch_bounds__(kPThreads, 1)
   }
 }
 
-template <int ACT, bool OUT_F32, bool WHILO>
+template <int ACT, bool OUT_F32, bool HILO, bool WHILO>
 static void launch_persistent_t(const GemmMapsW& maps, const GemmParams& p, int groups, cudaStream_t stream) {
   static int n_sm = 0;
   if (n_sm == 0) {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncSetAttribute(gemm_persistent_kernel<ACT, OUT_F32, false, WHILO>,
+    cudaFuncSetAttribute(gemm_persistent_kernel<ACT, OUT_F32, false, HILO, WHILO>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    cudaFuncSetAttribute(gemm_persistent_kernel<ACT, OUT_F32, true, WHILO>,
+    cudaFuncSetAttribute(gemm_persistent_kernel<ACT, OUT_F32, true, HILO, WHILO>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
   }
   GemmParams q = p;
@@ -577,7 +577,7 @@ static void launch_persistent_t(const GemmMapsW& maps, const GemmParams& p, int 
   const int row_bytes = 32 * (OUT_F32 ? 4 : 2);
   const int x_rows = q.cluster == 2 ? p.bn / 2 : p.bn;
   const size_t smem = static_cast<size_t>(q.stages) *
-                          (kATileBytes * (WHILO ? 2 : 1) + x_rows * 128 * (p.hilo ? 2 : 1)) +
+                          (kATileBytes * (WHILO ? 2 : 1) + x_rows * 128 * (HILO ? 2 : 1)) +
                       kPEpiWarps * 16 * row_bytes + 1024 + 256;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
@@ -594,8 +594,8 @@ static void launch_persistent_t(const GemmMapsW& maps, const GemmParams& p, int 
   cfg.attrs = attr;
   cfg.numAttrs = 2;
   const MapsOf<WHILO>& m = maps;  // the BERT instantiations get the plain maps (no weight-lo map)
-  if (q.cluster == 2) cudaLaunchKernelEx(&cfg, gemm_persistent_kernel<ACT, OUT_F32, true, WHILO>, m, q);
-  else cudaLaunchKernelEx(&cfg, gemm_persistent_kernel<ACT, OUT_F32, false, WHILO>, m, q);
+  if (q.cluster == 2) cudaLaunchKernelEx(&cfg, gemm_persistent_kernel<ACT, OUT_F32, true, HILO, WHILO>, m, q);
+  else cudaLaunchKernelEx(&cfg, gemm_persistent_kernel<ACT, OUT_F32, false, HILO, WHILO>, m, q);
 }
 
 // CTA pairs (cta_group::2) halve each CTA's token-tile traffic (both (hi, lo) terms): from 256 tokens
@@ -645,21 +645,34 @@ void gemm_configure_persistent(int t_rows, bool out_f32, int units_per_tile, int
   *stages = st;
 }
 
-// (the weight-lo operand is instantiated for the dense kind's tanh projections only)
+// Operand modes are template parameters (a runtime branch in the MMA-issue loop measured 2-7 us
+// per batch-1 request): token (hi, lo) pair or hi only; the weight-lo operand is instantiated for
+// the dense kind's tanh projections only.
+template <int ACT, bool OUT_F32>
+static void launch_persistent_x(const GemmMapsW& maps, const GemmParams& p, int groups, cudaStream_t stream) {
+  if (p.hilo) launch_persistent_t<ACT, OUT_F32, true, false>(maps, p, groups, stream);
+  else launch_persistent_t<ACT, OUT_F32, false, false>(maps, p, groups, stream);
+}
+template <bool OUT_F32>
+static void launch_persistent_w(const GemmMapsW& maps, const GemmParams& p, int groups, cudaStream_t stream) {
+  if (p.hilo) launch_persistent_t<ACT_TANH, OUT_F32, true, true>(maps, p, groups, stream);
+  else launch_persistent_t<ACT_TANH, OUT_F32, false, true>(maps, p, groups, stream);
+}
+
 void launch_gemm_persistent(const GemmMapsW& maps, const GemmParams& p, int groups, cudaStream_t stream) {
   const bool f32 = p.out_f32 != 0;
   if (p.whilo) {
-    if (f32) launch_persistent_t<ACT_TANH, true, true>(maps, p, groups, stream);
-    else launch_persistent_t<ACT_TANH, false, true>(maps, p, groups, stream);
+    if (f32) launch_persistent_w<true>(maps, p, groups, stream);
+    else launch_persistent_w<false>(maps, p, groups, stream);
   } else if (p.act == ACT_GELU) {
-    if (f32) launch_persistent_t<ACT_GELU, true, false>(maps, p, groups, stream);
-    else launch_persistent_t<ACT_GELU, false, false>(maps, p, groups, stream);
+    if (f32) launch_persistent_x<ACT_GELU, true>(maps, p, groups, stream);
+    else launch_persistent_x<ACT_GELU, false>(maps, p, groups, stream);
   } else if (p.act == ACT_TANH) {
-    if (f32) launch_persistent_t<ACT_TANH, true, false>(maps, p, groups, stream);
-    else launch_persistent_t<ACT_TANH, false, false>(maps, p, groups, stream);
+    if (f32) launch_persistent_x<ACT_TANH, true>(maps, p, groups, stream);
+    else launch_persistent_x<ACT_TANH, false>(maps, p, groups, stream);
   } else {
-    if (f32) launch_persistent_t<ACT_NONE, true, false>(maps, p, groups, stream);
-    else launch_persistent_t<ACT_NONE, false, false>(maps, p, groups, stream);
+    if (f32) launch_persistent_x<ACT_NONE, true>(maps, p, groups, stream);
+    else launch_persistent_x<ACT_NONE, false>(maps, p, groups, stream);
   }
 }
 
@@ -728,11 +741,12 @@ void gemm_configure_tiles(int t_rows, int* bn, int* n_tiles, int* stages) {
   *stages = st;
 }
 
-template <int ACT, bool OUT_F32, bool WHILO>
+template <int ACT, bool OUT_F32, bool HILO, bool WHILO>
 static void launch_gemm_t(const GemmMapsW& maps, const GemmParams& p, int groups, cudaStream_t stream) {
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(gemm_kernel<ACT, OUT_F32, WHILO>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(gemm_kernel<ACT, OUT_F32, HILO, WHILO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         200 * 1024);
     attr_set = true;
   }
   cudaLaunchConfig_t cfg = {};
@@ -752,28 +766,39 @@ static void launch_gemm_t(const GemmMapsW& maps, const GemmParams& p, int groups
     g_trace_counts.push_back(static_cast<int>(cfg.gridDim.x * cfg.gridDim.y));
   }
   const MapsOf<WHILO>& m = maps;
-  cudaLaunchKernelEx(&cfg, gemm_kernel<ACT, OUT_F32, WHILO>, m, q);
+  cudaLaunchKernelEx(&cfg, gemm_kernel<ACT, OUT_F32, HILO, WHILO>, m, q);
 }
 
 // Epilogue warps of the small-T kernel: 4 (192 threads) unless the launch has several wide token
 // tiles (measured in-graph: 4 warps -1..-3 us at 96-192 tokens, 8 warps better at 256 = 2 x 128).
 int gemm_epi_warps(int bn, int n_tiles) { return (bn <= 96 || n_tiles == 1) ? 4 : 8; }
 
+template <int ACT, bool OUT_F32>
+static void launch_gemm_x(const GemmMapsW& maps, const GemmParams& p, int groups, cudaStream_t stream) {
+  if (p.hilo) launch_gemm_t<ACT, OUT_F32, true, false>(maps, p, groups, stream);
+  else launch_gemm_t<ACT, OUT_F32, false, false>(maps, p, groups, stream);
+}
+template <bool OUT_F32>
+static void launch_gemm_w(const GemmMapsW& maps, const GemmParams& p, int groups, cudaStream_t stream) {
+  if (p.hilo) launch_gemm_t<ACT_TANH, OUT_F32, true, true>(maps, p, groups, stream);
+  else launch_gemm_t<ACT_TANH, OUT_F32, false, true>(maps, p, groups, stream);
+}
+
 void launch_gemm(const GemmMapsW& maps, const GemmParams& p, int groups, cudaStream_t stream) {
   const bool f32 = p.out_f32 || p.splits > 1;
   const int act = p.splits > 1 ? ACT_NONE : p.act;
   if (p.whilo) {  // dense kind: tanh projections, one split
-    if (f32) launch_gemm_t<ACT_TANH, true, true>(maps, p, groups, stream);
-    else launch_gemm_t<ACT_TANH, false, true>(maps, p, groups, stream);
+    if (f32) launch_gemm_w<true>(maps, p, groups, stream);
+    else launch_gemm_w<false>(maps, p, groups, stream);
   } else if (act == ACT_GELU) {
-    if (f32) launch_gemm_t<ACT_GELU, true, false>(maps, p, groups, stream);
-    else launch_gemm_t<ACT_GELU, false, false>(maps, p, groups, stream);
+    if (f32) launch_gemm_x<ACT_GELU, true>(maps, p, groups, stream);
+    else launch_gemm_x<ACT_GELU, false>(maps, p, groups, stream);
   } else if (act == ACT_TANH) {
-    if (f32) launch_gemm_t<ACT_TANH, true, false>(maps, p, groups, stream);
-    else launch_gemm_t<ACT_TANH, false, false>(maps, p, groups, stream);
+    if (f32) launch_gemm_x<ACT_TANH, true>(maps, p, groups, stream);
+    else launch_gemm_x<ACT_TANH, false>(maps, p, groups, stream);
   } else {
-    if (f32) launch_gemm_t<ACT_NONE, true, false>(maps, p, groups, stream);
-    else launch_gemm_t<ACT_NONE, false, false>(maps, p, groups, stream);
+    if (f32) launch_gemm_x<ACT_NONE, true>(maps, p, groups, stream);
+    else launch_gemm_x<ACT_NONE, false>(maps, p, groups, stream);
   }
 }
 
