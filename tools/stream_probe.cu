@@ -128,6 +128,17 @@ __global__ void stream_kernel(const __grid_constant__ CUtensorMap map, const uin
   if (acc == 0xdeadbeef) *sink = acc;
 }
 
+// read the flush buffer after writing it: L2 ends holding CLEAN lines (a write-only flush leaves
+// ~126 MB of dirty lines whose write-back then competes with the measured stream)
+__global__ void read_kernel(const float4* p, long long n, float* sink) {
+  float a = 0.f;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const float4 v = p[i];
+    a += v.x + v.y + v.z + v.w;
+  }
+  if (a == 1234.5f) *sink = a;
+}
+
 int main(int argc, char** argv) {
   if (argc < 6) {
     std::printf("usage: %s rows cols ctas stages mode [reps]\n", argv[0]);
@@ -161,6 +172,7 @@ int main(int argc, char** argv) {
   std::vector<float> ts;
   for (int r = 0; r < reps + 2; ++r) {
     CK(cudaMemsetAsync(flush, r, 256ull << 20));
+    if (!getenv("DIRTY_FLUSH")) read_kernel<<<148 * 4, 256>>>((const float4*)flush, (256ll << 20) / 16, (float*)sink);
     cudaEventRecord(e0);
     stream_kernel<<<ctas, 32, smem>>>(map, (const uint8_t*)w, (int)(rows / 128), (int)(cols / 64), stages,
                                       mode == 4 ? 3 : mode, (unsigned long long*)sink);
