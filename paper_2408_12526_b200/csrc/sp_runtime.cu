@@ -800,6 +800,10 @@ int get_graph(sp_group* g, int n_tokens, int k, int add_bias, bool host, cudaGra
   e = cudaGraphInstantiate(&exec, graph, 0);
   cudaGraphDestroy(graph);
   if (e != cudaSuccess) return fail(SP_ECUDA, "graph instantiate: %s", cudaGetErrorString(e));
+  // upload now so that the bucket's first request does not pay for it
+  e = cudaGraphUpload(exec, g->cap_stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(g->cap_stream);
+  if (e != cudaSuccess) return fail(SP_ECUDA, "graph upload: %s", cudaGetErrorString(e));
   g->graph_launches = g->last_launches;
   cache[key] = exec;
   *out = exec;
