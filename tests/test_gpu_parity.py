@@ -124,6 +124,26 @@ def test_dense_group_matches_oracle(exact):
         assert rel_err_rows(grp.rep(x, k), rep_ref) <= TOL
 
 
+def test_dense_exact_weights_with_hi_only_input():
+    """C-ABI dense forward with x_lo = NULL on a group that carries weight lo terms: the
+    (token hi only, weight hi+lo) kernel instantiations, small-token and persistent paths."""
+    from oracle.dense import group_forward_weights
+    from paper_2408_12526_b200 import StudentGroup, random_dense_group
+
+    w = random_dense_group(d_in=64, rep_dim=256, depth=2, n_students=3, n_classes=2, seed=12)
+    assert w.exact_weights
+    grp = StudentGroup(w, max_tokens=512)
+    for n in (8, 40, 300):
+        x = np.random.default_rng(n).normal(size=(n, 64)).astype(np.float16).astype(np.float64)
+        x16 = torch.zeros((n, w.d_in_padded), dtype=torch.float16, device=grp.device)
+        x16[:, :64] = torch.from_numpy(x).to(torch.float16).to(grp.device)
+        logits = torch.empty((n, 2), dtype=torch.float32, device=grp.device)
+        grp.forward_dense_device(x16, n, 3, None, logits, True, x16_lo=None)
+        torch.cuda.synchronize()
+        _, z_ref = group_forward_weights(w, x, 3)
+        _check_logits(logits.cpu().numpy(), z_ref)
+
+
 def test_dense_group_wide_matches_oracle():
     """Reference-architecture students at the BERT-base width (H=768, K=8)."""
     from oracle.dense import group_forward_weights
