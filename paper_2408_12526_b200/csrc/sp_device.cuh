@@ -84,8 +84,9 @@ __device__ __forceinline__ int seq_of(const int* cu, int n_seqs, int t) {
 }
 
 // Each lane owns NC chunks of 4 consecutive features: feature = c*128 + lane*4 + j.
-// Writes the fp32 residual stream x32 and the (hi, lo) fp16 GEMM operand (lo at x16 + x_lo_off),
-// plus the same pair for the CLS row (cls16, cls16 + cls_lo_off) when cls16 is set.
+// Writes the (hi, lo) fp16 pair (lo at x16 + x_lo_off) — both the next GEMM's operand and the
+// residual stream (hi + lo carries ~22 significant bits) — plus fp32 rows to x32 when set (the
+// last layer's CLS rows), and the same pair for the CLS row (cls16, cls16 + cls_lo_off) when set.
 template <int NC>
 __device__ __forceinline__ void layer_norm_store(float (&v)[NC][4], const float* gamma, const float* beta, float eps,
                                                  int hidden, float* x32, half* x16, long long x_lo_off, half* cls16,
@@ -120,7 +121,7 @@ __device__ __forceinline__ void layer_norm_store(float (&v)[NC][4], const float*
     y.y = (v[c][1] - mean) * rstd * gm[c].y + bt[c].y;
     y.z = (v[c][2] - mean) * rstd * gm[c].z + bt[c].z;
     y.w = (v[c][3] - mean) * rstd * gm[c].w + bt[c].w;
-    *reinterpret_cast<float4*>(x32 + f) = y;
+    if (x32) *reinterpret_cast<float4*>(x32 + f) = y;
     uint2 hi, lo;
     split_half2(y.x, y.y, hi.x, lo.x);
     split_half2(y.z, y.w, hi.y, lo.y);

@@ -155,10 +155,12 @@ struct RowLn {
   int splits;
   long long part_ss, part_gs;
   const float *bias, *gamma, *beta;  // [groups][hidden], already at the layer
-  const float* x_in;
+  const float* x_in;   // fp32 residual, or null: the residual is the (hi, lo) pair x_in16 (+ x_in16_lo)
+  const half* x_in16;
+  long long x_in16_lo;
   long long in_gs;
   const int* in_rows;  // residual row of output row t (the CLS rows: cu_seqlens), or null
-  float* x_out;
+  float* x_out;        // fp32 output rows, or null (the (hi, lo) output is the residual stream)
   long long out_gs;
   half* x16;
   long long x16_gs, x_lo_off;

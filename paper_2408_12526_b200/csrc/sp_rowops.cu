@@ -51,15 +51,16 @@ __global__ void __launch_bounds__(128)
     for (int j = 0; j < 4; ++j) v[c][j] = a[j] + bb[j] + cc[j];
   }
   const long long row = (long long)g * x_gs + (long long)t * hidden;
-  layer_norm_store<NC>(v, gamma + (long long)g * hidden, beta + (long long)g * hidden, eps, hidden, x32 + row,
-                       x16 + row, x_lo_off, nullptr, 0);
+  layer_norm_store<NC>(v, gamma + (long long)g * hidden, beta + (long long)g * hidden, eps, hidden,
+                       x32 ? x32 + row : nullptr, x16 + row, x_lo_off, nullptr, 0);
 }
 
 // SPLITS: number of split-K partials, a template parameter so only the live ones hold registers
 // (4 x NC float4 partials capped occupancy at 4 blocks/SM when the persistent path writes one).
 // Row t: x_out[t] = LN(x_in[in_rows ? in_rows[t] : t] + b + sum_s part[s][t]); the (hi, lo) operand
 // to x16; the CLS rows of the sequences also to cls16 (when set).
-template <int NC, int SPLITS>
+// RES16: the residual is the (hi, lo) fp16 stream (x_in16), else the fp32 rows x_in.
+template <int NC, int SPLITS, bool RES16>
 __global__ void __launch_bounds__(128) reduce_ln_kernel(const RowLn a) {
   // request inputs (cu_seqlens) and weights (bias) are read before the dependency wait
   pdl_launch_dependents();
@@ -79,14 +80,21 @@ __global__ void __launch_bounds__(128) reduce_ln_kernel(const RowLn a) {
     if (__ldg(a.cu + b) == t) cls_row = a.cls16 + (long long)g * a.cls_gs + (long long)b * hidden;
   }
   const int t_in = a.in_rows ? __ldg(a.in_rows + t) : t;
-  const float* x_in = a.x_in + (long long)g * a.in_gs + (long long)t_in * hidden;
+  const long long in_row = (long long)g * a.in_gs + (long long)t_in * hidden;
   const float* part = a.part + (long long)g * a.part_gs + (long long)t * hidden;
   pdl_wait();
   // then every load of the row at once: residual and up to kMaxSplitsRow partial sums
 #pragma unroll
   for (int c = 0; c < NC; ++c) {
     const int f = c * 128 + lane * 4;
-    r[c] = *reinterpret_cast<const float4*>(x_in + f);
+    if constexpr (RES16) {  // residual = the (hi, lo) stream itself (~22 significant bits)
+      float h[4], l[4];
+      h4_to_f4(*reinterpret_cast<const uint2*>(a.x_in16 + in_row + f), h);
+      h4_to_f4(*reinterpret_cast<const uint2*>(a.x_in16 + a.x_in16_lo + in_row + f), l);
+      r[c] = make_float4(h[0] + l[0], h[1] + l[1], h[2] + l[2], h[3] + l[3]);
+    } else {
+      r[c] = *reinterpret_cast<const float4*>(a.x_in + in_row + f);
+    }
 #pragma unroll
     for (int s = 0; s < SPLITS; ++s) pv[s][c] = *reinterpret_cast<const float4*>(part + s * a.part_ss + f);
   }
@@ -106,7 +114,7 @@ __global__ void __launch_bounds__(128) reduce_ln_kernel(const RowLn a) {
     }
   }
   layer_norm_store<NC>(v, a.gamma + (long long)g * hidden, a.beta + (long long)g * hidden, a.eps, hidden,
-                       a.x_out + (long long)g * a.out_gs + (long long)t * hidden,
+                       a.x_out ? a.x_out + (long long)g * a.out_gs + (long long)t * hidden : nullptr,
                        a.x16 + (long long)g * a.x16_gs + (long long)t * hidden, a.x_lo_off, cls_row, a.cls_lo_off);
 }
 
@@ -237,7 +245,11 @@ void launch_reduce_ln(const RowLn& a, int groups, cudaStream_t stream) {
   if (a.n_rows == 0 || groups <= 0) return;
   // n_rows < 0: grid sized for -n_rows rows, live count read from cu_seqlens (graph replay)
   dim3 grid(((a.n_rows < 0 ? -a.n_rows : a.n_rows) + 3) / 4, groups);
-#define SP_REDUCE_S(NC_, S_) launch_pdl(reduce_ln_kernel<NC_, S_>, grid, dim3(128), 0, stream, a)
+#define SP_REDUCE_S(NC_, S_)                                                             \
+  do {                                                                                   \
+    if (a.x_in16) launch_pdl(reduce_ln_kernel<NC_, S_, true>, grid, dim3(128), 0, stream, a); \
+    else launch_pdl(reduce_ln_kernel<NC_, S_, false>, grid, dim3(128), 0, stream, a);    \
+  } while (0)
 #define SP_REDUCE(NC_)                     \
   do {                                     \
     if (a.splits <= 1) SP_REDUCE_S(NC_, 1);  \

@@ -122,7 +122,6 @@ struct sp_group {
   int device = 0;
   int rows_cap = 0;  // max(max_tokens, max_seqs)
   // workspace; "[2]" planes are the (hi, lo) terms of a GEMM operand, lo at +*_lo elements
-  float* x32 = nullptr;    // [S][max_tokens][H] residual stream (fp32)
   half* x16 = nullptr;     // [2][S][max_tokens][H] LayerNorm output (QKV / FFN1 operand)
   half* qkv = nullptr;     // [S][max_tokens][3H]
   half* ctx = nullptr;     // [2][S][max_tokens][H] attention context (O operand)
@@ -332,7 +331,6 @@ int sp_group_create(const sp_config* cfg, const sp_weights* weights, int device,
     g->ctx_lo = g->x_lo;
     g->ffn_lo = (long long)(S * T * F);
     g->cls_lo = (long long)(S * B * H);
-    if ((rc = dev_alloc(g, &g->x32, S * T * H))) return bail(rc);
     if ((rc = dev_alloc(g, &g->x16, 2 * S * T * H))) return bail(rc);
     if ((rc = dev_alloc(g, &g->qkv, S * T * 3 * H))) return bail(rc);
     if ((rc = dev_alloc(g, &g->ctx, 2 * S * T * H))) return bail(rc);
@@ -606,11 +604,11 @@ int bert_forward(sp_group* g, const int32_t* ids, const int32_t* cu, int n_seqs,
   g->rec_reset(st);
   if (k > 0) {
     const double GTH = (double)k * n_tokens * H;
-    g->rec_begin(SP_LAUNCH_EMBED_LN, GTH * 12.0, 0.0);
+    g->rec_begin(SP_LAUNCH_EMBED_LN, GTH * 8.0, 0.0);
     sp::launch_embed_ln(ids, cu, n_seqs, n_rows_arg, k, static_cast<const half*>(w.word_emb),
                         static_cast<const half*>(w.pos_emb), static_cast<const half*>(w.type_emb),
                         (long long)c.vocab * H, (long long)c.max_pos * H, w.emb_ln_gamma, w.emb_ln_beta, H, c.ln_eps,
-                        g->x32, g->x16, xgs, g->x_lo, st);
+                        nullptr, g->x16, xgs, g->x_lo, st);
     g->rec_end();
     ++launches;
     int bn, n_tiles, stages;
@@ -644,6 +642,10 @@ int bert_forward(sp_group* g, const int32_t* ids, const int32_t* cu, int n_seqs,
       a.gamma = g_;
       a.beta = be_;
       a.x_in = x_in;
+      if (x_in == nullptr) {  // residual = the (hi, lo) stream itself (no separate fp32 copy)
+        a.x_in16 = g->x16;
+        a.x_in16_lo = g->x_lo;
+      }
       a.in_gs = in_gs;
       a.in_rows = in_rows;
       a.x_out = x_out;
@@ -656,7 +658,8 @@ int bert_forward(sp_group* g, const int32_t* ids, const int32_t* cu, int n_seqs,
       a.n_rows = n_rows;
       a.cu = cu;
       a.n_seqs = n_seqs;
-      g->rec_begin(SP_LAUNCH_REDUCE_LN, rows * H * (4.0 * splits + 12.0), 0.0);
+      // bytes: partials + residual (4 B: fp32 or the fp16 pair) + (hi, lo) out (+ fp32 out)
+      g->rec_begin(SP_LAUNCH_REDUCE_LN, rows * H * (4.0 * splits + 8.0 + (x_out ? 4.0 : 0.0)), 0.0);
       sp::launch_reduce_ln(a, k, st);
       g->rec_end();
       ++launches;
@@ -689,7 +692,7 @@ int bert_forward(sp_group* g, const int32_t* ids, const int32_t* cu, int n_seqs,
         run_gemm(g, SP_LAUNCH_GEMM_O, g->m_o[l], g->xm_ctxc, k, H, H, n_seqs, B, nullptr, H, sp::ACT_NONE, g->partc,
                  bgs, 0, 1, s_oc, partc_ss, st);
         ++launches;
-        layer_norm(g->partc, s_oc, partc_ss, bgs, w.b_o + lS * H, w.ln1_gamma + lS * H, w.ln1_beta + lS * H, g->x32,
+        layer_norm(g->partc, s_oc, partc_ss, bgs, w.b_o + lS * H, w.ln1_gamma + lS * H, w.ln1_beta + lS * H, nullptr,
                    xgs, cu, g->xc32, bgs, g->cln, bgs, g->cls_lo, n_seqs, GBH);
         run_gemm(g, SP_LAUNCH_GEMM_FFN1, g->m_f1[l], g->xm_cln, k, F, H, n_seqs, B, w.b_ffn1 + lS * F, F,
                  sp::ACT_GELU, g->ffnc, (long long)B * F, g->cf_lo, 0, 1, 0, st);
@@ -708,8 +711,8 @@ int bert_forward(sp_group* g, const int32_t* ids, const int32_t* cu, int n_seqs,
       run_gemm(g, SP_LAUNCH_GEMM_O, g->m_o[l], g->xm_ctx, k, H, H, n_tokens, T, nullptr, H, sp::ACT_NONE, g->part, xgs,
                0, 1, s_o, part_ss, st, t_dev);
       launches += 2;
-      layer_norm(g->part, s_o, part_ss, xgs, w.b_o + lS * H, w.ln1_gamma + lS * H, w.ln1_beta + lS * H, g->x32, xgs,
-                 nullptr, g->x32, xgs, g->x16, xgs, g->x_lo, n_rows_arg, GTH);
+      layer_norm(g->part, s_o, part_ss, xgs, w.b_o + lS * H, w.ln1_gamma + lS * H, w.ln1_beta + lS * H, nullptr, xgs,
+                 nullptr, nullptr, xgs, g->x16, xgs, g->x_lo, n_rows_arg, GTH);
       // FFN1 + FFN2 as one persistent kernel where both would take the single-CTA persistent path
       // (only where FFN2 itself would be a one-split persistent GEMM: measured -2% at L=512, but
       // +3% at L=256 where FFN2's split-K tiles beat the fused kernel's 96-token phase-B tiles)
@@ -727,8 +730,8 @@ int bert_forward(sp_group* g, const int32_t* ids, const int32_t* cu, int n_seqs,
                  g->part, xgs, 0, 1, s_f, part_ss, st, t_dev);
         launches += 2;
       }
-      layer_norm(g->part, s_ln2, part_ss, xgs, w.b_ffn2 + lS * H, w.ln2_gamma + lS * H, w.ln2_beta + lS * H, g->x32,
-                 xgs, nullptr, g->x32, xgs, g->x16, xgs, g->x_lo, n_rows_arg, GTH,
+      layer_norm(g->part, s_ln2, part_ss, xgs, w.b_ffn2 + lS * H, w.ln2_gamma + lS * H, w.ln2_beta + lS * H, nullptr,
+                 xgs, nullptr, nullptr, xgs, g->x16, xgs, g->x_lo, n_rows_arg, GTH,
                  split_q && l == c.n_layers - 2 ? g->cls16 : nullptr);
     }
     // pooler on the CLS rows: tanh(W_p h_CLS + b_p). Few rows: split-K partials (more CTAs stream the
