@@ -235,25 +235,35 @@ __global__ void __launch_bounds__(kThreads, 2)
     tc_fence_after();
     if (tr && warp == 2 && lane == 0) tr[6] = globaltimer();
     const uint32_t taddr = tmem + (static_cast<uint32_t>(q * 32) << 16);
-    for (int c = c_begin; c < c_begin + half_cols; c += 32) {
-      const int n = min(32, c_begin + half_cols - c);  // multiple of 8, warp-uniform
-      uint32_t r[32];
-      if (n == 32) {
-        tmem_ld32_nowait(taddr + c, r);
+    const long long lo_off = OUT_F32 ? 0 : p.out_lo_off;
+    // one chunk of NR accumulator columns (NR = 8 / 16 / 32 >= n: a 16-token tile computes its
+    // activation for 16 columns, not 32; the columns of a chunk are independent chains)
+    auto chunk = [&](auto nr, int c, int n) {
+      constexpr int NR = decltype(nr)::value;
+      uint32_t r[NR];
+      if constexpr (NR == 32) {
+        if (n == 32) tmem_ld32_nowait(taddr + c, r);
+        else
+          for (int i = 0; i < n; i += 8) tmem_ld8_nowait(taddr + c + i, r + i);
       } else {
-        for (int i = 0; i < n; i += 8) tmem_ld8_nowait(taddr + c + i, r + i);
+#pragma unroll
+        for (int i = 0; i < NR; i += 8) tmem_ld8_nowait(taddr + c + i, r + i);
       }
       tmem_wait_ld();
-      // all 32 columns unconditionally: independent chains interleave (rows >= n are never stored)
-      float y[32];
+      float y[NR];
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
+      for (int j = 0; j < NR; ++j) {
         y[j] = has_k ? __uint_as_float(r[j]) : 0.f;
         if (!partial) y[j] = apply_act<ACT>(y[j] + bias);
       }
-      warp_store_rows<OutT, 32>(y, n, stage, out, n0 + c, t_rows, p.out_ld, false);
-      if (!OUT_F32 && p.out_lo_off)
-        warp_store_rows<OutT, 32>(y, n, stage, out + p.out_lo_off, n0 + c, t_rows, p.out_ld, true);
+      warp_store_rows<OutT, NR>(y, n, stage, out, n0 + c, t_rows, p.out_ld, false);
+      if (lo_off) warp_store_rows<OutT, NR>(y, n, stage, out + lo_off, n0 + c, t_rows, p.out_ld, true);
+    };
+    for (int c = c_begin; c < c_begin + half_cols; c += 32) {
+      const int n = min(32, c_begin + half_cols - c);  // multiple of 8, warp-uniform
+      if (n > 16) chunk(std::integral_constant<int, 32>{}, c, n);
+      else if (n > 8) chunk(std::integral_constant<int, 16>{}, c, n);
+      else chunk(std::integral_constant<int, 8>{}, c, n);
     }
     if (tr && warp == 2 && lane == 0) tr[7] = globaltimer();
   }
@@ -504,6 +514,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
     const int c_begin = (e >> 2) * part_cols;
     OutT* stage = reinterpret_cast<OutT*>(staging + e * 16 * kRowBytes);
     const int t_rows = p.t_dev ? __ldg(p.t_dev) : p.t_rows;
+    const long long lo_off = OUT_F32 ? 0 : p.out_lo_off;
     // accumulator release: local barrier, or the leader's through the cluster window
     uint32_t acc_empty_leader0 = 0u;
     if constexpr (PAIR) acc_empty_leader0 = mapa_shared(smem_u32(&acc_empty[0]), 0);
@@ -520,13 +531,14 @@ __global__ void __launch_bounds__(kPThreads, 1)
       tc_fence_after();
       if (tr && j == 0 && warp == 2 && lane == 0) tr[6] = globaltimer();
       const uint32_t taddr = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(b * 256);
-      for (int c = c_begin; c < c_begin + part_cols; c += 16) {
-        const int n = min(16, c_begin + part_cols - c);  // 8 or 16
-        uint32_t r[16];
-        tmem_ld8_nowait(taddr + c, r);
-        if (n == 16) tmem_ld8_nowait(taddr + c + 8, r + 8);
+      // chunks of 16 columns (the last may be 8: computed at width 8, not 16)
+      auto chunk = [&](auto nr, int c) {
+        constexpr int NR = decltype(nr)::value;
+        uint32_t r[NR];
+#pragma unroll
+        for (int i = 0; i < NR; i += 8) tmem_ld8_nowait(taddr + c + i, r + i);
         tmem_wait_ld();
-        if (c + 16 >= c_begin + part_cols) {  // last TMEM read of this tile: hand the accumulator back
+        if (c + NR >= c_begin + part_cols) {  // last TMEM read of this tile: hand the accumulator back
           tc_fence_before();
           __syncwarp();
           if (lane == 0) {
@@ -534,12 +546,15 @@ __global__ void __launch_bounds__(kPThreads, 1)
             else mbar_arrive(&acc_empty[b]);
           }
         }
-        float y[16];
+        float y[NR];
 #pragma unroll
-        for (int jj = 0; jj < 16; ++jj) y[jj] = apply_act<ACT>(__uint_as_float(r[jj]) + bias);
-        warp_store_rows<OutT, 16>(y, n, stage, out, n0 + c, t_rows, p.out_ld, false);
-        if (!OUT_F32 && p.out_lo_off)
-          warp_store_rows<OutT, 16>(y, n, stage, out + p.out_lo_off, n0 + c, t_rows, p.out_ld, true);
+        for (int jj = 0; jj < NR; ++jj) y[jj] = apply_act<ACT>(__uint_as_float(r[jj]) + bias);
+        warp_store_rows<OutT, NR>(y, NR, stage, out, n0 + c, t_rows, p.out_ld, false);
+        if (lo_off) warp_store_rows<OutT, NR>(y, NR, stage, out + lo_off, n0 + c, t_rows, p.out_ld, true);
+      };
+      for (int c = c_begin; c < c_begin + part_cols; c += 16) {
+        if (c_begin + part_cols - c >= 16) chunk(std::integral_constant<int, 16>{}, c);
+        else chunk(std::integral_constant<int, 8>{}, c);
       }
     }
     if (tr && warp == 2 && lane == 0) tr[7] = globaltimer();

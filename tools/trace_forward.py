@@ -2,7 +2,8 @@
 import sys, numpy as np, torch
 sys.path.insert(0, ".")
 from paper_2408_12526_b200 import PRESETS, StudentGroup, random_bert_group, _lib
-cfg, K = PRESETS["base"]
+import os
+cfg, K = PRESETS[os.environ.get("PRESET", "base")]
 w = random_bert_group(cfg, K, seed=0)
 g = StudentGroup(w, max_tokens=512, max_seqs=1)
 lib = _lib.load()
