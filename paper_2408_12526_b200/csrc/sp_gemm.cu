@@ -166,6 +166,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       if (tr) tr[2] = globaltimer();
       // activations are produced by the previous kernel
       pdl_wait();
+      if (tr) tr[3] = globaltimer();  // dependency released
       for (int i = 0; i < n_pre; ++i) load_x(i, kb0 + i);
       int s = n_pre % p.stages;
       uint32_t ph = (n_pre == p.stages) ? 1u : 0u;
@@ -181,7 +182,6 @@ __global__ void __launch_bounds__(kThreads, 2)
           ph ^= 1;
         }
       }
-      if (tr) tr[3] = globaltimer();
     }
   } else if (warp == 1) {
     if (elect_one()) {

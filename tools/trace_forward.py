@@ -45,4 +45,4 @@ for L in [int(x) for x in sys.argv[1].split(",")]:
         if len(seg) == 0:
             continue
         print(f"  {nm:5s} ctas={n:4d} entry[{seg[:,0].min():6.1f},{seg[:,0].max():6.1f}] wpre={np.median(seg[:,2]):6.1f} mma0={np.median(seg[:,4]):6.1f} "
-              f"last_commit={seg[:,5].max():6.1f} epi0_max={seg[:,6].max():6.1f} end={seg[:,7].max():6.1f}")
+              f"dep={np.median(seg[:,3]):6.1f} last_commit={seg[:,5].max():6.1f} epi0_max={seg[:,6].max():6.1f} end={seg[:,7].max():6.1f}")
