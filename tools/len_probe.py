@@ -6,7 +6,7 @@ if os.environ.get("SP_LIB_OVERRIDE"):  # A/B another build of the engine library
     import paper_2408_12526_b200._lib as _L
     _L.LIB_PATH = Path(os.environ["SP_LIB_OVERRIDE"])
 from paper_2408_12526_b200 import PRESETS, StudentGroup, random_bert_group
-cfg, K = PRESETS["base"]
+cfg, K = PRESETS[os.environ.get("PRESET", "base")]
 g = StudentGroup(random_bert_group(cfg, K, seed=0), max_tokens=512, max_seqs=1)
 fw = torch.empty(256 << 18, device="cuda"); fr = torch.ones(256 << 18, device="cuda")
 logits = torch.empty(1, 2, device="cuda")
