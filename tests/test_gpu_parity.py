@@ -108,6 +108,23 @@ def test_tiny_bert_host_api_matches_device_api(tiny):
     np.testing.assert_array_equal(z_host, z_dev.astype(np.float32))  # same kernels, same order: bit-identical
 
 
+def test_torch_op_host_path_matches_forward_host(tiny):
+    """torch.ops.studentpar.group_forward_host (the C++ extension over the same C entry point) and
+    StudentGroup.forward_host (direct C call) return bit-identical logits."""
+    from paper_2408_12526_b200.group import pack_sequences, torch_ops
+
+    grp, _ = tiny
+    ops = torch_ops()
+    assert ops is not None, "the torch extension library was not built"
+    for seqs in (_seqs(np.random.default_rng(5), 1, 8, 64), _seqs(np.random.default_rng(6), 3, 8, 64)):
+        ids, cu, _ = pack_sequences(seqs)
+        z = grp.forward_host(ids, cu, 3)
+        out = torch.empty((len(cu) - 1, grp.n_classes), dtype=torch.float32)
+        ops.group_forward_host(grp._handle.value, torch.from_numpy(ids), torch.from_numpy(cu), 3, out, True,
+                               grp.device.index)
+        np.testing.assert_array_equal(out.numpy(), z)
+
+
 @pytest.mark.parametrize("exact", [True, False])
 def test_dense_group_matches_oracle(exact):
     """exact=True: fp16 (hi, lo) weights (3 products per k-slice); exact=False: fp16 weights only."""
