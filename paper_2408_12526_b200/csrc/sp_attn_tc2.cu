@@ -397,21 +397,33 @@ void launch_attention_tc2(const CUtensorMap& map_qkv, half* ctx, long long lo_of
 // CTAs (L <= 512: 4 query tiles x 96 heads = 384) run in one wave. Because S_j is issued after
 // PV_{j-1}, scores ready implies the previous PV finished: the softmax may rescale O right away.
 // Thread = query row (4 softmax warps), 64 keys per chunk; producer warp, MMA warp.
+// D (head_dim) = 64: 128-byte rows, SWIZZLE_128B; D = 32 (the tiny config): 64-byte rows,
+// SWIZZLE_64B, half the K steps of S = Q K^T and an N = 32 P V product.
 namespace {
-constexpr int kKv64 = 64 * 64 * 2;  // 64 keys x 64 dims fp16 = 8 KiB
 constexpr int kT3Threads = 192;
 constexpr uint32_t k3ColS = 0, k3ColO = 64;
+template <int D>
+struct T3 {
+  static constexpr int kQ = 128 * D * 2;   // query tile
+  static constexpr int kKv = 64 * D * 2;   // one 64-key chunk of K (or V)
+  static __device__ __forceinline__ uint64_t desc(uint32_t a) {
+    return D == 64 ? umma_sdesc_sw128(a) : umma_sdesc_sw64(a);
+  }
+};
 }  // namespace
 
+template <int D>
 __global__ void __launch_bounds__(kT3Threads, 3)
     attn_tc3_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_kv,
                     half* __restrict__ ctx, const int* __restrict__ cu, int n_heads, int hidden, long long group_rows,
                     float scale_log2, long long lo_off) {
+  static_assert(D == 64 || D == 32, "head_dim 64 or 32");
+  constexpr int kKv64 = T3<D>::kKv;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sQ = smem;                 // 16 KiB
-  uint8_t* sK = sQ + kTile;           // [2] x 8 KiB
-  uint8_t* sV = sK + 2 * kKv64;       // [2] x 8 KiB
+  uint8_t* sQ = smem;                 // 16 KiB (D = 64) / 8 KiB
+  uint8_t* sK = sQ + T3<D>::kQ;       // [2] x 8 / 4 KiB
+  uint8_t* sV = sK + 2 * kKv64;       // [2] x 8 / 4 KiB
   uint64_t* bars = reinterpret_cast<uint64_t*>(sV + 2 * kKv64);
   uint64_t* q_full = bars;
   uint64_t* kv_full = bars + 1;   // [2]
@@ -461,29 +473,30 @@ __global__ void __launch_bounds__(kT3Threads, 3)
     if (elect_one()) {
       const uint64_t pol = policy_evict_last();
       pdl_wait();  // qkv is the previous kernel's output
-      mbar_arrive_expect_tx(q_full, kTile);
-      tma_load_2d(&map_q, q_full, sQ, h * 64, row_base + q0, pol);
+      mbar_arrive_expect_tx(q_full, T3<D>::kQ);
+      tma_load_2d(&map_q, q_full, sQ, h * D, row_base + q0, pol);
       for (int j = 0; j < n_chunks; ++j) {
         const int st = j & 1;
         if (j >= 2) mbar_wait(&kv_empty[st], ((j >> 1) - 1) & 1);
         mbar_arrive_expect_tx(&kv_full[st], 2 * kKv64);
-        tma_load_2d(&map_kv, &kv_full[st], sK + st * kKv64, hidden + h * 64, row_base + j * 64, pol);
-        tma_load_2d(&map_kv, &kv_full[st], sV + st * kKv64, 2 * hidden + h * 64, row_base + j * 64, pol);
+        tma_load_2d(&map_kv, &kv_full[st], sK + st * kKv64, hidden + h * D, row_base + j * 64, pol);
+        tma_load_2d(&map_kv, &kv_full[st], sV + st * kKv64, 2 * hidden + h * D, row_base + j * 64, pol);
       }
     }
     __syncwarp();
   } else if (warp == kMma3) {
     if (elect_one()) {
       const uint32_t idesc_s = umma_idesc_f16(128, 64);
-      const uint32_t idesc_o = umma_idesc_f16(128, 64) | (1u << 16);  // B (= V) is MN-major
-      const uint64_t qdesc = umma_sdesc_sw128(smem_u32(sQ));
+      const uint32_t idesc_o = umma_idesc_f16(128, D) | (1u << 16);  // B (= V) is MN-major
+      const uint64_t qdesc = T3<D>::desc(smem_u32(sQ));
       mbar_wait(q_full, 0);
       auto issue_s = [&](int j) {
         mbar_wait(&kv_full[j & 1], (j >> 1) & 1);
         tc_fence_after();
-        const uint64_t kdesc = umma_sdesc_sw128(smem_u32(sK + (j & 1) * kKv64));
+        const uint64_t kdesc = T3<D>::desc(smem_u32(sK + (j & 1) * kKv64));
 #pragma unroll
-        for (int k = 0; k < 4; ++k) umma_f16_ss(tmem + k3ColS, qdesc + 2 * k, kdesc + 2 * k, idesc_s, k > 0 ? 1u : 0u);
+        for (int k = 0; k < D / 16; ++k)
+          umma_f16_ss(tmem + k3ColS, qdesc + 2 * k, kdesc + 2 * k, idesc_s, k > 0 ? 1u : 0u);
         umma_commit(s_full);
       };
       issue_s(0);
@@ -493,7 +506,7 @@ __global__ void __launch_bounds__(kT3Threads, 3)
         const uint8_t* vb = sV + (j & 1) * kKv64;
 #pragma unroll
         for (int k = 0; k < 4; ++k)  // 16 keys per step: P columns 8k.. (2 fp16 each), V rows 16k..
-          umma_f16_ts(tmem + k3ColO, tmem + k3ColS + 8 * k, umma_sdesc_sw128(smem_u32(vb + k * 2048)), idesc_o,
+          umma_f16_ts(tmem + k3ColO, tmem + k3ColS + 8 * k, T3<D>::desc(smem_u32(vb + k * 16 * D * 2)), idesc_o,
                       (j > 0 || k > 0) ? 1u : 0u);
         umma_commit(pv_done);
         umma_commit(&kv_empty[j & 1]);
@@ -558,7 +571,7 @@ __global__ void __launch_bounds__(kT3Threads, 3)
       l += ps;
       if (j >= 1 && __any_sync(0xffffffffu, alpha != 1.f)) {  // rare: rescale this warp's O rows
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
+        for (int c = 0; c < D / 16; ++c) {
           uint32_t o[16];
           tmem_ld16_nowait(tmem + lane_base + k3ColO + 16 * c, o);
           tmem_wait_ld();
@@ -576,11 +589,11 @@ __global__ void __launch_bounds__(kT3Threads, 3)
     if (live) {
       tc_fence_after();
       const float inv = 1.f / l;
-      uint4* out = reinterpret_cast<uint4*>(ctx + (static_cast<long long>(row_base) + q0 + row) * hidden + h * 64);
+      uint4* out = reinterpret_cast<uint4*>(ctx + (static_cast<long long>(row_base) + q0 + row) * hidden + h * D);
       uint4* out_lo = reinterpret_cast<uint4*>(ctx + lo_off + (static_cast<long long>(row_base) + q0 + row) * hidden +
-                                               h * 64);
+                                               h * D);
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {  // 16 output columns at a time
+      for (int c = 0; c < D / 16; ++c) {  // 16 output columns at a time
         uint32_t o[16];
         tmem_ld16_nowait(tmem + lane_base + k3ColO + 16 * c, o);
         tmem_wait_ld();
@@ -607,22 +620,36 @@ __global__ void __launch_bounds__(kT3Threads, 3)
   }
 }
 
-size_t attn_tc3_smem_bytes() { return 1024 + kTile + 4 * kKv64 + 128; }
+size_t attn_tc3_smem_bytes(int head_dim) {
+  return 1024 + (size_t)128 * head_dim * 2 + 4 * (size_t)64 * head_dim * 2 + 128;
+}
+
+template <int D>
+static void launch_tc3_t(const CUtensorMap& map_q, const CUtensorMap& map_kv, half* ctx, long long lo_off,
+                         const int* cu_seqlens, int n_seqs, int max_len, int groups, int n_heads, int hidden,
+                         long long group_rows, cudaStream_t stream) {
+  static bool attr_set = false;
+  const size_t smem = attn_tc3_smem_bytes(D);
+  if (!attr_set) {
+    cudaFuncSetAttribute(attn_tc3_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    attr_set = true;
+  }
+  const float scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(D));
+  dim3 grid(groups * n_heads, n_seqs, (max_len + 127) / 128);
+  launch_pdl(attn_tc3_kernel<D>, grid, dim3(kT3Threads), smem, stream, map_q, map_kv, ctx, cu_seqlens, n_heads, hidden,
+             group_rows, scale_log2, lo_off);
+}
 
 void launch_attention_tc3(const CUtensorMap& map_q, const CUtensorMap& map_kv, half* ctx, long long lo_off,
                           const int* cu_seqlens, int n_seqs, int max_len, int groups, int n_heads, int hidden,
                           long long group_rows, cudaStream_t stream) {
   if (n_seqs <= 0 || max_len <= 0 || groups <= 0) return;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(attn_tc3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(attn_tc3_smem_bytes()));
-    attr_set = true;
-  }
-  const float scale_log2 = 1.4426950408889634f / 8.0f;
-  dim3 grid(groups * n_heads, n_seqs, (max_len + 127) / 128);
-  launch_pdl(attn_tc3_kernel, grid, dim3(kT3Threads), attn_tc3_smem_bytes(), stream, map_q, map_kv, ctx, cu_seqlens,
-             n_heads, hidden, group_rows, scale_log2, lo_off);
+  if (hidden / n_heads == 32)
+    launch_tc3_t<32>(map_q, map_kv, ctx, lo_off, cu_seqlens, n_seqs, max_len, groups, n_heads, hidden, group_rows,
+                     stream);
+  else
+    launch_tc3_t<64>(map_q, map_kv, ctx, lo_off, cu_seqlens, n_seqs, max_len, groups, n_heads, hidden, group_rows,
+                     stream);
 }
 
 }  // namespace sp

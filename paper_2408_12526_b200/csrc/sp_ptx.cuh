@@ -268,6 +268,18 @@ __device__ __forceinline__ uint64_t umma_sdesc_sw128(uint32_t smem_addr) {
   return d;
 }
 
+// The same for 64-byte rows (32 fp16): SWIZZLE_64B atoms of 8 rows x 64 B, so SBO = 512 B
+// (K-major; and MN-major with the MN extent one atom wide, where LBO is unused).
+__device__ __forceinline__ uint64_t umma_sdesc_sw64(uint32_t smem_addr) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((smem_addr >> 4) & 0x3FFFu);
+  d |= static_cast<uint64_t>(1u) << 16;            // LBO (unused)
+  d |= static_cast<uint64_t>(512u >> 4) << 32;     // SBO
+  d |= static_cast<uint64_t>(1u) << 46;            // descriptor version (sm_100)
+  d |= static_cast<uint64_t>(4u) << 61;            // SWIZZLE_64B
+  return d;
+}
+
 // TMEM -> registers: 32 lanes x 32 bit, 16 consecutive columns per thread.
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
   uint32_t r[16];

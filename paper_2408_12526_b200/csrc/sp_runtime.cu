@@ -58,16 +58,18 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 // fp16 row-major [rows, cols] viewed as a 2-D tensor map with a {64, box_rows} box, 128-B swizzle.
-bool make_map(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+// box_cols 64 (128-byte rows, SWIZZLE_128B) or 32 (64-byte rows, SWIZZLE_64B: head_dim-32 attention)
+bool make_map(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols, uint32_t box_rows,
+              uint32_t box_cols = 64) {
   auto fn = encode_fn();
   if (fn == nullptr || ptr == nullptr || rows == 0) return false;
   cuuint64_t dims[2] = {cols, rows};
   cuuint64_t strides[1] = {cols * 2};
-  cuuint32_t box[2] = {64, box_rows};
+  cuuint32_t box[2] = {box_cols, box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, box_cols == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
 
@@ -368,8 +370,9 @@ int sp_group_create(const sp_config* cfg, const sp_weights* weights, int device,
     ok &= make_xmaps(&g->xm_cln, g->cln, g->cln + g->cls_lo, S * B, H);
     ok &= make_xmaps(&g->xm_ctxc, g->ctxc, g->ctxc + g->cls_lo, S * B, H);
     ok &= make_xmaps(&g->xm_ffnc, g->ffnc, g->ffnc + g->cf_lo, S * B, F);
-    ok &= make_map(&g->m_qkv_attn, g->qkv, S * T, 3 * H, 128);
-    ok &= make_map(&g->m_qkv_kv64, g->qkv, S * T, 3 * H, 64);
+    const uint32_t head_box = (H / c.n_heads == 32) ? 32 : 64;  // head_dim-32 tiles: 64-byte rows
+    ok &= make_map(&g->m_qkv_attn, g->qkv, S * T, 3 * H, 128, head_box);
+    ok &= make_map(&g->m_qkv_kv64, g->qkv, S * T, 3 * H, 64, head_box);
     // rows past a request's tokens are read (masked) by the attention tiles: keep them finite
     if (cudaMemset(g->qkv, 0, S * T * 3 * H * sizeof(half)) != cudaSuccess) ok = false;
     if (!ok) return bail(fail(SP_EINVAL, "tensor-map creation failed (pointer alignment / shape)"));
@@ -451,7 +454,8 @@ int attn_kind(int head_dim, int max_len) {
     const char* v = getenv("SP_ATTN_TC");
     return v == nullptr ? -1 : atoi(v);
   }();
-  if (head_dim != 64 || max_len > 512) return 0;
+  if (max_len > 512 || (head_dim != 64 && head_dim != 32)) return 0;
+  if (head_dim == 32) return mode == 0 ? 0 : 3;  // the three-CTA tcgen05 kernel has a head_dim-32 variant
   if (mode >= 0) return mode;
   if (max_len <= 64) return 3;
   return max_len <= 128 ? 1 : (max_len <= 384 ? 2 : 3);
@@ -1062,8 +1066,9 @@ int sp_op_attention(const void* qkv, void* ctx, void* ctx_lo, const int32_t* cu_
   const int hidden = n_heads * head_dim;
   const int kind = attn_kind(head_dim, max_seq_len);
   CUtensorMap m{}, m64{};
-  if (kind != 0 && (!make_map(&m, qkv, (uint64_t)groups * group_rows, 3 * hidden, 128) ||
-                    !make_map(&m64, qkv, (uint64_t)groups * group_rows, 3 * hidden, 64)))
+  const uint32_t head_box = head_dim == 32 ? 32 : 64;
+  if (kind != 0 && (!make_map(&m, qkv, (uint64_t)groups * group_rows, 3 * hidden, 128, head_box) ||
+                    !make_map(&m64, qkv, (uint64_t)groups * group_rows, 3 * hidden, 64, head_box)))
     return fail(SP_EINVAL, "attention tensor map failed");
   const long long lo_off = static_cast<half*>(ctx_lo) - static_cast<half*>(ctx);
   launch_attention_any(kind, m, m64, static_cast<const half*>(qkv), static_cast<half*>(ctx), lo_off, cu_seqlens,

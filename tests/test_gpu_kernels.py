@@ -128,6 +128,7 @@ def _attn_ref(qkv, cu, G, nh, hd):
 
 
 @pytest.mark.parametrize("hd,nh,lens", [(64, 12, [1, 17, 64, 65, 200]), (32, 4, [8, 33, 64, 3]),
+                                         (32, 8, [200, 1, 65]),
                                          (64, 16, [512, 1, 130]), (64, 8, [100, 1, 128, 37]),
                                          (64, 12, [416, 385, 3])])
 def test_attention_varlen_matches_torch(cuda_lib, hd, nh, lens):
@@ -158,7 +159,8 @@ from paper_2408_12526_b200 import _lib
 from test_gpu_kernels import _attn_ref
 lib = _lib.load()
 cases = [(64, 12, [1, 17, 64, 65, 200]), (64, 16, [512, 1, 130]), (64, 8, [100, 1, 128, 37]),
-         (64, 12, [416, 385, 3]), (64, 4, [256, 255, 129]), (64, 4, [511, 300])]
+         (64, 12, [416, 385, 3]), (64, 4, [256, 255, 129]), (64, 4, [511, 300]),
+         (32, 4, [8, 33, 64, 3]), (32, 8, [300, 1, 129])]  # head_dim 32: mma.sync (0) or the tc3 variant
 for grow in (False, True):
     for hd, nh, lens in cases:
         torch.manual_seed(sum(lens) + grow)
