@@ -79,6 +79,27 @@ def test_tiny_bert_edge_lengths(tiny):
     _check_logits(grp.logits(seqs), z_ref)
 
 
+def test_tiny_bert_at_capacity(tiny):
+    """A packed request that fills the group exactly (64 ragged sequences = max_seqs, 2048 tokens =
+    max_tokens) matches the oracle for every prefix; one token or one sequence more is rejected."""
+    grp, orc = tiny
+    rng = np.random.default_rng(17)
+    lens = rng.integers(1, 64, size=64)
+    lens[-1] += 2048 - int(lens.sum())  # exactly max_tokens
+    while lens[-1] < 1 or lens[-1] > 512:  # keep every sequence a legal length
+        lens = rng.integers(1, 64, size=64)
+        lens[-1] += 2048 - int(lens.sum())
+    seqs = [np.concatenate([[101], rng.integers(1000, 30522, size=int(L) - 1)]).astype(np.int32) for L in lens]
+    assert sum(len(x) for x in seqs) == 2048 and len(seqs) == 64
+    for k in (1, 4):
+        _, z_ref = orc.forward(seqs, k)
+        _check_logits(grp.logits(seqs, k), z_ref)
+    with pytest.raises(ValueError):
+        grp.logits(seqs[:-1] + [np.concatenate([seqs[-1], [1000]]).astype(np.int32)])
+    with pytest.raises(ValueError):
+        grp.logits(seqs + [np.array([101], np.int32)])
+
+
 def test_tiny_bert_k_out_of_range(tiny):
     grp, _ = tiny
     seqs = _seqs(np.random.default_rng(1), 2, 8, 16)
