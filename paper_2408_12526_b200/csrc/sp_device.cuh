@@ -87,22 +87,29 @@ __device__ __forceinline__ int seq_of(const int* cu, int n_seqs, int t) {
 // Writes the (hi, lo) fp16 pair (lo at x16 + x_lo_off) — both the next GEMM's operand and the
 // residual stream (hi + lo carries ~22 significant bits) — plus fp32 rows to x32 when set (the
 // last layer's CLS rows), and the same pair for the CLS row (cls16, cls16 + cls_lo_off) when set.
-template <int NC>
+// PRE: gamma / beta were staged in shared memory by the caller (before its dependency wait: weights,
+// off the critical path; gb_pre[c * 32 + lane] / gb_pre[NC * 32 + c * 32 + lane]) — short launches,
+// where the global round trip after the mean reduction costs ~1 us. Otherwise they are loaded after
+// the mean (the row's inputs are dead by then, so they add no registers).
+template <int NC, bool PRE = false>
 __device__ __forceinline__ void layer_norm_store(float (&v)[NC][4], const float* gamma, const float* beta, float eps,
                                                  int hidden, float* x32, half* x16, long long x_lo_off, half* cls16,
-                                                 long long cls_lo_off) {
+                                                 long long cls_lo_off, const float4* gb_pre = nullptr) {
   const int lane = lane_id();
   float s = 0.f;
 #pragma unroll
   for (int c = 0; c < NC; ++c) s += (v[c][0] + v[c][1]) + (v[c][2] + v[c][3]);
   const float mean = warp_sum(s) / hidden;
-  // gamma / beta issued here (not with the row loads): the row's inputs are dead by now, so they
-  // do not add to the peak register count, and the loads overlap the variance reduction
   float4 gm[NC], bt[NC];
 #pragma unroll
   for (int c = 0; c < NC; ++c) {
-    gm[c] = __ldg(reinterpret_cast<const float4*>(gamma + c * 128 + lane * 4));
-    bt[c] = __ldg(reinterpret_cast<const float4*>(beta + c * 128 + lane * 4));
+    if constexpr (PRE) {
+      gm[c] = gb_pre[c * 32 + lane];
+      bt[c] = gb_pre[NC * 32 + c * 32 + lane];
+    } else {
+      gm[c] = __ldg(reinterpret_cast<const float4*>(gamma + c * 128 + lane * 4));
+      bt[c] = __ldg(reinterpret_cast<const float4*>(beta + c * 128 + lane * 4));
+    }
   }
   float q = 0.f;
 #pragma unroll

@@ -90,6 +90,8 @@ struct GemmParams {
 // Debug hook: when set, every GEMM launch records a per-CTA timeline into this device buffer.
 void set_gemm_trace(unsigned long long* buf);
 int gemm_trace_counts(int* out, int max);
+// debug: trace slots for a row kernel launch (recorded with a negative CTA count), or null
+unsigned long long* trace_alloc_aux(int ctas);
 
 struct GemmMaps {
   CUtensorMap w;      // box {64, 128}
@@ -171,6 +173,7 @@ struct RowLn {
   int n_rows;
   const int* cu;
   int n_seqs;
+  unsigned long long* trace;  // debug: set by launch_reduce_ln when the GEMM trace is on
 };
 void launch_reduce_ln(const RowLn& a, int groups, cudaStream_t stream);
 

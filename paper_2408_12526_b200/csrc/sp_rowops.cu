@@ -9,6 +9,8 @@
 namespace sp {
 
 static constexpr int kMaxSplitsRow = 4;
+// CTAs up to which the row kernels preload gamma / beta (more registers: ~3 CTAs per SM fit)
+static constexpr long long kPreLnCtas = 3 * 148;
 
 template <int NC>
 __global__ void __launch_bounds__(128)
@@ -60,16 +62,28 @@ __global__ void __launch_bounds__(128)
 // Row t: x_out[t] = LN(x_in[in_rows ? in_rows[t] : t] + b + sum_s part[s][t]); the (hi, lo) operand
 // to x16; the CLS rows of the sequences also to cls16 (when set).
 // RES16: the residual is the (hi, lo) fp16 stream (x_in16), else the fp32 rows x_in.
-template <int NC, int SPLITS, bool RES16>
+template <int NC, int SPLITS, bool RES16, bool PRE>
 __global__ void __launch_bounds__(128) reduce_ln_kernel(const RowLn a) {
   // request inputs (cu_seqlens) and weights (bias) are read before the dependency wait
   pdl_launch_dependents();
+  unsigned long long* tr = a.trace ? a.trace + 8ull * (blockIdx.y * gridDim.x + blockIdx.x) : nullptr;
+  if (tr && threadIdx.x == 0) tr[0] = globaltimer();
+  const int g = blockIdx.y;
+  const int hidden = a.hidden;
+  __shared__ float4 s_gb[PRE ? 2 * NC * 32 : 1];  // this student's gamma | beta
+  if constexpr (PRE) {  // weights: staged before the dependency wait (every thread, before any exit)
+    const float4* gm4 = reinterpret_cast<const float4*>(a.gamma + (long long)g * hidden);
+    const float4* bt4 = reinterpret_cast<const float4*>(a.beta + (long long)g * hidden);
+    for (int i = threadIdx.x; i < NC * 32; i += blockDim.x) {
+      s_gb[i] = __ldg(gm4 + i);
+      s_gb[NC * 32 + i] = __ldg(bt4 + i);
+    }
+    __syncthreads();
+  }
   const int t = blockIdx.x * 4 + warp_id();
   const int n_rows = a.n_rows < 0 ? __ldg(a.cu + a.n_seqs) : a.n_rows;
   if (t >= n_rows) return;
-  const int g = blockIdx.y;
   const int lane = lane_id();
-  const int hidden = a.hidden;
   float4 r[NC], bs[NC], pv[SPLITS][NC];
 #pragma unroll
   for (int c = 0; c < NC; ++c)
@@ -83,6 +97,7 @@ __global__ void __launch_bounds__(128) reduce_ln_kernel(const RowLn a) {
   const long long in_row = (long long)g * a.in_gs + (long long)t_in * hidden;
   const float* part = a.part + (long long)g * a.part_gs + (long long)t * hidden;
   pdl_wait();
+  if (tr && threadIdx.x == 0) tr[3] = globaltimer();
   // then every load of the row at once: residual and up to kMaxSplitsRow partial sums
 #pragma unroll
   for (int c = 0; c < NC; ++c) {
@@ -113,9 +128,11 @@ __global__ void __launch_bounds__(128) reduce_ln_kernel(const RowLn a) {
       v[c][3] += pv[s][c].w;
     }
   }
-  layer_norm_store<NC>(v, a.gamma + (long long)g * hidden, a.beta + (long long)g * hidden, a.eps, hidden,
+  layer_norm_store<NC, PRE>(v, a.gamma + (long long)g * hidden, a.beta + (long long)g * hidden, a.eps, hidden,
                        a.x_out ? a.x_out + (long long)g * a.out_gs + (long long)t * hidden : nullptr,
-                       a.x16 + (long long)g * a.x16_gs + (long long)t * hidden, a.x_lo_off, cls_row, a.cls_lo_off);
+                       a.x16 + (long long)g * a.x16_gs + (long long)t * hidden, a.x_lo_off, cls_row, a.cls_lo_off,
+                       s_gb);
+  if (tr && threadIdx.x == 0) tr[7] = globaltimer();
 }
 
 // One CTA per output row b, one thread per feature j (blockDim = hidden <= 1024).
@@ -241,14 +258,23 @@ void launch_embed_ln(const int* ids, const int* cu_seqlens, int n_seqs, int n_to
 #undef SP_EMBED
 }
 
-void launch_reduce_ln(const RowLn& a, int groups, cudaStream_t stream) {
-  if (a.n_rows == 0 || groups <= 0) return;
+void launch_reduce_ln(const RowLn& a_in, int groups, cudaStream_t stream) {
+  if (a_in.n_rows == 0 || groups <= 0) return;
   // n_rows < 0: grid sized for -n_rows rows, live count read from cu_seqlens (graph replay)
-  dim3 grid(((a.n_rows < 0 ? -a.n_rows : a.n_rows) + 3) / 4, groups);
-#define SP_REDUCE_S(NC_, S_)                                                             \
-  do {                                                                                   \
-    if (a.x_in16) launch_pdl(reduce_ln_kernel<NC_, S_, true>, grid, dim3(128), 0, stream, a); \
-    else launch_pdl(reduce_ln_kernel<NC_, S_, false>, grid, dim3(128), 0, stream, a);    \
+  dim3 grid(((a_in.n_rows < 0 ? -a_in.n_rows : a_in.n_rows) + 3) / 4, groups);
+  RowLn a = a_in;
+  a.trace = trace_alloc_aux(static_cast<int>(grid.x * grid.y));
+  // short launches (<= one wave at the PRE kernels' register count) load gamma / beta up front
+  const bool pre = (long long)grid.x * grid.y <= kPreLnCtas;
+#define SP_REDUCE_S(NC_, S_)                                                                       \
+  do {                                                                                             \
+    if (a.x_in16) {                                                                                \
+      if (pre) launch_pdl(reduce_ln_kernel<NC_, S_, true, true>, grid, dim3(128), 0, stream, a);   \
+      else launch_pdl(reduce_ln_kernel<NC_, S_, true, false>, grid, dim3(128), 0, stream, a);      \
+    } else {                                                                                       \
+      if (pre) launch_pdl(reduce_ln_kernel<NC_, S_, false, true>, grid, dim3(128), 0, stream, a);  \
+      else launch_pdl(reduce_ln_kernel<NC_, S_, false, false>, grid, dim3(128), 0, stream, a);     \
+    }                                                                                              \
   } while (0)
 #define SP_REDUCE(NC_)                     \
   do {                                     \

@@ -34,15 +34,28 @@ for L in [int(x) for x in sys.argv[1].split(",")]:
     e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
     e0.record(); graph.replay(); e1.record(); torch.cuda.synchronize()
     t = tr.view(-1, 8).cpu().numpy().astype(np.float64)
-    t = t[t[:, 0] > 0]
-    base = t[:, 0].min()
+    base = t[t[:, 0] > 0][:, 0].min()
     off = 0
     print(f"L={L}: event {e0.elapsed_time(e1)*1e3:.1f} us")
+    gi = 0
     for li, n in enumerate(sizes):
         names = names_for(L)
-        nm = names[li] if li < len(names) else f"g{li}"
-        seg = (t[off:off + n] - base) / 1e3; off += n
+        aux = n < 0
+        n = abs(n)
+        if aux:
+            nm = "ln"
+        else:
+            nm = names[gi] if gi < len(names) else f"g{gi}"
+            gi += 1
+        raw = t[off:off + n]; off += n
+        raw = raw[raw[:, 0] > 0]
+        seg = (raw - base) / 1e3
         if len(seg) == 0:
+            continue
+        if aux:
+            live = seg[raw[:, 3] > 0]
+            print(f"  {nm:5s} ctas={n:4d} entry[{seg[:,0].min():6.1f},{seg[:,0].max():6.1f}] "
+                  f"dep={np.median(live[:,3]) if len(live) else -1:6.1f} end={live[:,7].max() if len(live) else -1:6.1f}")
             continue
         print(f"  {nm:5s} ctas={n:4d} entry[{seg[:,0].min():6.1f},{seg[:,0].max():6.1f}] wpre={np.median(seg[:,2]):6.1f} mma0={np.median(seg[:,4]):6.1f} "
               f"dep={np.median(seg[:,3]):6.1f} last_commit={seg[:,5].max():6.1f} epi0_max={seg[:,6].max():6.1f} end={seg[:,7].max():6.1f}")
