@@ -190,6 +190,7 @@ __global__ void __launch_bounds__(Tc2Cfg<SPLIT>::kThreads, Tc2Cfg<SPLIT>::kMinBl
         umma_commit(s_full);
       };
       issue_s(0);
+      if (tr) tr[2] = globaltimer();
       for (int j = 0; j < n_chunks; ++j) {
         if (j + 1 < n_chunks) issue_s(j + 1);  // next scores while the softmax works on chunk j
         mbar_wait(p_full, j & 1);
@@ -416,7 +417,12 @@ template <int D>
 __global__ void __launch_bounds__(kT3Threads, 3)
     attn_tc3_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_kv,
                     half* __restrict__ ctx, const int* __restrict__ cu, int n_heads, int hidden, long long group_rows,
-                    float scale_log2, long long lo_off) {
+                    float scale_log2, long long lo_off, unsigned long long* trace) {
+  // debug trace (8 stamps per CTA): entry, dependency released, first S issued, scores seen by the
+  // softmax, last P V issued, P V done seen by the epilogue, end
+  unsigned long long* tr =
+      trace ? trace + 8ull * ((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) : nullptr;
+  if (tr && threadIdx.x == 0) tr[0] = globaltimer();
   static_assert(D == 64 || D == 32, "head_dim 64 or 32");
   constexpr int kKv64 = T3<D>::kKv;
   extern __shared__ uint8_t smem_raw[];
@@ -473,6 +479,7 @@ __global__ void __launch_bounds__(kT3Threads, 3)
     if (elect_one()) {
       const uint64_t pol = policy_evict_last();
       pdl_wait();  // qkv is the previous kernel's output
+      if (tr) tr[1] = globaltimer();
       mbar_arrive_expect_tx(q_full, T3<D>::kQ);
       tma_load_2d(&map_q, q_full, sQ, h * D, row_base + q0, pol);
       for (int j = 0; j < n_chunks; ++j) {
@@ -500,6 +507,7 @@ __global__ void __launch_bounds__(kT3Threads, 3)
         umma_commit(s_full);
       };
       issue_s(0);
+      if (tr) tr[2] = globaltimer();
       for (int j = 0; j < n_chunks; ++j) {
         mbar_wait(p_full, j & 1);  // P_j is in TMEM columns [0, 32)
         tc_fence_after();
@@ -512,6 +520,7 @@ __global__ void __launch_bounds__(kT3Threads, 3)
         umma_commit(&kv_empty[j & 1]);
         if (j + 1 < n_chunks) issue_s(j + 1);  // after PV_j in the tensor pipe: P_j is consumed first
       }
+      if (tr) tr[4] = globaltimer();
     }
     __syncwarp();
   } else {
@@ -521,6 +530,7 @@ __global__ void __launch_bounds__(kT3Threads, 3)
     float m = 0.f, l = 0.f;
     for (int j = 0; j < n_chunks; ++j) {
       mbar_wait(s_full, j & 1);  // also: PV_{j-1} has completed (issued before S_j)
+      if (tr && j == 0 && threadIdx.x == 0) tr[3] = globaltimer();
       if (!live) {
         __syncwarp();
         if (lane == 0) mbar_arrive(p_full);
@@ -586,6 +596,7 @@ __global__ void __launch_bounds__(kT3Threads, 3)
       if (lane == 0) mbar_arrive(p_full);
     }
     mbar_wait(pv_done, (n_chunks - 1) & 1);
+    if (tr && threadIdx.x == 0) tr[5] = globaltimer();
     if (live) {
       tc_fence_after();
       const float inv = 1.f / l;
@@ -614,6 +625,7 @@ __global__ void __launch_bounds__(kT3Threads, 3)
   }
   tc_fence_before();
   __syncthreads();
+  if (tr && threadIdx.x == 0) tr[7] = globaltimer();
   if (warp == kMma3) {
     tc_fence_after();
     tmem_dealloc(tmem, 128);
@@ -636,8 +648,9 @@ static void launch_tc3_t(const CUtensorMap& map_q, const CUtensorMap& map_kv, ha
   }
   const float scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(D));
   dim3 grid(groups * n_heads, n_seqs, (max_len + 127) / 128);
+  unsigned long long* tr = trace_alloc_aux(static_cast<int>(grid.x * grid.y * grid.z), 2);
   launch_pdl(attn_tc3_kernel<D>, grid, dim3(kT3Threads), smem, stream, map_q, map_kv, ctx, cu_seqlens, n_heads, hidden,
-             group_rows, scale_log2, lo_off);
+             group_rows, scale_log2, lo_off, tr);
 }
 
 void launch_attention_tc3(const CUtensorMap& map_q, const CUtensorMap& map_kv, half* ctx, long long lo_off,

@@ -278,7 +278,7 @@ __global__ void __launch_bounds__(kThreads, 2)
 
 // Debug trace: launches append their per-CTA stamps one after another (slot 0 of the buffer
 // holds the number of CTAs recorded so far, host-side mirror in g_trace_used).
-static unsigned long long* trace_ptr_advance(int ctas, bool aux = false);
+static unsigned long long* trace_ptr_advance(int ctas, int aux_kind = 0);
 
 // ============================================================================ persistent variant
 // For large token counts (T > 128: long batch-1 requests, batched load) one CTA per SM loops over
@@ -709,14 +709,17 @@ void set_gemm_trace(unsigned long long* buf) {
   g_trace_used = 0;
   g_trace_counts.clear();
 }
-static unsigned long long* trace_ptr_advance(int ctas, bool aux) {
+static unsigned long long* trace_ptr_advance(int ctas, int aux_kind) {
   if (!g_trace) return nullptr;
   unsigned long long* p = g_trace + 8 * g_trace_used;
   g_trace_used += (size_t)ctas;
-  g_trace_counts.push_back(aux ? -ctas : ctas);  // aux (row kernels): negative CTA count
+  // GEMMs: the CTA count; other kernels: -(kind * 100000 + CTA count)
+  g_trace_counts.push_back(aux_kind ? -(aux_kind * 100000 + ctas) : ctas);
   return p;
 }
-unsigned long long* trace_alloc_aux(int ctas) { return trace_ptr_advance(ctas, true); }int gemm_trace_counts(int* out, int max) {
+unsigned long long* trace_alloc_aux(int ctas, int kind) { return trace_ptr_advance(ctas, kind); }
+
+int gemm_trace_counts(int* out, int max) {
   const int n = static_cast<int>(g_trace_counts.size());
   for (int i = 0; i < n && i < max; ++i) out[i] = g_trace_counts[i];
   return n;

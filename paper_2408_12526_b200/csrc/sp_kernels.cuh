@@ -90,8 +90,9 @@ struct GemmParams {
 // Debug hook: when set, every GEMM launch records a per-CTA timeline into this device buffer.
 void set_gemm_trace(unsigned long long* buf);
 int gemm_trace_counts(int* out, int max);
-// debug: trace slots for a row kernel launch (recorded with a negative CTA count), or null
-unsigned long long* trace_alloc_aux(int ctas);
+// debug: trace slots (8 per CTA) for a non-GEMM launch, kind 1 = LayerNorm, 2 = attention;
+// recorded as -(kind * 100000 + ctas); null when tracing is off
+unsigned long long* trace_alloc_aux(int ctas, int kind);
 
 struct GemmMaps {
   CUtensorMap w;      // box {64, 128}

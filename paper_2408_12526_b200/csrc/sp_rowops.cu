@@ -263,7 +263,7 @@ void launch_reduce_ln(const RowLn& a_in, int groups, cudaStream_t stream) {
   // n_rows < 0: grid sized for -n_rows rows, live count read from cu_seqlens (graph replay)
   dim3 grid(((a_in.n_rows < 0 ? -a_in.n_rows : a_in.n_rows) + 3) / 4, groups);
   RowLn a = a_in;
-  a.trace = trace_alloc_aux(static_cast<int>(grid.x * grid.y));
+  a.trace = trace_alloc_aux(static_cast<int>(grid.x * grid.y), 1);
   // short launches (<= one wave at the PRE kernels' register count) load gamma / beta up front
   const bool pre = (long long)grid.x * grid.y <= kPreLnCtas;
 #define SP_REDUCE_S(NC_, S_)                                                                       \

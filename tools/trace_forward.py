@@ -41,9 +41,10 @@ for L in [int(x) for x in sys.argv[1].split(",")]:
     for li, n in enumerate(sizes):
         names = names_for(L)
         aux = n < 0
-        n = abs(n)
+        kind = (-n) // 100000 if aux else 0
+        n = (-n) % 100000 if aux else n
         if aux:
-            nm = "ln"
+            nm = {1: "ln", 2: "attn"}.get(kind, "aux")
         else:
             nm = names[gi] if gi < len(names) else f"g{gi}"
             gi += 1
@@ -53,6 +54,12 @@ for L in [int(x) for x in sys.argv[1].split(",")]:
         if len(seg) == 0:
             continue
         if aux:
+            if kind == 2:  # attention: entry, dep, S issued, scores seen, last PV issued, PV done, end
+                med = lambda c: np.median(seg[raw[:, c] > 0][:, c]) if (raw[:, c] > 0).any() else -1
+                print(f"  {nm:5s} ctas={n:4d} entry[{seg[:,0].min():6.1f},{seg[:,0].max():6.1f}] dep={med(1):6.1f} "
+                      f"s0={med(2):6.1f} scores={med(3):6.1f} pv_issued={med(4):6.1f} pv_done={med(5):6.1f} "
+                      f"end={seg[raw[:, 7] > 0][:, 7].max():6.1f}")
+                continue
             live = seg[raw[:, 3] > 0]
             print(f"  {nm:5s} ctas={n:4d} entry[{seg[:,0].min():6.1f},{seg[:,0].max():6.1f}] "
                   f"dep={np.median(live[:,3]) if len(live) else -1:6.1f} end={live[:,7].max() if len(live) else -1:6.1f}")
