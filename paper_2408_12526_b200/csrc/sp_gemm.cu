@@ -260,7 +260,11 @@ __global__ void __launch_bounds__(kThreads, 2)
       if (lo_off) warp_store_rows<OutT, NR>(y, n, stage, out + lo_off, n0 + c, t_rows, p.out_ld, true);
     };
     for (int c = c_begin; c < c_begin + half_cols; c += 32) {
-      const int n = min(32, c_begin + half_cols - c);  // multiple of 8, warp-uniform
+      // columns of this chunk that hold live tokens (CLS-row GEMMs: n_seqs of a 16-wide tile;
+      // graph replay: the live length inside the bucket), rounded up to the TMEM load width 8
+      const int live = t_rows - (n0 + c);
+      if (live <= 0) break;                      // warp-uniform
+      const int n = min(min(32, c_begin + half_cols - c), (live + 7) & ~7);
       if (n > 16) chunk(std::integral_constant<int, 32>{}, c, n);
       else if (n > 8) chunk(std::integral_constant<int, 16>{}, c, n);
       else chunk(std::integral_constant<int, 8>{}, c, n);
