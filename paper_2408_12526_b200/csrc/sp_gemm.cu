@@ -514,14 +514,22 @@ __global__ void __launch_bounds__(kPThreads, 1)
   } else {
     const int e = warp - 2;
     const int q = warp & 3;
-    const int part_cols = p.bn >> 2;  // bn is a multiple of 32
-    const int c_begin = (e >> 2) * part_cols;
+    const int wg = e >> 2;            // warp group 0..3: 16-column chunks wg, wg + 4, ...
+    const int n_chunks = p.bn >> 4;   // bn is a multiple of 16
     OutT* stage = reinterpret_cast<OutT*>(staging + e * 16 * kRowBytes);
     const int t_rows = p.t_dev ? __ldg(p.t_dev) : p.t_rows;
     const long long lo_off = OUT_F32 ? 0 : p.out_lo_off;
     // accumulator release: local barrier, or the leader's through the cluster window
     uint32_t acc_empty_leader0 = 0u;
     if constexpr (PAIR) acc_empty_leader0 = mapa_shared(smem_u32(&acc_empty[0]), 0);
+    auto release = [&](int b) {  // after this warp's last TMEM read of the tile
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if constexpr (PAIR) mbar_arrive_cluster(acc_empty_leader0 + (uint32_t)(b * sizeof(uint64_t)));
+        else mbar_arrive(&acc_empty[b]);
+      }
+    };
     int j = 0;
     for (int u = u_first; u < units; u += u_stride, ++j) {
       int g, mt, nt;
@@ -535,31 +543,27 @@ __global__ void __launch_bounds__(kPThreads, 1)
       tc_fence_after();
       if (tr && j == 0 && warp == 2 && lane == 0) tr[6] = globaltimer();
       const uint32_t taddr = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(b * 256);
-      // chunks of 16 columns (the last may be 8: computed at width 8, not 16)
-      auto chunk = [&](auto nr, int c) {
-        constexpr int NR = decltype(nr)::value;
-        uint32_t r[NR];
-#pragma unroll
-        for (int i = 0; i < NR; i += 8) tmem_ld8_nowait(taddr + c + i, r + i);
+      // chunks holding live tokens only (graph replay: the live length inside the bucket)
+      const int live = t_rows - n0;
+      const int live_chunks = live <= 0 ? 0 : min(n_chunks, (live + 15) >> 4);
+      bool released = false;
+      for (int ci = wg; ci < live_chunks; ci += 4) {
+        const int c = ci * 16;
+        uint32_t r[16];
+        tmem_ld8_nowait(taddr + c, r);
+        tmem_ld8_nowait(taddr + c + 8, r + 8);
         tmem_wait_ld();
-        if (c + NR >= c_begin + part_cols) {  // last TMEM read of this tile: hand the accumulator back
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) {
-            if constexpr (PAIR) mbar_arrive_cluster(acc_empty_leader0 + (uint32_t)(b * sizeof(uint64_t)));
-            else mbar_arrive(&acc_empty[b]);
-          }
+        if (ci + 4 >= live_chunks) {
+          release(b);
+          released = true;
         }
-        float y[NR];
+        float y[16];
 #pragma unroll
-        for (int jj = 0; jj < NR; ++jj) y[jj] = apply_act<ACT>(__uint_as_float(r[jj]) + bias);
-        warp_store_rows<OutT, NR>(y, NR, stage, out, n0 + c, t_rows, p.out_ld, false);
-        if (lo_off) warp_store_rows<OutT, NR>(y, NR, stage, out + lo_off, n0 + c, t_rows, p.out_ld, true);
-      };
-      for (int c = c_begin; c < c_begin + part_cols; c += 16) {
-        if (c_begin + part_cols - c >= 16) chunk(std::integral_constant<int, 16>{}, c);
-        else chunk(std::integral_constant<int, 8>{}, c);
+        for (int jj = 0; jj < 16; ++jj) y[jj] = apply_act<ACT>(__uint_as_float(r[jj]) + bias);
+        warp_store_rows<OutT, 16>(y, 16, stage, out, n0 + c, t_rows, p.out_ld, false);
+        if (lo_off) warp_store_rows<OutT, 16>(y, 16, stage, out + lo_off, n0 + c, t_rows, p.out_ld, true);
       }
+      if (!released) release(b);  // no (live) chunk for this warp in this tile
     }
     if (tr && warp == 2 && lane == 0) tr[7] = globaltimer();
   }
@@ -629,7 +633,7 @@ bool gemm_persistent_pair(int t_rows, int m_tiles, int groups) {
 // 6 per student) still fill every SM; ring as deep as the smem left after staging.
 // Every operand is an (hi, lo) pair: two token terms per stage and two MMAs per k-slice.
 void gemm_configure_persistent(int t_rows, bool out_f32, int units_per_tile, int n_ctas, bool pair, int* bn,
-                               int* n_tiles, int* stages) {
+                               int* n_tiles, int* stages, int gran_override) {
   // Cost of a tiling = rounds x per-unit time, in cycles per 64-wide k-block of one CTA:
   //   MMA      2 * 2 * bn                          (two 128 x bn x 64 MMAs at 8192 flop/clk)
   //   operands 3 * (128 + 2 * token rows staged)   (L2 -> SM at ~42 B/clk per SM, 12.4 TB/s / 148)
@@ -637,11 +641,16 @@ void gemm_configure_persistent(int t_rows, bool out_f32, int units_per_tile, int
   // units_per_tile / 2 units on n_ctas / 2 pairs.
   const int ctas = pair ? n_ctas / 2 : n_ctas;
   const int upt = pair ? units_per_tile / 2 : units_per_tile;
+  // the tile count is chosen on 32-column tiles (the model was fitted there); the chosen tile is then
+  // trimmed to a 16-column multiple (MMA N step; the epilogue deals 16-column chunks round-robin)
+  // unless the caller needs 32 (pairs stage bn / 2 rows per CTA in 16-row TMA boxes; the fused MLP)
+  const int gran = 32;
+  const int trim = gran_override ? gran_override : (pair ? 32 : 16);
   int best_tiles = (t_rows + 255) / 256;
   long long best_cost = 0x7fffffffffffll;
   for (int tiles = (t_rows + 255) / 256; tiles <= (t_rows + 63) / 64; ++tiles) {
     const int per = (t_rows + tiles - 1) / tiles;
-    const int b = ((per + 31) / 32) * 32;  // 16 epilogue warps take a quarter each (multiples of 8)
+    const int b = ((per + gran - 1) / gran) * gran;
     if (b > 256) continue;
     const int x = pair ? b / 2 : b;
     const long long rounds = (upt * (long long)tiles + ctas - 1) / ctas;
@@ -654,7 +663,12 @@ void gemm_configure_persistent(int t_rows, bool out_f32, int units_per_tile, int
   }
   const int tiles = best_tiles;
   const int per = (t_rows + tiles - 1) / tiles;
-  int b = ((per + 31) / 32) * 32;
+  int b = ((per + gran - 1) / gran) * gran;
+  // trim only where it does not add TMA boxes per token term (64- and 16-row boxes: 33 tokens stay
+  // one 64-row box rather than three 16-row boxes — measured slower)
+  auto boxes = [](int rows) { return rows / 64 + (rows % 64) / 16; };
+  const int bt = ((per + trim - 1) / trim) * trim;
+  if (bt < b && boxes(bt) <= boxes(b)) b = bt;
   *bn = b;
   *n_tiles = tiles;
   const int staging = kPEpiWarps * 16 * 32 * (out_f32 ? 4 : 2);

@@ -111,8 +111,9 @@ void launch_gemm(const GemmMapsW& maps, const GemmParams& p, int groups, cudaStr
 // Persistent variant for large token counts (splits must be 1).
 void launch_gemm_persistent(const GemmMapsW& maps, const GemmParams& p, int groups, cudaStream_t stream);
 bool gemm_persistent_pair(int t_rows, int m_tiles, int groups);
+// gran: token-tile granularity override (0: 16, or 32 for pairs; the fused MLP kernel needs 32)
 void gemm_configure_persistent(int t_rows, bool out_f32, int units_per_tile, int n_ctas, bool pair, int* bn,
-                               int* n_tiles, int* stages);
+                               int* n_tiles, int* stages, int gran = 0);
 int sm_count();
 size_t gemm_smem_bytes(int bn, int stages, int whilo = 0);
 // ring depth when every stage also holds the weights' lo tile (x_rows = token rows staged per CTA)

@@ -554,8 +554,10 @@ int run_mlp(sp_group* g, int l, int k, int n_tokens, const int* t_dev, cudaStrea
   p.n_b = H;
   p.k_b = F;
   int stages = 0;
-  sp::gemm_configure_persistent(n_tokens, false, k * (F / 128), sp::sm_count(), false, &p.bn_a, &p.n_tiles_a, &stages);
-  sp::gemm_configure_persistent(n_tokens, true, k * (H / 128), sp::sm_count(), false, &p.bn_b, &p.n_tiles_b, &stages);
+  sp::gemm_configure_persistent(n_tokens, false, k * (F / 128), sp::sm_count(), false, &p.bn_a, &p.n_tiles_a, &stages,
+                                32);
+  sp::gemm_configure_persistent(n_tokens, true, k * (H / 128), sp::sm_count(), false, &p.bn_b, &p.n_tiles_b, &stages,
+                                32);
   sp::mlp_smem_bytes(std::max(p.bn_a, p.bn_b), &p.stages);
   p.groups = k;
   p.t_rows = n_tokens;
