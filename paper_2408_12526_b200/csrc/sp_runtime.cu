@@ -91,16 +91,21 @@ bool make_xmaps(XMaps* m, const void* hi, const void* lo, uint64_t rows, uint64_
 }
 
 // Split-K count of a projection with few output tiles: balance the CTAs over the SMs (the makespan
-// in k-blocks of the busiest SM, plus a small cost per extra partial; -2 us at L=128-256 against
-// "first split count with >= 128 CTAs"). With >= 1 tile per SM the one-split persistent path wins.
-int choose_splits(int units, int nkb, int smax) {
+// in k-blocks of the busiest slot, plus a small cost per extra partial). Two small-kernel CTAs
+// (<= 110 KiB smem each) share an SM and stream concurrently, so the slots are 2 x 148: a
+// single-token-tile projection takes 4 splits / 192 CTAs rather than 3 / 144 (-1.5..-3 us per
+// request at every length, measured) — for token tiles of <= 64 columns, where the weights
+// dominate the traffic; wider tiles keep one slot per SM (two 112-column CTAs per SM measured
+// slower at 320-384 tokens). With >= 1 tile per SM the one-split persistent path wins.
+int choose_splits(int units, int nkb, int smax, int bn) {
   if (units >= 148) return 1;
+  const int slots = bn <= 64 ? 296 : 148;
   int best = 1;
   long long best_cost = 0x7fffffffffffll;
   for (int s = 1; s <= smax; ++s) {
     if (nkb % s || (s > 1 && nkb / s < 2)) continue;
     const long long ctas = (long long)units * s;
-    const long long per_sm = (ctas + 147) / 148;
+    const long long per_sm = (ctas + slots - 1) / slots;
     const long long cost = per_sm * (nkb / s) * 4 + s;
     if (cost < best_cost) {
       best_cost = cost;
@@ -620,15 +625,15 @@ int bert_forward(sp_group* g, const int32_t* ids, const int32_t* cu, int n_seqs,
     int bn, n_tiles, stages;
     sp::gemm_configure_tiles(n_tokens, &bn, &n_tiles, &stages);
     const long long part_ss = (long long)S * xgs;
-    const int s_o = choose_splits(k * (H / 128) * n_tiles, H / 64, kMaxSplits);
-    const int s_f = choose_splits(k * (H / 128) * n_tiles, F / 64, kMaxSplits);
+    const int s_o = choose_splits(k * (H / 128) * n_tiles, H / 64, kMaxSplits, bn);
+    const int s_f = choose_splits(k * (H / 128) * n_tiles, F / 64, kMaxSplits, bn);
     const int akind = attn_kind(H / c.n_heads, max_len);
     // CLS-row projections of the last layer: n_seqs rows per student
     const long long bgs = (long long)B * H, partc_ss = (long long)S * bgs;
     int bn_c, n_tiles_c;
     sp::gemm_configure_tiles(n_seqs, &bn_c, &n_tiles_c, &stages);
-    const int s_oc = choose_splits(k * (H / 128) * n_tiles_c, H / 64, kMaxSplits);
-    const int s_fc = choose_splits(k * (H / 128) * n_tiles_c, F / 64, kMaxSplits);
+    const int s_oc = choose_splits(k * (H / 128) * n_tiles_c, H / 64, kMaxSplits, bn_c);
+    const int s_fc = choose_splits(k * (H / 128) * n_tiles_c, F / 64, kMaxSplits, bn_c);
     const double GBH = (double)k * n_seqs * H;
     const bool split_q = c.n_layers > 1 && n_tokens >= 256;
     // one LayerNorm launch (rows of k students)
@@ -742,7 +747,7 @@ int bert_forward(sp_group* g, const int32_t* ids, const int32_t* cu, int n_seqs,
     }
     // pooler on the CLS rows: tanh(W_p h_CLS + b_p). Few rows: split-K partials (more CTAs stream the
     // pooler weights), finished by the head kernel; many rows: one pass with the tanh epilogue.
-    const int s_p = n_seqs <= 128 ? choose_splits(k * (H / 128), H / 64, kMaxSplits) : 1;
+    const int s_p = n_seqs <= 128 ? choose_splits(k * (H / 128), H / 64, kMaxSplits, bn_c) : 1;
     pool_splits = s_p;
     run_gemm(g, SP_LAUNCH_GEMM_POOL, g->m_pool, g->xm_cls, k, H, H, n_seqs, B, s_p > 1 ? nullptr : w.b_pool, H,
              sp::ACT_TANH, g->final32, (long long)g->rows_cap * H, 0, 1, s_p, (long long)S * g->rows_cap * H, st);
