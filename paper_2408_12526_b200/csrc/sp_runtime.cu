@@ -516,8 +516,9 @@ void run_gemm(sp_group* grp, int kind, const CUtensorMap& wmap, const XMaps& xm,
   // are L2-resident at batch-1 and not part of the request's compulsory HBM traffic)
   const double G = groups, N = n_out, K = k_dim, T = t_rows;
   const double wbytes = G * N * K * 2.0 * (wlo ? 2 : 1) + (bias ? G * N * 4.0 : 0.0);
-  // one-split projections from 17 tokens on: the persistent kernel (measured equal or 2-4 us faster)
-  if (splits == 1 && t_rows >= 17) {
+  // one-split projections from 33 tokens on: the persistent kernel (2.8-4 us faster at 48-64 tokens;
+  // at 17-32 tokens the small kernel is ~2 us faster, measured on the final engine)
+  if (splits == 1 && t_rows >= 33) {
     p.splits = 1;
     p.kb_per_split = k_dim / 64;
     sp::gemm_configure_persistent(t_rows, out_f32 != 0, groups * p.m_tiles, sp::sm_count(),
