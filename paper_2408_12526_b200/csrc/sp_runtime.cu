@@ -636,7 +636,9 @@ int bert_forward(sp_group* g, const int32_t* ids, const int32_t* cu, int n_seqs,
     const int s_oc = choose_splits(k * (H / 128) * n_tiles_c, H / 64, kMaxSplits, bn_c);
     const int s_fc = choose_splits(k * (H / 128) * n_tiles_c, F / 64, kMaxSplits, bn_c);
     const double GBH = (double)k * n_seqs * H;
-    const bool split_q = c.n_layers > 1 && n_tokens >= 256;
+    // last layer: K/V of every token + the CLS query as a second GEMM only for the largest requests
+    // (L12 at 512 tokens: -4.7 us); for B8 it measured 2-4.5 us slower at every length (256-512)
+    const bool split_q = c.n_layers > 1 && (long long)n_tokens * H >= 448LL * 1024;
     // one LayerNorm launch (rows of k students)
     auto layer_norm = [&](const float* part, int splits, long long pss, long long pgs, const float* b_, const float* g_,
                           const float* be_, const float* x_in, long long in_gs, const int* in_rows, float* x_out,
@@ -682,7 +684,7 @@ int bert_forward(sp_group* g, const int32_t* ids, const int32_t* cu, int n_seqs,
       if (split_q && last) {
         // long requests, last layer: K and V of every token (weight rows [H, 3H) of each student's
         // QKV slab), the query of the CLS rows only (rows [0, H) on the CLS copies the previous
-        // LayerNorm wrote): -12 us at L = 512 (measured); below 256 tokens the extra launch costs more
+        // LayerNorm wrote)
         run_gemm(g, SP_LAUNCH_GEMM_QKV, g->m_qkv[l], g->xm_x16, k, 2 * H, H, n_tokens, T, w.b_qkv + lS * 3 * H + H,
                  3 * H, sp::ACT_NONE, g->qkv + H, (long long)T * 3 * H, 0, 0, 1, 0, st, t_dev, 3 * H, 3 * H, H);
         run_gemm(g, SP_LAUNCH_GEMM_QKV, g->m_qkv[l], g->xm_cls, k, H, H, n_seqs, B, w.b_qkv + lS * 3 * H, 3 * H,
