@@ -526,9 +526,10 @@ void run_gemm(sp_group* grp, int kind, const CUtensorMap& wmap, const XMaps& xm,
     if (wlo)  // a second weight tile per stage: re-derive the ring depth (same smem budget)
       p.stages = sp::gemm_whilo_stages(sp::gemm_persistent_pair(t_rows, p.m_tiles, groups) ? p.bn / 2 : p.bn, true,
                                        out_f32 != 0);
-    // weights re-read by many token tiles stay in L2 (evict_last); streamed once or twice (batch-1)
-    // they must not push the residual stream out (evict_first: -2% at L=512)
-    p.w_keep = p.n_tiles > 2 ? 2 : 0;
+    // weights re-read by many token tiles stay in L2 (evict_last); streamed up to four times
+    // (batch-1, <= 512 tokens) they must not push the activations out (evict_first: -1..-2 us at
+    // 384-512 tokens against evict_last from 3 tiles, measured)
+    p.w_keep = p.n_tiles > 4 ? 2 : 0;
     if (grp) grp->rec_begin(kind, wbytes, 2.0 * G * N * K * T);
     sp::launch_gemm_persistent(maps, p, groups, st);
     if (grp) grp->rec_end();
@@ -730,7 +731,9 @@ int bert_forward(sp_group* g, const int32_t* ids, const int32_t* cu, int n_seqs,
       // FFN1 + FFN2 as one persistent kernel where both would take the single-CTA persistent path
       // (only where FFN2 itself would be a one-split persistent GEMM: measured -2% at L=512, but
       // +3% at L=256 where FFN2's split-K tiles beat the fused kernel's 96-token phase-B tiles)
-      const bool mlp = s_f == 1 && n_tokens >= 129 && k <= sp::kMlpMaxStudents &&
+      // (re-measured on the final engine: it wins only for many students at <= 192 tokens — K32
+      // -10 us at 192 — and loses for L12 (K=12) at 144-240 and for K32 at 240 tokens)
+      const bool mlp = s_f == 1 && n_tokens >= 129 && n_tokens <= 224 && k > 16 && k <= sp::kMlpMaxStudents &&
                        !sp::gemm_persistent_pair(n_tokens, F / 128, k) &&
                        !sp::gemm_persistent_pair(n_tokens, H / 128, k);
       int s_ln2 = s_f;
