@@ -23,7 +23,8 @@ def emulate(name, K, seed, L, k, pts):
         nl = len(s["layers"])
         for li, lay in enumerate(s["layers"]):
             last = li == nl - 1
-            qkv = h(dense_layer(*lay["qkv"], x, IDENTITY), "qkv" in pts)
+            qkv = h(dense_layer(*lay["qkv"], x, IDENTITY),
+                    "qkv" in pts or (f"qkv{li}" in pts) or ("qkvL" in pts and last))
             q, kk, v = (qkv[:, i * H:(i + 1) * H].reshape(L, nh, hd) for i in range(3))
             sc = np.einsum("qhd,khd->hqk", q, kk) / np.sqrt(hd)
             p = np.exp(sc - sc.max(-1, keepdims=True))
@@ -40,7 +41,7 @@ name, seed, L, k = (sys.argv[1], int(sys.argv[2]), int(sys.argv[3]), int(sys.arg
 from paper_2408_12526_b200 import PRESETS
 K = PRESETS[name][1]
 z0, ids = emulate(name, K, seed, L, k, set())
-for pts in (["qkv"], ["p"], ["qkv", "p"]):
+for pts in (["qkv"], ["qkv0"], ["qkvL"], ["p"], ["qkv", "p"], ["qkv0", "p"]):
     z, _ = emulate(name, K, seed, L, k, set(pts))
     print(f"emulated fp16 at {'+'.join(pts):8s}: {np.abs(z - z0).max() / np.abs(z0).max():.2e}  (max|z| {np.abs(z0).max():.4f})")
 if os.environ.get("DIAG_CHILD") is None:
