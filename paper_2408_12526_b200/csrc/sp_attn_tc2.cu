@@ -74,6 +74,11 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16
       "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
       : "memory");
 }
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&r)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(r[0]),
+               "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+               : "memory");
+}
 __device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, uint32_t (&r)[16]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
@@ -413,11 +418,16 @@ struct T3 {
 };
 }  // namespace
 
-template <int D>
+// QLO: V is an (hi, lo) fp16 pair (the lo tile at map row + lo_rows) and P is split into (hi, lo)
+// too: O += Ph Vh + Ph Vl + Pl Vh (three MMAs per 16-key step), so the context carries ~22-bit
+// operands like the projections. The fp16 rounding of V and P dominated the adaptive-prefix cases
+// whose logits cancel (tools/diag_prefix.py: V 0.7-3.0e-3, P 0.1-1.3e-3 of max|z|; Q and K
+// together <= 4.8e-4), so S = Q K^T stays one MMA on the hi terms.
+template <int D, bool QLO>
 __global__ void __launch_bounds__(kT3Threads, 3)
     attn_tc3_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_kv,
                     half* __restrict__ ctx, const int* __restrict__ cu, int n_heads, int hidden, long long group_rows,
-                    float scale_log2, long long lo_off, unsigned long long* trace) {
+                    float scale_log2, long long lo_off, unsigned long long* trace, long long lo_rows) {
   // debug trace (8 stamps per CTA): entry, dependency released, first S issued, scores seen by the
   // softmax, last P V issued, P V done seen by the epilogue, end
   unsigned long long* tr =
@@ -430,7 +440,8 @@ __global__ void __launch_bounds__(kT3Threads, 3)
   uint8_t* sQ = smem;                 // 16 KiB (D = 64) / 8 KiB
   uint8_t* sK = sQ + T3<D>::kQ;       // [2] x 8 / 4 KiB
   uint8_t* sV = sK + 2 * kKv64;       // [2] x 8 / 4 KiB
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + 2 * kKv64);
+  uint8_t* sVl = sV + 2 * kKv64;      // QLO: [2] V lo
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sVl + (QLO ? 2 * kKv64 : 0));
   uint64_t* q_full = bars;
   uint64_t* kv_full = bars + 1;   // [2]
   uint64_t* kv_empty = bars + 3;  // [2]
@@ -485,9 +496,12 @@ __global__ void __launch_bounds__(kT3Threads, 3)
       for (int j = 0; j < n_chunks; ++j) {
         const int st = j & 1;
         if (j >= 2) mbar_wait(&kv_empty[st], ((j >> 1) - 1) & 1);
-        mbar_arrive_expect_tx(&kv_full[st], 2 * kKv64);
+        mbar_arrive_expect_tx(&kv_full[st], (QLO ? 3 : 2) * kKv64);
         tma_load_2d(&map_kv, &kv_full[st], sK + st * kKv64, hidden + h * D, row_base + j * 64, pol);
         tma_load_2d(&map_kv, &kv_full[st], sV + st * kKv64, 2 * hidden + h * D, row_base + j * 64, pol);
+        if constexpr (QLO)
+          tma_load_2d(&map_kv, &kv_full[st], sVl + st * kKv64, 2 * hidden + h * D, (int)(row_base + j * 64 + lo_rows),
+                      pol);
       }
     }
     __syncwarp();
@@ -512,10 +526,16 @@ __global__ void __launch_bounds__(kT3Threads, 3)
         mbar_wait(p_full, j & 1);  // P_j is in TMEM columns [0, 32)
         tc_fence_after();
         const uint8_t* vb = sV + (j & 1) * kKv64;
+        const uint8_t* vbl = sVl + (j & 1) * kKv64;
 #pragma unroll
-        for (int k = 0; k < 4; ++k)  // 16 keys per step: P columns 8k.. (2 fp16 each), V rows 16k..
-          umma_f16_ts(tmem + k3ColO, tmem + k3ColS + 8 * k, T3<D>::desc(smem_u32(vb + k * 16 * D * 2)), idesc_o,
-                      (j > 0 || k > 0) ? 1u : 0u);
+        for (int k = 0; k < 4; ++k) {  // 16 keys per step: P columns 8k.. (2 fp16 each), V rows 16k..
+          const uint64_t vdesc = T3<D>::desc(smem_u32(vb + k * 16 * D * 2));
+          umma_f16_ts(tmem + k3ColO, tmem + k3ColS + 8 * k, vdesc, idesc_o, (j > 0 || k > 0) ? 1u : 0u);
+          if constexpr (QLO) {  // P lo at columns 32 + 8k
+            umma_f16_ts(tmem + k3ColO, tmem + k3ColS + 8 * k, T3<D>::desc(smem_u32(vbl + k * 16 * D * 2)), idesc_o, 1u);
+            umma_f16_ts(tmem + k3ColO, tmem + k3ColS + 32 + 8 * k, vdesc, idesc_o, 1u);
+          }
+        }
         umma_commit(pv_done);
         umma_commit(&kv_empty[j & 1]);
         if (j + 1 < n_chunks) issue_s(j + 1);  // after PV_j in the tensor pipe: P_j is consumed first
@@ -565,18 +585,35 @@ __global__ void __launch_bounds__(kT3Threads, 3)
       }
       const float neg_m = -m;
       float ps = 0.f;
+      if constexpr (QLO) {  // P = hi + lo: hi packed into columns [0, 32), lo into [32, 64), 8 at a time
 #pragma unroll
-      for (int c = 0; c < 2; ++c) {  // P over the (already read) scores, 16 packed columns at a time
-        uint32_t pk[16];
+        for (int g4 = 0; g4 < 4; ++g4) {
+          uint32_t pk[8], pl[8];
 #pragma unroll
-        for (int i = 0; i < 32; i += 2) {
-          const float p0 = ex2(fmaf(__uint_as_float(r[c][i]), scale_log2, neg_m));
-          const float p1 = ex2(fmaf(__uint_as_float(r[c][i + 1]), scale_log2, neg_m));
-          ps += p0 + p1;
-          __half2 hp = __floats2half2_rn(p0, p1);
-          pk[i >> 1] = *reinterpret_cast<uint32_t*>(&hp);
+          for (int i = 0; i < 16; i += 2) {
+            const int c = g4 >> 1, e = (g4 & 1) * 16 + i;
+            const float p0 = ex2(fmaf(__uint_as_float(r[c][e]), scale_log2, neg_m));
+            const float p1 = ex2(fmaf(__uint_as_float(r[c][e + 1]), scale_log2, neg_m));
+            ps += p0 + p1;
+            split_half2(p0, p1, pk[i >> 1], pl[i >> 1]);
+          }
+          tmem_st8(tmem + lane_base + k3ColS + 8 * g4, pk);
+          tmem_st8(tmem + lane_base + k3ColS + 32 + 8 * g4, pl);
         }
-        tmem_st16(tmem + lane_base + k3ColS + 16 * c, pk);
+      } else {
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {  // P over the (already read) scores, 16 packed columns at a time
+          uint32_t pk[16];
+#pragma unroll
+          for (int i = 0; i < 32; i += 2) {
+            const float p0 = ex2(fmaf(__uint_as_float(r[c][i]), scale_log2, neg_m));
+            const float p1 = ex2(fmaf(__uint_as_float(r[c][i + 1]), scale_log2, neg_m));
+            ps += p0 + p1;
+            __half2 hp = __floats2half2_rn(p0, p1);
+            pk[i >> 1] = *reinterpret_cast<uint32_t*>(&hp);
+          }
+          tmem_st16(tmem + lane_base + k3ColS + 16 * c, pk);
+        }
       }
       l += ps;
       if (j >= 1 && __any_sync(0xffffffffu, alpha != 1.f)) {  // rare: rescale this warp's O rows
@@ -632,37 +669,43 @@ __global__ void __launch_bounds__(kT3Threads, 3)
   }
 }
 
-size_t attn_tc3_smem_bytes(int head_dim) {
-  return 1024 + (size_t)128 * head_dim * 2 + 4 * (size_t)64 * head_dim * 2 + 128;
+size_t attn_tc3_smem_bytes(int head_dim, bool qlo) {
+  return 1024 + (size_t)128 * head_dim * 2 + (qlo ? 6 : 4) * (size_t)64 * head_dim * 2 + 128;
 }
 
-template <int D>
+template <int D, bool QLO>
 static void launch_tc3_t(const CUtensorMap& map_q, const CUtensorMap& map_kv, half* ctx, long long lo_off,
                          const int* cu_seqlens, int n_seqs, int max_len, int groups, int n_heads, int hidden,
-                         long long group_rows, cudaStream_t stream) {
+                         long long group_rows, long long lo_rows, cudaStream_t stream) {
   static bool attr_set = false;
-  const size_t smem = attn_tc3_smem_bytes(D);
+  const size_t smem = attn_tc3_smem_bytes(D, QLO);
   if (!attr_set) {
-    cudaFuncSetAttribute(attn_tc3_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaFuncSetAttribute(attn_tc3_kernel<D, QLO>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     attr_set = true;
   }
   const float scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(D));
   dim3 grid(groups * n_heads, n_seqs, (max_len + 127) / 128);
   unsigned long long* tr = trace_alloc_aux(static_cast<int>(grid.x * grid.y * grid.z), 2);
-  launch_pdl(attn_tc3_kernel<D>, grid, dim3(kT3Threads), smem, stream, map_q, map_kv, ctx, cu_seqlens, n_heads, hidden,
-             group_rows, scale_log2, lo_off, tr);
+  launch_pdl(attn_tc3_kernel<D, QLO>, grid, dim3(kT3Threads), smem, stream, map_q, map_kv, ctx, cu_seqlens, n_heads,
+             hidden, group_rows, scale_log2, lo_off, tr, lo_rows);
 }
 
 void launch_attention_tc3(const CUtensorMap& map_q, const CUtensorMap& map_kv, half* ctx, long long lo_off,
                           const int* cu_seqlens, int n_seqs, int max_len, int groups, int n_heads, int hidden,
-                          long long group_rows, cudaStream_t stream) {
+                          long long group_rows, cudaStream_t stream, long long lo_rows) {
   if (n_seqs <= 0 || max_len <= 0 || groups <= 0) return;
-  if (hidden / n_heads == 32)
-    launch_tc3_t<32>(map_q, map_kv, ctx, lo_off, cu_seqlens, n_seqs, max_len, groups, n_heads, hidden, group_rows,
-                     stream);
-  else
-    launch_tc3_t<64>(map_q, map_kv, ctx, lo_off, cu_seqlens, n_seqs, max_len, groups, n_heads, hidden, group_rows,
-                     stream);
+  const bool d32 = hidden / n_heads == 32;
+  if (lo_rows) {
+    if (d32) launch_tc3_t<32, true>(map_q, map_kv, ctx, lo_off, cu_seqlens, n_seqs, max_len, groups, n_heads, hidden,
+                                    group_rows, lo_rows, stream);
+    else launch_tc3_t<64, true>(map_q, map_kv, ctx, lo_off, cu_seqlens, n_seqs, max_len, groups, n_heads, hidden,
+                                group_rows, lo_rows, stream);
+  } else {
+    if (d32) launch_tc3_t<32, false>(map_q, map_kv, ctx, lo_off, cu_seqlens, n_seqs, max_len, groups, n_heads, hidden,
+                                     group_rows, 0, stream);
+    else launch_tc3_t<64, false>(map_q, map_kv, ctx, lo_off, cu_seqlens, n_seqs, max_len, groups, n_heads, hidden,
+                                 group_rows, 0, stream);
+  }
 }
 
 }  // namespace sp

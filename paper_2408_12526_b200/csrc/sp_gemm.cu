@@ -235,7 +235,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     tc_fence_after();
     if (tr && warp == 2 && lane == 0) tr[6] = globaltimer();
     const uint32_t taddr = tmem + (static_cast<uint32_t>(q * 32) << 16);
-    const long long lo_off = OUT_F32 ? 0 : p.out_lo_off;
+    const long long lo_off = (OUT_F32 || m0 < p.lo_from) ? 0 : p.out_lo_off;
     // one chunk of NR accumulator columns (NR = 8 / 16 / 32 >= n: a 16-token tile computes its
     // activation for 16 columns, not 32; the columns of a chunk are independent chains)
     auto chunk = [&](auto nr, int c, int n) {
@@ -561,7 +561,8 @@ __global__ void __launch_bounds__(kPThreads, 1)
 #pragma unroll
         for (int jj = 0; jj < 16; ++jj) y[jj] = apply_act<ACT>(__uint_as_float(r[jj]) + bias);
         warp_store_rows<OutT, 16>(y, 16, stage, out, n0 + c, t_rows, p.out_ld, false);
-        if (lo_off) warp_store_rows<OutT, 16>(y, 16, stage, out + lo_off, n0 + c, t_rows, p.out_ld, true);
+        if (lo_off && m0 >= p.lo_from)
+          warp_store_rows<OutT, 16>(y, 16, stage, out + lo_off, n0 + c, t_rows, p.out_ld, true);
       }
       if (!released) release(b);  // no (live) chunk for this warp in this tile
     }

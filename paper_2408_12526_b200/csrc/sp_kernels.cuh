@@ -74,6 +74,7 @@ struct GemmParams {
   long long out_group_stride;  // elements
   long long out_split_stride;  // elements
   long long out_lo_off;        // fp16 output: lo term at out + out_lo_off (0: hi only)
+  int lo_from;                 // lo term only for output features >= lo_from (the V third of a QKV tile)
   int out_ld;                  // elements between rows
   const float* bias;           // [groups][n_out] or null
   int bias_group_stride;
@@ -140,7 +141,7 @@ void set_attn_trace(unsigned long long* buf);  // debug: per-CTA timeline of att
 // 64-key-chunk variant, three CTAs per SM; map_kv: the qkv buffer with a {64, 64} box.
 void launch_attention_tc3(const CUtensorMap& map_q, const CUtensorMap& map_kv, half* ctx, long long lo_off,
                           const int* cu_seqlens, int n_seqs, int max_len, int groups, int n_heads, int hidden,
-                          long long group_rows, cudaStream_t stream);
+                          long long group_rows, cudaStream_t stream, long long lo_rows = 0);
 
 // Embedding gather + LayerNorm: x = LN(E_word[g][id_t] + E_pos[g][pos_t] + E_type[g][0]); writes
 // x32 and the (hi, lo) operand pair x16 / x16 + x_lo_off.
@@ -184,9 +185,11 @@ void launch_reduce_ln(const RowLn& a, int groups, cudaStream_t stream);
 // values from qkv [g][T][3H]; the query from q[g][seq] (row stride hidden, group stride q_gs), or,
 // when q is null, from the CLS row of qkv. The context row is written as an (hi, lo) pair to
 // ctx[g][seq] (row stride hidden, group stride ctx_gs).
+// qkv_lo / q_lo: element offsets of the (hi, lo) lo planes of qkv / q (0: hi only).
 void launch_attention_cls(const half* qkv, long long qkv_gs, const half* q, long long q_gs, const int* cu_seqlens,
                           int n_seqs, int groups, int n_heads, int head_dim, int hidden, half* ctx, long long ctx_gs,
-                          long long lo_off, int max_len, cudaStream_t stream);
+                          long long lo_off, int max_len, cudaStream_t stream, long long qkv_lo = 0,
+                          long long q_lo = 0);
 
 // Boosting sum + shared classifier (distill.py:169-178, :512):
 //   final[m][b] = splits ? tanh(sum_s part[s][m][b] + b_pool[m]) : final_rep[m][b]

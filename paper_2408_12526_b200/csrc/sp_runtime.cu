@@ -130,7 +130,8 @@ struct sp_group {
   int rows_cap = 0;  // max(max_tokens, max_seqs)
   // workspace; "[2]" planes are the (hi, lo) terms of a GEMM operand, lo at +*_lo elements
   half* x16 = nullptr;     // [2][S][max_tokens][H] LayerNorm output (QKV / FFN1 operand)
-  half* qkv = nullptr;     // [S][max_tokens][3H]
+  half* qkv = nullptr;     // [2][S][max_tokens][3H]: hi plane, then the lo plane at qkv_lo
+  long long qkv_lo = 0;
   half* ctx = nullptr;     // [2][S][max_tokens][H] attention context (O operand)
   half* ffn = nullptr;     // [2][S][max_tokens][F] GELU output (FFN2 operand)
   float* part = nullptr;   // [kMaxSplits][S][max_tokens][H] split-K partials
@@ -339,7 +340,8 @@ int sp_group_create(const sp_config* cfg, const sp_weights* weights, int device,
     g->ffn_lo = (long long)(S * T * F);
     g->cls_lo = (long long)(S * B * H);
     if ((rc = dev_alloc(g, &g->x16, 2 * S * T * H))) return bail(rc);
-    if ((rc = dev_alloc(g, &g->qkv, S * T * 3 * H))) return bail(rc);
+    g->qkv_lo = (long long)S * T * 3 * H;
+    if ((rc = dev_alloc(g, &g->qkv, 2 * S * T * 3 * H))) return bail(rc);
     if ((rc = dev_alloc(g, &g->ctx, 2 * S * T * H))) return bail(rc);
     if ((rc = dev_alloc(g, &g->ffn, 2 * S * T * F))) return bail(rc);
     if ((rc = dev_alloc(g, &g->part, (size_t)kMaxSplits * S * T * H))) return bail(rc);
@@ -350,7 +352,7 @@ int sp_group_create(const sp_config* cfg, const sp_weights* weights, int device,
     if ((rc = dev_alloc(g, &g->ctxc, 2 * S * B * H))) return bail(rc);
     if ((rc = dev_alloc(g, &g->ffnc, 2 * S * B * F))) return bail(rc);
     if ((rc = dev_alloc(g, &g->partc, (size_t)kMaxSplits * S * B * H))) return bail(rc);
-    if ((rc = dev_alloc(g, &g->qc, S * B * H))) return bail(rc);
+    if ((rc = dev_alloc(g, &g->qc, 2 * S * B * H))) return bail(rc);  // (hi, lo)
 
     const auto* wq = static_cast<const half*>(w.w_qkv);
     const auto* wo = static_cast<const half*>(w.w_o);
@@ -376,10 +378,11 @@ int sp_group_create(const sp_config* cfg, const sp_weights* weights, int device,
     ok &= make_xmaps(&g->xm_ctxc, g->ctxc, g->ctxc + g->cls_lo, S * B, H);
     ok &= make_xmaps(&g->xm_ffnc, g->ffnc, g->ffnc + g->cf_lo, S * B, F);
     const uint32_t head_box = (H / c.n_heads == 32) ? 32 : 64;  // head_dim-32 tiles: 64-byte rows
-    ok &= make_map(&g->m_qkv_attn, g->qkv, S * T, 3 * H, 128, head_box);
-    ok &= make_map(&g->m_qkv_kv64, g->qkv, S * T, 3 * H, 64, head_box);
+    // over both planes: a lo tile is the hi tile's rows + S * T
+    ok &= make_map(&g->m_qkv_attn, g->qkv, 2 * S * T, 3 * H, 128, head_box);
+    ok &= make_map(&g->m_qkv_kv64, g->qkv, 2 * S * T, 3 * H, 64, head_box);
     // rows past a request's tokens are read (masked) by the attention tiles: keep them finite
-    if (cudaMemset(g->qkv, 0, S * T * 3 * H * sizeof(half)) != cudaSuccess) ok = false;
+    if (cudaMemset(g->qkv, 0, 2 * S * T * 3 * H * sizeof(half)) != cudaSuccess) ok = false;
     if (!ok) return bail(fail(SP_EINVAL, "tensor-map creation failed (pointer alignment / shape)"));
   } else {
     if (!w.w_in || !w.b_in || !w.w_layers || !w.b_layers || !w.alpha || !w.w_cls || !w.b_cls)
@@ -454,13 +457,24 @@ namespace {
 // latency chain) up to 64 tokens (-2 us), tc1 to 128, tc2 from 129; above 384 (4 query tiles per
 // head) tc3's one wave at three CTAs per SM beats tc2's two waves (-6..-10 us per request).
 // SP_ATTN_TC=0..3 forces one kernel (the forced-kernel parity tests).
-int attn_kind(int head_dim, int max_len) {
+// Attention inputs (Q / K / V) as (hi, lo) pairs; SP_ATTN_LO=0 keeps them hi only (A/B switch)
+bool attn_lo_enabled() {
+  static const bool on = [] {
+    const char* v = getenv("SP_ATTN_LO");
+    return v == nullptr || atoi(v) != 0;
+  }();
+  return on;
+}
+
+// lo: Q/K/V carry (hi, lo) pairs — only the three-CTA kernel takes them (unless a kernel is forced)
+int attn_kind(int head_dim, int max_len, bool lo = false) {
   static const int mode = [] {
     const char* v = getenv("SP_ATTN_TC");
     return v == nullptr ? -1 : atoi(v);
   }();
   if (max_len > 512 || (head_dim != 64 && head_dim != 32)) return 0;
   if (head_dim == 32) return mode == 0 ? 0 : 3;  // the three-CTA tcgen05 kernel has a head_dim-32 variant
+  if (lo && mode < 0) return 3;
   if (mode >= 0) return mode;
   if (max_len <= 64) return 3;
   return max_len <= 128 ? 1 : (max_len <= 384 ? 2 : 3);
@@ -468,10 +482,10 @@ int attn_kind(int head_dim, int max_len) {
 
 void launch_attention_any(int kind, const CUtensorMap& map_qkv, const CUtensorMap& map_kv64, const half* qkv,
                           half* ctx, long long lo_off, const int* cu, int n_seqs, int max_len, int groups, int n_heads,
-                          int head_dim, int hidden, long long group_rows, cudaStream_t st) {
+                          int head_dim, int hidden, long long group_rows, cudaStream_t st, long long lo_rows = 0) {
   if (kind == 3)
     sp::launch_attention_tc3(map_qkv, map_kv64, ctx, lo_off, cu, n_seqs, max_len, groups, n_heads, hidden, group_rows,
-                             st);
+                             st, lo_rows);
   else if (kind == 2)
     sp::launch_attention_tc2(map_qkv, ctx, lo_off, cu, n_seqs, max_len, groups, n_heads, hidden, group_rows, st);
   else if (kind == 1)
@@ -485,7 +499,7 @@ void run_gemm(sp_group* grp, int kind, const CUtensorMap& wmap, const XMaps& xm,
               int t_rows, int x_group_rows, const float* bias, int bias_gs, int act, void* out, long long out_gs,
               long long out_lo_off, int out_f32, int splits, long long split_stride, cudaStream_t st,
               const int* t_dev = nullptr, int out_ld = 0, int w_gs = 0, int w_r0 = 0,
-              const CUtensorMap* wlo = nullptr) {
+              const CUtensorMap* wlo = nullptr, int lo_from = 0) {
   sp::GemmParams p{};
   p.t_dev = t_dev;
   p.n_out = n_out;
@@ -499,6 +513,7 @@ void run_gemm(sp_group* grp, int kind, const CUtensorMap& wmap, const XMaps& xm,
   p.out = out;
   p.out_group_stride = out_gs;
   p.out_lo_off = out_f32 ? 0 : out_lo_off;
+  p.lo_from = lo_from;
   p.out_ld = out_ld ? out_ld : n_out;
   p.bias = bias;
   p.bias_group_stride = bias_gs;
@@ -629,7 +644,7 @@ int bert_forward(sp_group* g, const int32_t* ids, const int32_t* cu, int n_seqs,
     const long long part_ss = (long long)S * xgs;
     const int s_o = choose_splits(k * (H / 128) * n_tiles, H / 64, kMaxSplits, bn);
     const int s_f = choose_splits(k * (H / 128) * n_tiles, F / 64, kMaxSplits, bn);
-    const int akind = attn_kind(H / c.n_heads, max_len);
+    const int akind = attn_kind(H / c.n_heads, max_len, attn_lo_enabled());
     // CLS-row projections of the last layer: n_seqs rows per student
     const long long bgs = (long long)B * H, partc_ss = (long long)S * bgs;
     int bn_c, n_tiles_c;
@@ -640,6 +655,7 @@ int bert_forward(sp_group* g, const int32_t* ids, const int32_t* cu, int n_seqs,
     // last layer: K/V of every token + the CLS query as a second GEMM only for the largest requests
     // (L12 at 512 tokens: -4.7 us); for B8 it measured 2-4.5 us slower at every length (256-512)
     const bool split_q = c.n_layers > 1 && (long long)n_tokens * H >= 448LL * 1024;
+    const long long qkv_lo = attn_lo_enabled() ? g->qkv_lo : 0;
     // one LayerNorm launch (rows of k students)
     auto layer_norm = [&](const float* part, int splits, long long pss, long long pgs, const float* b_, const float* g_,
                           const float* be_, const float* x_in, long long in_gs, const int* in_rows, float* x_out,
@@ -687,13 +703,18 @@ int bert_forward(sp_group* g, const int32_t* ids, const int32_t* cu, int n_seqs,
         // QKV slab), the query of the CLS rows only (rows [0, H) on the CLS copies the previous
         // LayerNorm wrote)
         run_gemm(g, SP_LAUNCH_GEMM_QKV, g->m_qkv[l], g->xm_x16, k, 2 * H, H, n_tokens, T, w.b_qkv + lS * 3 * H + H,
-                 3 * H, sp::ACT_NONE, g->qkv + H, (long long)T * 3 * H, 0, 0, 1, 0, st, t_dev, 3 * H, 3 * H, H);
+                 3 * H, sp::ACT_NONE, g->qkv + H, (long long)T * 3 * H, qkv_lo, 0, 1, 0, st, t_dev, 3 * H, 3 * H, H);
         run_gemm(g, SP_LAUNCH_GEMM_QKV, g->m_qkv[l], g->xm_cls, k, H, H, n_seqs, B, w.b_qkv + lS * 3 * H, 3 * H,
-                 sp::ACT_NONE, g->qc, bgs, 0, 0, 1, 0, st, nullptr, H, 3 * H, 0);
+                 sp::ACT_NONE, g->qc, bgs, qkv_lo ? (long long)S * B * H : 0, 0, 1, 0, st, nullptr, H, 3 * H, 0);
         launches += 2;
       } else {
+        // lo terms where they matter (tools/diag_prefix.py, worst prefix cases: V 0.7-3.0e-3 of
+        // max|z|, Q and K together <= 4.8e-4): V for the tensor-core attention of the inner layers,
+        // Q, K and V for the last layer's fp32 CLS attention (without q / K lo the worst case went
+        // from 6.7e-4 to 8.1e-4 at no measurable saving)
         run_gemm(g, SP_LAUNCH_GEMM_QKV, g->m_qkv[l], g->xm_x16, k, 3 * H, H, n_tokens, T, w.b_qkv + lS * 3 * H,
-                 3 * H, sp::ACT_NONE, g->qkv, (long long)T * 3 * H, 0, 0, 1, 0, st, t_dev);
+                 3 * H, sp::ACT_NONE, g->qkv, (long long)T * 3 * H, qkv_lo, 0, 1, 0, st, t_dev, 0, 0, 0, nullptr,
+                 last ? 0 : 2 * H);
         ++launches;
       }
       if (last) {
@@ -702,7 +723,8 @@ int bert_forward(sp_group* g, const int32_t* ids, const int32_t* cu, int n_seqs,
         // (n_seqs rows per student; the residual input is gathered at cu_seqlens[b]).
         g->rec_begin(SP_LAUNCH_ATTENTION, GTH * 4.0, 4.0 * k * H * (double)n_tokens);
         sp::launch_attention_cls(g->qkv, (long long)T * 3 * H, split_q ? g->qc : nullptr, bgs, cu, n_seqs, k,
-                                 c.n_heads, H / c.n_heads, H, g->ctxc, bgs, g->cls_lo, max_len, st);
+                                 c.n_heads, H / c.n_heads, H, g->ctxc, bgs, g->cls_lo, max_len, st, qkv_lo,
+                                 split_q ? (qkv_lo ? (long long)S * B * H : 0) : qkv_lo);
         g->rec_end();
         run_gemm(g, SP_LAUNCH_GEMM_O, g->m_o[l], g->xm_ctxc, k, H, H, n_seqs, B, nullptr, H, sp::ACT_NONE, g->partc,
                  bgs, 0, 1, s_oc, partc_ss, st);
@@ -720,7 +742,7 @@ int bert_forward(sp_group* g, const int32_t* ids, const int32_t* cu, int n_seqs,
       }
       g->rec_begin(SP_LAUNCH_ATTENTION, GTH * 10.0, 4.0 * k * H * g->sum_len_sq);
       launch_attention_any(akind, g->m_qkv_attn, g->m_qkv_kv64, g->qkv, g->ctx, g->ctx_lo, cu, n_seqs, max_len, k,
-                           c.n_heads, H / c.n_heads, H, T, st);
+                           c.n_heads, H / c.n_heads, H, T, st, akind == 3 && qkv_lo ? (long long)S * T : 0);
       g->rec_end();
       // O and FFN2 write raw partial sums; the reduce+LN kernel owns bias, residual and LayerNorm
       run_gemm(g, SP_LAUNCH_GEMM_O, g->m_o[l], g->xm_ctx, k, H, H, n_tokens, T, nullptr, H, sp::ACT_NONE, g->part, xgs,

@@ -25,6 +25,10 @@ def emulate(name, K, seed, L, k, pts):
             last = li == nl - 1
             qkv = h(dense_layer(*lay["qkv"], x, IDENTITY),
                     "qkv" in pts or (f"qkv{li}" in pts) or ("qkvL" in pts and last))
+            if li == 0:  # per-operand rounding of the first layer's attention inputs
+                for nm, i in (("q0", 0), ("k0", 1), ("v0", 2)):
+                    if nm in pts:
+                        qkv[:, i * H:(i + 1) * H] = h(qkv[:, i * H:(i + 1) * H], True)
             q, kk, v = (qkv[:, i * H:(i + 1) * H].reshape(L, nh, hd) for i in range(3))
             sc = np.einsum("qhd,khd->hqk", q, kk) / np.sqrt(hd)
             p = np.exp(sc - sc.max(-1, keepdims=True))
@@ -41,7 +45,7 @@ name, seed, L, k = (sys.argv[1], int(sys.argv[2]), int(sys.argv[3]), int(sys.arg
 from paper_2408_12526_b200 import PRESETS
 K = PRESETS[name][1]
 z0, ids = emulate(name, K, seed, L, k, set())
-for pts in (["qkv"], ["qkv0"], ["qkvL"], ["p"], ["qkv", "p"], ["qkv0", "p"]):
+for pts in (["qkv0"], ["q0"], ["k0"], ["v0"], ["p"], ["q0", "k0"], ["q0", "k0", "p"], ["v0", "p"]):
     z, _ = emulate(name, K, seed, L, k, set(pts))
     print(f"emulated fp16 at {'+'.join(pts):8s}: {np.abs(z - z0).max() / np.abs(z0).max():.2e}  (max|z| {np.abs(z0).max():.4f})")
 if os.environ.get("DIAG_CHILD") is None:
