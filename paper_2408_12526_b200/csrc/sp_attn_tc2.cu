@@ -423,7 +423,9 @@ struct T3 {
 // operands like the projections. The fp16 rounding of V and P dominated the adaptive-prefix cases
 // whose logits cancel (tools/diag_prefix.py: V 0.7-3.0e-3, P 0.1-1.3e-3 of max|z|; Q and K
 // together <= 4.8e-4), so S = Q K^T stays one MMA on the hi terms.
-template <int D, bool QLO>
+// QKLO (implies QLO): Q and K are (hi, lo) pairs too: S = Qh Kh + Ql Kh + Qh Kl. 99 KiB of shared
+// memory per CTA (two CTAs per SM) for the last fp16 rounding point of the attention inputs.
+template <int D, bool QLO, bool QKLO = false>
 __global__ void __launch_bounds__(kT3Threads, 3)
     attn_tc3_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_kv,
                     half* __restrict__ ctx, const int* __restrict__ cu, int n_heads, int hidden, long long group_rows,
@@ -437,11 +439,14 @@ __global__ void __launch_bounds__(kT3Threads, 3)
   constexpr int kKv64 = T3<D>::kKv;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  static_assert(QLO || !QKLO, "QKLO implies QLO");
   uint8_t* sQ = smem;                 // 16 KiB (D = 64) / 8 KiB
-  uint8_t* sK = sQ + T3<D>::kQ;       // [2] x 8 / 4 KiB
+  uint8_t* sQl = sQ + T3<D>::kQ;      // QKLO: Q lo
+  uint8_t* sK = sQl + (QKLO ? T3<D>::kQ : 0);  // [2] x 8 / 4 KiB
   uint8_t* sV = sK + 2 * kKv64;       // [2] x 8 / 4 KiB
   uint8_t* sVl = sV + 2 * kKv64;      // QLO: [2] V lo
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sVl + (QLO ? 2 * kKv64 : 0));
+  uint8_t* sKl = sVl + (QLO ? 2 * kKv64 : 0);  // QKLO: [2] K lo
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sKl + (QKLO ? 2 * kKv64 : 0));
   uint64_t* q_full = bars;
   uint64_t* kv_full = bars + 1;   // [2]
   uint64_t* kv_empty = bars + 3;  // [2]
@@ -491,16 +496,20 @@ __global__ void __launch_bounds__(kT3Threads, 3)
       const uint64_t pol = policy_evict_last();
       pdl_wait();  // qkv is the previous kernel's output
       if (tr) tr[1] = globaltimer();
-      mbar_arrive_expect_tx(q_full, T3<D>::kQ);
+      mbar_arrive_expect_tx(q_full, (QKLO ? 2 : 1) * T3<D>::kQ);
       tma_load_2d(&map_q, q_full, sQ, h * D, row_base + q0, pol);
+      if constexpr (QKLO) tma_load_2d(&map_q, q_full, sQl, h * D, (int)(row_base + q0 + lo_rows), pol);
       for (int j = 0; j < n_chunks; ++j) {
         const int st = j & 1;
         if (j >= 2) mbar_wait(&kv_empty[st], ((j >> 1) - 1) & 1);
-        mbar_arrive_expect_tx(&kv_full[st], (QLO ? 3 : 2) * kKv64);
+        mbar_arrive_expect_tx(&kv_full[st], (QKLO ? 4 : QLO ? 3 : 2) * kKv64);
         tma_load_2d(&map_kv, &kv_full[st], sK + st * kKv64, hidden + h * D, row_base + j * 64, pol);
         tma_load_2d(&map_kv, &kv_full[st], sV + st * kKv64, 2 * hidden + h * D, row_base + j * 64, pol);
         if constexpr (QLO)
           tma_load_2d(&map_kv, &kv_full[st], sVl + st * kKv64, 2 * hidden + h * D, (int)(row_base + j * 64 + lo_rows),
+                      pol);
+        if constexpr (QKLO)
+          tma_load_2d(&map_kv, &kv_full[st], sKl + st * kKv64, hidden + h * D, (int)(row_base + j * 64 + lo_rows),
                       pol);
       }
     }
@@ -518,6 +527,15 @@ __global__ void __launch_bounds__(kT3Threads, 3)
 #pragma unroll
         for (int k = 0; k < D / 16; ++k)
           umma_f16_ss(tmem + k3ColS, qdesc + 2 * k, kdesc + 2 * k, idesc_s, k > 0 ? 1u : 0u);
+        if constexpr (QKLO) {
+          const uint64_t qldesc = T3<D>::desc(smem_u32(sQl));
+          const uint64_t kldesc = T3<D>::desc(smem_u32(sKl + (j & 1) * kKv64));
+#pragma unroll
+          for (int k = 0; k < D / 16; ++k) {
+            umma_f16_ss(tmem + k3ColS, qldesc + 2 * k, kdesc + 2 * k, idesc_s, 1u);
+            umma_f16_ss(tmem + k3ColS, qdesc + 2 * k, kldesc + 2 * k, idesc_s, 1u);
+          }
+        }
         umma_commit(s_full);
       };
       issue_s(0);
@@ -669,33 +687,39 @@ __global__ void __launch_bounds__(kT3Threads, 3)
   }
 }
 
-size_t attn_tc3_smem_bytes(int head_dim, bool qlo) {
-  return 1024 + (size_t)128 * head_dim * 2 + (qlo ? 6 : 4) * (size_t)64 * head_dim * 2 + 128;
+size_t attn_tc3_smem_bytes(int head_dim, bool qlo, bool qklo) {
+  return 1024 + (size_t)(qklo ? 2 : 1) * 128 * head_dim * 2 + (qklo ? 8 : qlo ? 6 : 4) * (size_t)64 * head_dim * 2 +
+         128;
 }
 
-template <int D, bool QLO>
+template <int D, bool QLO, bool QKLO = false>
 static void launch_tc3_t(const CUtensorMap& map_q, const CUtensorMap& map_kv, half* ctx, long long lo_off,
                          const int* cu_seqlens, int n_seqs, int max_len, int groups, int n_heads, int hidden,
                          long long group_rows, long long lo_rows, cudaStream_t stream) {
   static bool attr_set = false;
-  const size_t smem = attn_tc3_smem_bytes(D, QLO);
+  const size_t smem = attn_tc3_smem_bytes(D, QLO, QKLO);
   if (!attr_set) {
-    cudaFuncSetAttribute(attn_tc3_kernel<D, QLO>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaFuncSetAttribute(attn_tc3_kernel<D, QLO, QKLO>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     attr_set = true;
   }
   const float scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(D));
   dim3 grid(groups * n_heads, n_seqs, (max_len + 127) / 128);
   unsigned long long* tr = trace_alloc_aux(static_cast<int>(grid.x * grid.y * grid.z), 2);
-  launch_pdl(attn_tc3_kernel<D, QLO>, grid, dim3(kT3Threads), smem, stream, map_q, map_kv, ctx, cu_seqlens, n_heads,
+  launch_pdl(attn_tc3_kernel<D, QLO, QKLO>, grid, dim3(kT3Threads), smem, stream, map_q, map_kv, ctx, cu_seqlens, n_heads,
              hidden, group_rows, scale_log2, lo_off, tr, lo_rows);
 }
 
 void launch_attention_tc3(const CUtensorMap& map_q, const CUtensorMap& map_kv, half* ctx, long long lo_off,
                           const int* cu_seqlens, int n_seqs, int max_len, int groups, int n_heads, int hidden,
-                          long long group_rows, cudaStream_t stream, long long lo_rows) {
+                          long long group_rows, cudaStream_t stream, long long lo_rows, bool qk_lo) {
   if (n_seqs <= 0 || max_len <= 0 || groups <= 0) return;
   const bool d32 = hidden / n_heads == 32;
-  if (lo_rows) {
+  if (lo_rows && qk_lo) {
+    if (d32) launch_tc3_t<32, true, true>(map_q, map_kv, ctx, lo_off, cu_seqlens, n_seqs, max_len, groups, n_heads,
+                                          hidden, group_rows, lo_rows, stream);
+    else launch_tc3_t<64, true, true>(map_q, map_kv, ctx, lo_off, cu_seqlens, n_seqs, max_len, groups, n_heads, hidden,
+                                      group_rows, lo_rows, stream);
+  } else if (lo_rows) {
     if (d32) launch_tc3_t<32, true>(map_q, map_kv, ctx, lo_off, cu_seqlens, n_seqs, max_len, groups, n_heads, hidden,
                                     group_rows, lo_rows, stream);
     else launch_tc3_t<64, true>(map_q, map_kv, ctx, lo_off, cu_seqlens, n_seqs, max_len, groups, n_heads, hidden,

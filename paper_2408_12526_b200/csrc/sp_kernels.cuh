@@ -141,7 +141,7 @@ void set_attn_trace(unsigned long long* buf);  // debug: per-CTA timeline of att
 // 64-key-chunk variant, three CTAs per SM; map_kv: the qkv buffer with a {64, 64} box.
 void launch_attention_tc3(const CUtensorMap& map_q, const CUtensorMap& map_kv, half* ctx, long long lo_off,
                           const int* cu_seqlens, int n_seqs, int max_len, int groups, int n_heads, int hidden,
-                          long long group_rows, cudaStream_t stream, long long lo_rows = 0);
+                          long long group_rows, cudaStream_t stream, long long lo_rows = 0, bool qk_lo = false);
 
 // Embedding gather + LayerNorm: x = LN(E_word[g][id_t] + E_pos[g][pos_t] + E_type[g][0]); writes
 // x32 and the (hi, lo) operand pair x16 / x16 + x_lo_off.

@@ -457,14 +457,18 @@ namespace {
 // latency chain) up to 64 tokens (-2 us), tc1 to 128, tc2 from 129; above 384 (4 query tiles per
 // head) tc3's one wave at three CTAs per SM beats tc2's two waves (-6..-10 us per request).
 // SP_ATTN_TC=0..3 forces one kernel (the forced-kernel parity tests).
-// Attention inputs (Q / K / V) as (hi, lo) pairs; SP_ATTN_LO=0 keeps them hi only (A/B switch)
-bool attn_lo_enabled() {
-  static const bool on = [] {
+// Attention inputs as (hi, lo) pairs. SP_ATTN_LO: 0 = hi only (A/B switch), 1 = V and P of the
+// tensor-core attention (Q / K / V of the CLS attention), 2 = Q and K of the tensor-core attention too
+constexpr int kAttnLoDefault = 2;
+int attn_lo_level() {
+  static const int level = [] {
     const char* v = getenv("SP_ATTN_LO");
-    return v == nullptr || atoi(v) != 0;
+    return v == nullptr ? kAttnLoDefault : atoi(v);
   }();
-  return on;
+  return level;
 }
+bool attn_lo_enabled() { return attn_lo_level() > 0; }
+bool attn_qk_lo() { return attn_lo_level() >= 2; }
 
 // lo: Q/K/V carry (hi, lo) pairs — only the three-CTA kernel takes them (unless a kernel is forced)
 int attn_kind(int head_dim, int max_len, bool lo = false) {
@@ -482,10 +486,11 @@ int attn_kind(int head_dim, int max_len, bool lo = false) {
 
 void launch_attention_any(int kind, const CUtensorMap& map_qkv, const CUtensorMap& map_kv64, const half* qkv,
                           half* ctx, long long lo_off, const int* cu, int n_seqs, int max_len, int groups, int n_heads,
-                          int head_dim, int hidden, long long group_rows, cudaStream_t st, long long lo_rows = 0) {
+                          int head_dim, int hidden, long long group_rows, cudaStream_t st, long long lo_rows = 0,
+                          bool qk_lo = false) {
   if (kind == 3)
     sp::launch_attention_tc3(map_qkv, map_kv64, ctx, lo_off, cu, n_seqs, max_len, groups, n_heads, hidden, group_rows,
-                             st, lo_rows);
+                             st, lo_rows, qk_lo);
   else if (kind == 2)
     sp::launch_attention_tc2(map_qkv, ctx, lo_off, cu, n_seqs, max_len, groups, n_heads, hidden, group_rows, st);
   else if (kind == 1)
@@ -714,7 +719,7 @@ int bert_forward(sp_group* g, const int32_t* ids, const int32_t* cu, int n_seqs,
         // from 6.7e-4 to 8.1e-4 at no measurable saving)
         run_gemm(g, SP_LAUNCH_GEMM_QKV, g->m_qkv[l], g->xm_x16, k, 3 * H, H, n_tokens, T, w.b_qkv + lS * 3 * H,
                  3 * H, sp::ACT_NONE, g->qkv, (long long)T * 3 * H, qkv_lo, 0, 1, 0, st, t_dev, 0, 0, 0, nullptr,
-                 last ? 0 : 2 * H);
+                 last || attn_qk_lo() ? 0 : 2 * H);
         ++launches;
       }
       if (last) {
@@ -742,7 +747,8 @@ int bert_forward(sp_group* g, const int32_t* ids, const int32_t* cu, int n_seqs,
       }
       g->rec_begin(SP_LAUNCH_ATTENTION, GTH * 10.0, 4.0 * k * H * g->sum_len_sq);
       launch_attention_any(akind, g->m_qkv_attn, g->m_qkv_kv64, g->qkv, g->ctx, g->ctx_lo, cu, n_seqs, max_len, k,
-                           c.n_heads, H / c.n_heads, H, T, st, akind == 3 && qkv_lo ? (long long)S * T : 0);
+                           c.n_heads, H / c.n_heads, H, T, st, akind == 3 && qkv_lo ? (long long)S * T : 0,
+                           attn_qk_lo());
       g->rec_end();
       // O and FFN2 write raw partial sums; the reduce+LN kernel owns bias, residual and LayerNorm
       run_gemm(g, SP_LAUNCH_GEMM_O, g->m_o[l], g->xm_ctx, k, H, H, n_tokens, T, nullptr, H, sp::ACT_NONE, g->part, xgs,
