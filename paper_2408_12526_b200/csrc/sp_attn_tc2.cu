@@ -422,10 +422,10 @@ struct T3 {
 // too: O += Ph Vh + Ph Vl + Pl Vh (three MMAs per 16-key step), so the context carries ~22-bit
 // operands like the projections. The fp16 rounding of V and P dominated the adaptive-prefix cases
 // whose logits cancel (tools/diag_prefix.py: V 0.7-3.0e-3, P 0.1-1.3e-3 of max|z|; Q and K
-// together <= 4.8e-4), so S = Q K^T stays one MMA on the hi terms.
+// together <= 4.8e-4 there, but 9.6e-4 in K32 seed 146's k=30 prefix: hence QKLO, the default).
 // QKLO (implies QLO): Q and K are (hi, lo) pairs too: S = Qh Kh + Ql Kh + Qh Kl. 99 KiB of shared
-// memory per CTA (two CTAs per SM) for the last fp16 rounding point of the attention inputs.
-template <int D, bool QLO, bool QKLO = false>
+// memory per CTA (two CTAs per SM): +0 us up to L=384, +14 us at L=512 (two waves, len_probe).
+template <int D, bool QLO, bool QKLO = false, int NS = 2>
 __global__ void __launch_bounds__(kT3Threads, 3)
     attn_tc3_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_kv,
                     half* __restrict__ ctx, const int* __restrict__ cu, int n_heads, int hidden, long long group_rows,
@@ -443,10 +443,11 @@ __global__ void __launch_bounds__(kT3Threads, 3)
   uint8_t* sQ = smem;                 // 16 KiB (D = 64) / 8 KiB
   uint8_t* sQl = sQ + T3<D>::kQ;      // QKLO: Q lo
   uint8_t* sK = sQl + (QKLO ? T3<D>::kQ : 0);  // [2] x 8 / 4 KiB
-  uint8_t* sV = sK + 2 * kKv64;       // [2] x 8 / 4 KiB
-  uint8_t* sVl = sV + 2 * kKv64;      // QLO: [2] V lo
-  uint8_t* sKl = sVl + (QLO ? 2 * kKv64 : 0);  // QKLO: [2] K lo
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sKl + (QKLO ? 2 * kKv64 : 0));
+  static_assert(NS == 1 || NS == 2, "K/V ring of one or two 64-key stages");
+  uint8_t* sV = sK + NS * kKv64;      // [NS] x 8 / 4 KiB
+  uint8_t* sVl = sV + NS * kKv64;     // QLO: [NS] V lo
+  uint8_t* sKl = sVl + (QLO ? NS * kKv64 : 0);  // QKLO: [NS] K lo
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sKl + (QKLO ? NS * kKv64 : 0));
   uint64_t* q_full = bars;
   uint64_t* kv_full = bars + 1;   // [2]
   uint64_t* kv_empty = bars + 3;  // [2]
@@ -500,8 +501,8 @@ __global__ void __launch_bounds__(kT3Threads, 3)
       tma_load_2d(&map_q, q_full, sQ, h * D, row_base + q0, pol);
       if constexpr (QKLO) tma_load_2d(&map_q, q_full, sQl, h * D, (int)(row_base + q0 + lo_rows), pol);
       for (int j = 0; j < n_chunks; ++j) {
-        const int st = j & 1;
-        if (j >= 2) mbar_wait(&kv_empty[st], ((j >> 1) - 1) & 1);
+        const int st = j % NS;
+        if (j >= NS) mbar_wait(&kv_empty[st], (j / NS - 1) & 1);
         mbar_arrive_expect_tx(&kv_full[st], (QKLO ? 4 : QLO ? 3 : 2) * kKv64);
         tma_load_2d(&map_kv, &kv_full[st], sK + st * kKv64, hidden + h * D, row_base + j * 64, pol);
         tma_load_2d(&map_kv, &kv_full[st], sV + st * kKv64, 2 * hidden + h * D, row_base + j * 64, pol);
@@ -521,15 +522,15 @@ __global__ void __launch_bounds__(kT3Threads, 3)
       const uint64_t qdesc = T3<D>::desc(smem_u32(sQ));
       mbar_wait(q_full, 0);
       auto issue_s = [&](int j) {
-        mbar_wait(&kv_full[j & 1], (j >> 1) & 1);
+        mbar_wait(&kv_full[j % NS], (j / NS) & 1);
         tc_fence_after();
-        const uint64_t kdesc = T3<D>::desc(smem_u32(sK + (j & 1) * kKv64));
+        const uint64_t kdesc = T3<D>::desc(smem_u32(sK + (j % NS) * kKv64));
 #pragma unroll
         for (int k = 0; k < D / 16; ++k)
           umma_f16_ss(tmem + k3ColS, qdesc + 2 * k, kdesc + 2 * k, idesc_s, k > 0 ? 1u : 0u);
         if constexpr (QKLO) {
           const uint64_t qldesc = T3<D>::desc(smem_u32(sQl));
-          const uint64_t kldesc = T3<D>::desc(smem_u32(sKl + (j & 1) * kKv64));
+          const uint64_t kldesc = T3<D>::desc(smem_u32(sKl + (j % NS) * kKv64));
 #pragma unroll
           for (int k = 0; k < D / 16; ++k) {
             umma_f16_ss(tmem + k3ColS, qldesc + 2 * k, kdesc + 2 * k, idesc_s, 1u);
@@ -543,8 +544,8 @@ __global__ void __launch_bounds__(kT3Threads, 3)
       for (int j = 0; j < n_chunks; ++j) {
         mbar_wait(p_full, j & 1);  // P_j is in TMEM columns [0, 32)
         tc_fence_after();
-        const uint8_t* vb = sV + (j & 1) * kKv64;
-        const uint8_t* vbl = sVl + (j & 1) * kKv64;
+        const uint8_t* vb = sV + (j % NS) * kKv64;
+        const uint8_t* vbl = sVl + (j % NS) * kKv64;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {  // 16 keys per step: P columns 8k.. (2 fp16 each), V rows 16k..
           const uint64_t vdesc = T3<D>::desc(smem_u32(vb + k * 16 * D * 2));
@@ -555,7 +556,7 @@ __global__ void __launch_bounds__(kT3Threads, 3)
           }
         }
         umma_commit(pv_done);
-        umma_commit(&kv_empty[j & 1]);
+        umma_commit(&kv_empty[j % NS]);
         if (j + 1 < n_chunks) issue_s(j + 1);  // after PV_j in the tensor pipe: P_j is consumed first
       }
       if (tr) tr[4] = globaltimer();
@@ -687,25 +688,27 @@ __global__ void __launch_bounds__(kT3Threads, 3)
   }
 }
 
-size_t attn_tc3_smem_bytes(int head_dim, bool qlo, bool qklo) {
-  return 1024 + (size_t)(qklo ? 2 : 1) * 128 * head_dim * 2 + (qklo ? 8 : qlo ? 6 : 4) * (size_t)64 * head_dim * 2 +
-         128;
+size_t attn_tc3_smem_bytes(int head_dim, bool qlo, bool qklo, int ns) {
+  return 1024 + (size_t)(qklo ? 2 : 1) * 128 * head_dim * 2 +
+         (qklo ? 4 : qlo ? 3 : 2) * (size_t)ns * 64 * head_dim * 2 + 128;
 }
 
-template <int D, bool QLO, bool QKLO = false>
+constexpr int kTc3OneStageFrom = 384;
+
+template <int D, bool QLO, bool QKLO = false, int NS = 2>
 static void launch_tc3_t(const CUtensorMap& map_q, const CUtensorMap& map_kv, half* ctx, long long lo_off,
                          const int* cu_seqlens, int n_seqs, int max_len, int groups, int n_heads, int hidden,
                          long long group_rows, long long lo_rows, cudaStream_t stream) {
   static bool attr_set = false;
-  const size_t smem = attn_tc3_smem_bytes(D, QLO, QKLO);
+  const size_t smem = attn_tc3_smem_bytes(D, QLO, QKLO, NS);
   if (!attr_set) {
-    cudaFuncSetAttribute(attn_tc3_kernel<D, QLO, QKLO>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaFuncSetAttribute(attn_tc3_kernel<D, QLO, QKLO, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     attr_set = true;
   }
   const float scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(D));
   dim3 grid(groups * n_heads, n_seqs, (max_len + 127) / 128);
   unsigned long long* tr = trace_alloc_aux(static_cast<int>(grid.x * grid.y * grid.z), 2);
-  launch_pdl(attn_tc3_kernel<D, QLO, QKLO>, grid, dim3(kT3Threads), smem, stream, map_q, map_kv, ctx, cu_seqlens, n_heads,
+  launch_pdl(attn_tc3_kernel<D, QLO, QKLO, NS>, grid, dim3(kT3Threads), smem, stream, map_q, map_kv, ctx, cu_seqlens, n_heads,
              hidden, group_rows, scale_log2, lo_off, tr, lo_rows);
 }
 
@@ -714,7 +717,19 @@ void launch_attention_tc3(const CUtensorMap& map_q, const CUtensorMap& map_kv, h
                           long long group_rows, cudaStream_t stream, long long lo_rows, bool qk_lo) {
   if (n_seqs <= 0 || max_len <= 0 || groups <= 0) return;
   const bool d32 = hidden / n_heads == 32;
-  if (lo_rows && qk_lo) {
+  static const int stages = [] {  // A/B: SP_TC3_STAGES=1|2 forces the K/V ring depth of the QKLO kernel
+    const char* v = getenv("SP_TC3_STAGES");
+    return v == nullptr ? 0 : atoi(v);
+  }();
+  // QKLO at two stages is 99 KiB (two CTAs per SM): above 384 tokens (four query tiles per head) a
+  // one-stage ring keeps three CTAs per SM and one wave
+  const bool one_stage = stages == 1 || (stages == 0 && max_len > kTc3OneStageFrom);
+  if (lo_rows && qk_lo && one_stage) {
+    if (d32) launch_tc3_t<32, true, true, 1>(map_q, map_kv, ctx, lo_off, cu_seqlens, n_seqs, max_len, groups, n_heads,
+                                             hidden, group_rows, lo_rows, stream);
+    else launch_tc3_t<64, true, true, 1>(map_q, map_kv, ctx, lo_off, cu_seqlens, n_seqs, max_len, groups, n_heads,
+                                         hidden, group_rows, lo_rows, stream);
+  } else if (lo_rows && qk_lo) {
     if (d32) launch_tc3_t<32, true, true>(map_q, map_kv, ctx, lo_off, cu_seqlens, n_seqs, max_len, groups, n_heads,
                                           hidden, group_rows, lo_rows, stream);
     else launch_tc3_t<64, true, true>(map_q, map_kv, ctx, lo_off, cu_seqlens, n_seqs, max_len, groups, n_heads, hidden,
